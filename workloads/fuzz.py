@@ -1,0 +1,206 @@
+"""Seeded random MAP generator (test inputs only; no method arithmetic here).
+
+Produces a plain-data AST (tuples) and its MAP text.  The same AST is evaluated
+by the pure-Python brute force (tests/brute.py) while the text goes to the C++
+oracle and to the CUDA path, so a parser bug on either side shows up as a
+disagreement.  Shape limits follow SURVEY.md §4 item 3: blockDim <= 16, trip
+counts <= 4, <= 3 phases, <= 2 arrays, <= 2 blocks.  In the spirit of
+SPEC.md:474-482 (``generate_typable_kernel``): MAPs are data-independent by
+construction (indices and guards use only tid, bid, loop variables, params and
+literals).
+
+AST node shapes
+  num : ("nat", v) | ("var", name) | ("tid",) | ("bid",)
+        | ("bin", op, a, b)   op in + - * / % << >> min max
+  cond: ("true",) | ("false",) | ("rel", op, a, b)   op in = != < <= > >=
+        | ("and", l, r) | ("or", l, r)
+  stmt: ("skip",) | ("sync",) | ("acc", kind, array, idx)   kind in rd wr
+        | ("seq", [stmt...]) | ("if", cond, then, else)
+        | ("forU"|"forS", var, lo, hi, step, body)
+  program: {"params": [names], "arrays": [names], "body": stmt}
+"""
+from __future__ import annotations
+
+import random
+from typing import List
+
+from . import Instance
+
+_ARITH = ["+", "+", "-", "*", "/", "%", "<<", ">>", "min", "max"]
+_RELS = ["=", "!=", "<", "<=", ">", ">="]
+
+
+class _Gen:
+    def __init__(self, seed: int):
+        self.r = random.Random(seed)
+        self.n_loopvars = 0
+        self.syncs_left = 2
+
+    # -- expressions --------------------------------------------------------
+    def leaf(self, scope: List[str], uniform: bool):
+        r = self.r
+        choices = ["nat", "nat"]
+        if not uniform:
+            choices += ["tid", "tid", "bid"]
+        if scope:
+            choices += ["var", "var"]
+        c = r.choice(choices)
+        if c == "nat":
+            return ("nat", r.randint(0, 5))
+        if c == "var":
+            return ("var", r.choice(scope))
+        return (c,)
+
+    def num(self, scope, depth, uniform=False):
+        r = self.r
+        if depth <= 0 or r.random() < 0.35:
+            return self.leaf(scope, uniform)
+        op = r.choice(_ARITH)
+        a = self.num(scope, depth - 1, uniform)
+        if op in ("/", "%"):
+            b = ("nat", r.randint(1, 4))           # never divide by zero
+        elif op in ("<<", ">>"):
+            b = ("nat", r.randint(0, 2))
+        elif op == "*":
+            b = ("nat", r.randint(0, 3)) if r.random() < 0.6 else self.num(scope, depth - 1, uniform)
+        else:
+            b = self.num(scope, depth - 1, uniform)
+        return ("bin", op, a, b)
+
+    def index(self, scope):
+        # fold into a small range so distinct threads collide often
+        e = self.num(scope, 2)
+        return ("bin", "%", e, ("nat", self.r.randint(2, 9)))
+
+    def cond(self, scope, depth=1):
+        r = self.r
+        x = r.random()
+        if depth > 0 and x < 0.2:
+            return (r.choice(["and", "or"]), self.cond(scope, depth - 1), self.cond(scope, depth - 1))
+        if x < 0.25:
+            return (r.choice(["true", "false"]),)
+        return ("rel", r.choice(_RELS), self.num(scope, 1), self.num(scope, 1))
+
+    # -- statements ---------------------------------------------------------
+    def fresh(self):
+        self.n_loopvars += 1
+        return f"x{self.n_loopvars}"
+
+    def bounds(self, scope, uniform):
+        r = self.r
+        lo = ("nat", r.randint(0, 2)) if r.random() < 0.7 else self.leaf(scope, uniform)
+        span = ("nat", r.randint(0, 4)) if r.random() < 0.6 else \
+            ("bin", "%", self.num(scope, 1, uniform), ("nat", r.randint(1, 5)))
+        hi = ("bin", "+", lo, span)
+        step = ("nat", r.choice([1, 1, 1, 2]))
+        return lo, hi, step
+
+    def u(self, scope, arrays, depth):
+        r = self.r
+        x = r.random()
+        if depth <= 0 or x < 0.35:
+            if r.random() < 0.1:
+                return ("skip",)
+            return ("acc", r.choice(["rd", "wr"]), r.choice(arrays), self.index(scope))
+        if x < 0.55:
+            return ("seq", [self.u(scope, arrays, depth - 1) for _ in range(r.randint(2, 3))])
+        if x < 0.75:
+            els = self.u(scope, arrays, depth - 1) if r.random() < 0.7 else ("skip",)
+            return ("if", self.cond(scope), self.u(scope, arrays, depth - 1), els)
+        v = self.fresh()
+        lo, hi, step = self.bounds(scope, uniform=False)
+        return ("forU", v, lo, hi, step, self.u(scope + [v], arrays, depth - 1))
+
+    def p(self, scope, arrays, depth, allow_fors=True):
+        r = self.r
+        items = []
+        for _ in range(r.randint(1, 3)):
+            x = r.random()
+            if x < 0.55 or depth <= 0:
+                items.append(self.u(scope, arrays, 2))
+            elif x < 0.8 and self.syncs_left > 0:
+                self.syncs_left -= 1
+                items.append(("sync",))
+            elif allow_fors:
+                v = self.fresh()
+                lo = ("nat", r.randint(0, 1))
+                hi = ("bin", "+", lo, ("nat", r.randint(0, 2)) if r.random() < 0.7
+                      else self.leaf([s for s in scope if s.startswith("P")], True))
+                body = self.p(scope + [v], arrays, depth - 1, allow_fors=False)
+                body = ("seq", [body, ("sync",)]) if r.random() < 0.8 else body
+                items.append(("forS", v, lo, hi, ("nat", 1), body))
+        if not items:
+            items.append(self.u(scope, arrays, 2))
+        return items[0] if len(items) == 1 else ("seq", items)
+
+
+def random_program(seed: int) -> dict:
+    g = _Gen(seed)
+    r = g.r
+    params = [f"P{i}" for i in range(r.randint(0, 2))]
+    n_arr = r.randint(1, 2)
+    arrays = ["A", "B"][:n_arr]
+    body = g.p(list(params), arrays, depth=2)
+    return {"params": params, "arrays": arrays, "body": body}
+
+
+def random_instance(seed: int) -> tuple[Instance, dict]:
+    """(instance, ast) for fuzz seed ``seed``."""
+    prog = random_program(seed)
+    r = random.Random(seed ^ 0x5EED)
+    block = (r.choice([1, 2, 3, 4, 5, 8, 16]), 1, 1)
+    grid = (r.choice([1, 1, 2]), 1, 1)
+    params = {p: r.randint(0, 4) for p in prog["params"]}
+    return Instance(f"fuzz{seed}", to_text(prog), grid=grid, block=block, params=params), prog
+
+
+# -- printing ---------------------------------------------------------------
+def num_text(e) -> str:
+    k = e[0]
+    if k == "nat":
+        return str(e[1])
+    if k == "var":
+        return e[1]
+    if k in ("tid", "bid"):
+        return k
+    _, op, a, b = e
+    if op in ("min", "max"):
+        return f"{op}({num_text(a)}, {num_text(b)})"
+    return f"({num_text(a)} {op} {num_text(b)})"
+
+
+def cond_text(c) -> str:
+    k = c[0]
+    if k in ("true", "false"):
+        return k
+    if k == "rel":
+        return f"{num_text(c[2])} {c[1]} {num_text(c[3])}"
+    return f"({cond_text(c[1])} {k} {cond_text(c[2])})"
+
+
+def stmt_text(s, multi_array: bool) -> str:
+    k = s[0]
+    if k in ("skip", "sync"):
+        return k
+    if k == "acc":
+        arr = f" {s[2]}" if multi_array else ""
+        return f"{s[1]}{arr}[{num_text(s[3])}]"
+    if k == "seq":
+        return "; ".join(stmt_text(x, multi_array) for x in s[1])
+    if k == "if":
+        return (f"if ({cond_text(s[1])}) {{ {stmt_text(s[2], multi_array)} }} "
+                f"else {{ {stmt_text(s[3], multi_array)} }}")
+    _, v, lo, hi, step, body = s
+    st = "" if step == ("nat", 1) else f" step {num_text(step)}"
+    return f"{k} {v} in {num_text(lo)}..{num_text(hi)}{st} {{ {stmt_text(body, multi_array)} }}"
+
+
+def to_text(prog: dict) -> str:
+    parts = []
+    if prog["params"]:
+        parts.append("params " + ", ".join(prog["params"]) + ";")
+    multi = len(prog["arrays"]) > 1
+    if multi:
+        parts.append("shared " + ", ".join(prog["arrays"]) + ";")
+    parts.append(stmt_text(prog["body"], multi))
+    return "\n".join(parts)
