@@ -1,0 +1,150 @@
+/*
+ * mapcheck.h -- C ABI of the B200-native concrete MAP data-race checker.
+ *
+ * What it computes (arxiv 2203.12878, "BabyCUDA"): a memory access protocol
+ * (MAP; Fig. 2) is instantiated at fixed grid/block
+ * dimensions and parameter values; every access value alpha = i : o[y]
+ * of every thread i in T = {0..blockDim-1} (rule par,
+ * PAPER.md:579-589) is enumerated on the GPU, tagged with its barrier phase
+ * (PAPER.md:179-182), array and block, and the library decides whether two
+ * DISTINCT threads touch the same index of the same array in the same phase of
+ * the same block with at least one write (the data-race definition of
+ * PAPER.md:111-113).  By Theorem 1 the verdict is the
+ * ground truth for a typable kernel at this instantiation.  The reported
+ * witness is canonical: the lexicographic minimum of
+ *   (phase, array, block, index, tid_lo, tid_hi, kind_lo, kind_hi),
+ * tid_lo < tid_hi, rd = 0 < wr = 1 -- independent of launch order and of the
+ * number of GPUs (reading R14).
+ *
+ * MAP text grammar: DESIGN.md §3 (extends SPEC.md:179 with sync/forS, named
+ * arrays, params, `step`, bid, shifts and min/max).
+ *
+ * Conventions
+ *  - Every entry point returns a map_status; out-parameters are written only
+ *    on MAP_OK.  No C++ exception crosses the ABI.
+ *  - map_program is opaque and library-owned (free with map_program_free).
+ *    Distinct programs may be used concurrently from different host threads;
+ *    one program is not re-entrant.
+ *  - Device memory is BORROWED: the caller passes a device scratch buffer of
+ *    at least map_scratch_bytes() bytes (PyTorch allocates it) and a CUDA
+ *    stream; the library never cudaMallocs on the hot path.  All work is
+ *    enqueued on that stream; map_check_races synchronizes it once at the end.
+ *  - There is no CPU fallback: without a usable CUDA device the run entry
+ *    points return MAP_E_CUDA.
+ */
+#ifndef MAPCHECK_H
+#define MAPCHECK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MAP_OK = 0,
+  MAP_E_PARSE = 1,   /* syntax error in the MAP text (diag: "line:col: msg")            */
+  MAP_E_SCOPE = 2,   /* unbound / duplicate / shadowing identifier          */
+  MAP_E_BARRIER = 3, /* sync/forS under if or forU, or forS bounds mention tid/bid       */
+  MAP_E_RANGE = 4,   /* a value may exceed 64 bits, key/witness fields do not fit 64
+                        bits, a loop step may be 0, or too many phases/instances        */
+  MAP_E_ARITH = 5,   /* division or modulo by zero reached at run time                  */
+  MAP_E_CUDA = 6,    /* CUDA error or no device                                          */
+  MAP_E_COMM = 7,    /* reserved for the multi-GPU orchestration (NCCL lives in Python)  */
+  MAP_E_ARG = 8,     /* bad argument: null pointer, missing/unknown parameter, ...       */
+  MAP_E_NOMEM = 9    /* scratch too small for one (phase, block) unit                    */
+} map_status;
+
+typedef struct map_program map_program;
+
+/* Instantiation (PAPER.md:431 T subset of N; here T = {0..prod(block)-1}).
+ * 3-D dims are flattened: tid = tz*bx*by + ty*bx + tx, same for bid. */
+typedef struct {
+  uint32_t grid[3];
+  uint32_t block[3];
+  uint32_t n_params;
+  const char *const *param_names;   /* n_params NUL-terminated names        */
+  const uint64_t *param_values;     /* n_params naturals     */
+} map_instance;
+
+/* Execution resources borrowed from the caller. */
+typedef struct {
+  int device;                 /* CUDA device ordinal                                  */
+  void *stream;               /* cudaStream_t (0 = legacy default stream)             */
+  void *scratch;              /* device buffer, >= map_scratch_bytes(p, chunk)        */
+  size_t scratch_bytes;
+  uint64_t chunk_max_accesses;/* accesses per chunk (0 = derive from scratch_bytes)  */
+} map_exec;
+
+typedef struct {
+  int32_t verdict;            /* 0 = DRF, 1 = RACY                                    */
+  int32_t n_chunks;           /* chunks the run was split into                       */
+  uint64_t n_accesses;        /* accesses enumerated, counted with multiplicity      */
+  uint64_t racy_segments;     /* (phase, array, block, index) cells holding a race   */
+  float device_ms;            /* device time of the whole run (CUDA events)          */
+  uint32_t gpu_launches;      /* kernels launched by this call                       */
+} map_result;
+
+typedef struct {
+  uint32_t phase, array, block;
+  uint64_t index;
+  uint32_t tid_lo, tid_hi;
+  uint8_t kind_lo, kind_hi;   /* 0 = rd, 1 = wr                                       */
+  const char *array_name;     /* valid until map_program_free                        */
+} map_witness;
+
+/* Static facts of a compiled program (for sizing and reporting). */
+typedef struct {
+  uint32_t n_phases;          /* barrier phases (syncs executed + 1)                  */
+  uint32_t n_arrays;
+  uint32_t n_instances;       /* (u-fragment, forS iteration) instances              */
+  uint32_t n_groups;          /* (instance, loop nest) groups = generate segments    */
+  uint64_t max_accesses;      /* upper bound on accesses (bounding boxes)            */
+  uint64_t max_unit_accesses; /* largest (phase, block) unit bound                   */
+  uint32_t u32_mode;          /* 1 if every value provably fits 32 bits              */
+  uint32_t bytecode_ops;
+} map_info;
+
+/* Parse, resolve, interval-analyse and lower the MAP `src` (len bytes, need not
+ * be NUL-terminated) at the instantiation `inst`.  On error a diagnostic
+ * "line:col: message" is written to diag (if non-null). */
+map_status map_compile(const char *src, size_t len, const map_instance *inst, map_program **out,
+                       char *diag, size_t diag_cap);
+
+map_status map_info_get(const map_program *p, map_info *out);
+
+/* Device scratch needed to process chunks of up to chunk_max_accesses
+ * accesses (0 = the largest (phase, block) unit of this program). */
+size_t map_scratch_bytes(const map_program *p, uint64_t chunk_max_accesses);
+
+/* Run the whole pipeline (generate -> radix sort -> detect per chunk) on one
+ * GPU; blocking.  Writes verdict, counts and timing to *out. */
+map_status map_check_races(map_program *p, const map_exec *ex, map_result *out);
+
+/* Canonical witness of the last racy map_check_races; MAP_E_ARG if it was DRF. */
+map_status map_witness_get(const map_program *p, map_witness *out);
+
+void map_program_free(map_program *p);
+const char *map_status_str(map_status s);
+
+/* ---- stage API (multi-GPU orchestration from Python; NCCL via torch) -----
+ * Shard `rank` of `world` owns the access keys whose sort field hashes to it
+ * (SURVEY.md §8e).  map_generate_bucketed enumerates this rank's slice of the
+ * tuple space (tuples t with t % world == rank) for chunk `chunk` and writes
+ * keys grouped by destination rank into keys_out (capacity = the chunk's
+ * bound), counts_out[world] on the HOST.  Keys use the chunk layout
+ * (map_chunk_count / map_key_layout). */
+map_status map_chunk_count(const map_program *p, uint64_t chunk_max_accesses, uint32_t *n_chunks);
+map_status map_generate_bucketed(map_program *p, const map_exec *ex, uint32_t rank, uint32_t world,
+                                 uint32_t chunk, void *keys_out, uint64_t *counts_out);
+/* Sort + detect n device-resident keys of chunk `chunk`; packed witness of the
+ * chunk (UINT64_MAX = DRF) and its racy-segment count are written to the HOST. */
+map_status map_sort_detect(map_program *p, const map_exec *ex, uint32_t chunk, void *keys, uint64_t n,
+                           uint64_t *packed_witness, uint64_t *racy_segments);
+map_status map_unpack_witness(const map_program *p, uint32_t chunk, uint64_t packed, map_witness *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPCHECK_H */

@@ -1,0 +1,239 @@
+"""paper_2203_12878_b200 -- B200-native concrete MAP data-race checker.
+
+Thin ctypes binding of the C ABI in include/mapcheck.h (argument marshalling
+only: every step of the hot path runs in the sm_100a kernels of
+libmapcheck.so).  PyTorch supplies device memory (the scratch buffer) and the
+CUDA stream.  There is no CPU fallback: if the library is missing, importing
+this package raises; if there is no GPU, ``check_races`` raises MapError
+(MAP_E_CUDA).
+
+Paper: arxiv 2203.12878 -- a MAP instantiated at fixed
+grid/block dims and parameters is enumerated exhaustively; two distinct threads
+touching one index of one array in one barrier phase, one of them writing, is a
+data race; by Theorem 1 the verdict is
+the ground truth for a typable kernel at that instantiation.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Dict, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmapcheck.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2203_12878_b200._build` "
+        "(nvcc, sm_100a).  There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = {
+    0: "MAP_OK", 1: "MAP_E_PARSE", 2: "MAP_E_SCOPE", 3: "MAP_E_BARRIER", 4: "MAP_E_RANGE",
+    5: "MAP_E_ARITH", 6: "MAP_E_CUDA", 7: "MAP_E_COMM", 8: "MAP_E_ARG", 9: "MAP_E_NOMEM",
+}
+
+EXPORTS = (
+    "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
+    "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
+    "map_sort_detect", "map_unpack_witness",
+)
+
+
+class _Instance(ctypes.Structure):
+    _fields_ = [("grid", ctypes.c_uint32 * 3), ("block", ctypes.c_uint32 * 3), ("n_params", ctypes.c_uint32),
+                ("param_names", ctypes.POINTER(ctypes.c_char_p)), ("param_values", ctypes.POINTER(ctypes.c_uint64))]
+
+
+class _Exec(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("scratch", ctypes.c_void_p),
+                ("scratch_bytes", ctypes.c_size_t), ("chunk_max_accesses", ctypes.c_uint64)]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("verdict", ctypes.c_int32), ("n_chunks", ctypes.c_int32), ("n_accesses", ctypes.c_uint64),
+                ("racy_segments", ctypes.c_uint64), ("device_ms", ctypes.c_float), ("gpu_launches", ctypes.c_uint32)]
+
+
+class _Witness(ctypes.Structure):
+    _fields_ = [("phase", ctypes.c_uint32), ("array", ctypes.c_uint32), ("block", ctypes.c_uint32),
+                ("index", ctypes.c_uint64), ("tid_lo", ctypes.c_uint32), ("tid_hi", ctypes.c_uint32),
+                ("kind_lo", ctypes.c_uint8), ("kind_hi", ctypes.c_uint8), ("array_name", ctypes.c_char_p)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n_phases", ctypes.c_uint32), ("n_arrays", ctypes.c_uint32), ("n_instances", ctypes.c_uint32),
+                ("n_groups", ctypes.c_uint32), ("max_accesses", ctypes.c_uint64),
+                ("max_unit_accesses", ctypes.c_uint64), ("u32_mode", ctypes.c_uint32),
+                ("bytecode_ops", ctypes.c_uint32)]
+
+
+_P = ctypes.c_void_p
+_lib.map_compile.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_Instance), ctypes.POINTER(_P),
+                             ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_compile.restype = ctypes.c_int
+_lib.map_info_get.argtypes = [_P, ctypes.POINTER(_Info)]
+_lib.map_info_get.restype = ctypes.c_int
+_lib.map_scratch_bytes.argtypes = [_P, ctypes.c_uint64]
+_lib.map_scratch_bytes.restype = ctypes.c_size_t
+_lib.map_check_races.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.POINTER(_Result)]
+_lib.map_check_races.restype = ctypes.c_int
+_lib.map_witness_get.argtypes = [_P, ctypes.POINTER(_Witness)]
+_lib.map_witness_get.restype = ctypes.c_int
+_lib.map_program_free.argtypes = [_P]
+_lib.map_program_free.restype = None
+_lib.map_status_str.argtypes = [ctypes.c_int]
+_lib.map_status_str.restype = ctypes.c_char_p
+_lib.map_last_error.argtypes = [_P]
+_lib.map_last_error.restype = ctypes.c_char_p
+_lib.map_chunk_count.argtypes = [_P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32)]
+_lib.map_chunk_count.restype = ctypes.c_int
+_lib.mapc_test_fastdiv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+_lib.mapc_test_fastdiv.restype = ctypes.c_uint32
+
+
+class MapError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+@dataclass
+class Witness:
+    phase: int
+    array: int
+    block: int
+    index: int
+    tid_lo: int
+    tid_hi: int
+    kind_lo: int
+    kind_hi: int
+    array_name: str
+
+    def as_tuple(self):
+        return (self.phase, self.array, self.block, self.index, self.tid_lo, self.tid_hi, self.kind_lo, self.kind_hi)
+
+
+@dataclass
+class Result:
+    verdict: int                  # 0 DRF, 1 racy
+    n_accesses: int
+    racy_segments: int
+    n_chunks: int
+    device_ms: float
+    gpu_launches: int
+    witness: Optional[Witness] = None
+
+    @property
+    def racy(self) -> bool:
+        return self.verdict == 1
+
+
+@dataclass
+class Info:
+    n_phases: int
+    n_arrays: int
+    n_instances: int
+    n_groups: int
+    max_accesses: int
+    max_unit_accesses: int
+    u32_mode: bool
+    bytecode_ops: int
+
+
+def _dims(d: Sequence[int]):
+    d = tuple(int(x) for x in d) + (1, 1, 1)
+    return (ctypes.c_uint32 * 3)(*d[:3])
+
+
+class MapProgram:
+    """A MAP compiled at one instantiation (map_compile)."""
+
+    def __init__(self, src: str, grid: Sequence[int] = (1, 1, 1), block: Sequence[int] = (1, 1, 1),
+                 params: Optional[Dict[str, int]] = None):
+        params = params or {}
+        names = list(params)
+        self._keep = [n.encode() for n in names]
+        inst = _Instance()
+        inst.grid = _dims(grid)
+        inst.block = _dims(block)
+        inst.n_params = len(names)
+        inst.param_names = (ctypes.c_char_p * max(1, len(names)))(*self._keep)
+        inst.param_values = (ctypes.c_uint64 * max(1, len(names)))(*[int(params[n]) for n in names])
+        h = _P()
+        diag = ctypes.create_string_buffer(1024)
+        raw = src.encode()
+        st = _lib.map_compile(raw, len(raw), ctypes.byref(inst), ctypes.byref(h), diag, 1024)
+        if st != 0:
+            raise MapError(st, diag.value.decode(errors="replace"))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.map_program_free(h)
+            self._h = None
+
+    @property
+    def info(self) -> Info:
+        i = _Info()
+        _lib.map_info_get(self._h, ctypes.byref(i))
+        return Info(i.n_phases, i.n_arrays, i.n_instances, i.n_groups, i.max_accesses, i.max_unit_accesses,
+                    bool(i.u32_mode), i.bytecode_ops)
+
+    def scratch_bytes(self, chunk_max_accesses: int = 0) -> int:
+        n = _lib.map_scratch_bytes(self._h, int(chunk_max_accesses))
+        if n == 0:
+            raise MapError(9, _lib.map_last_error(self._h).decode())
+        return n
+
+    def n_chunks(self, chunk_max_accesses: int = 0) -> int:
+        c = ctypes.c_uint32()
+        st = _lib.map_chunk_count(self._h, int(chunk_max_accesses), ctypes.byref(c))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        return c.value
+
+    def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None) -> Result:
+        """Run generate -> sort -> detect on one GPU (blocking).
+
+        scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
+        stream: a torch.cuda.Stream (default: the current stream)."""
+        import torch
+        if not torch.cuda.is_available():
+            raise MapError(6, "no CUDA device (there is no CPU fallback)")
+        dev = torch.cuda.current_device() if device is None else int(device)
+        need = self.scratch_bytes(chunk_max_accesses)
+        if scratch is None:
+            scratch = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
+                   scratch.numel() * scratch.element_size(), int(chunk_max_accesses))
+        r = _Result()
+        st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        res = Result(r.verdict, r.n_accesses, r.racy_segments, r.n_chunks, r.device_ms, r.gpu_launches)
+        if r.verdict:
+            w = _Witness()
+            if _lib.map_witness_get(self._h, ctypes.byref(w)) == 0:
+                res.witness = Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
+                                      w.array_name.decode())
+        return res
+
+
+def check(src: str, grid=(1, 1, 1), block=(1, 1, 1), params=None, chunk_max_accesses: int = 0, **kw) -> Result:
+    """Compile and check a MAP in one call."""
+    return MapProgram(src, grid, block, params).check_races(chunk_max_accesses=chunk_max_accesses, **kw)
+
+
+def status_str(status: int) -> str:
+    return _lib.map_status_str(status).decode()
+
+
+def fastdiv_selftest(n: int, d: int) -> int:
+    """Host copy of the kernels' invariant-divisor quotient (for CPU tests)."""
+    return _lib.mapc_test_fastdiv(n, d)

@@ -1,0 +1,566 @@
+// mapcheck.cpp -- C ABI (include/mapcheck.h): compile, plan, launch, decode.
+//
+// Host orchestration of the hot path on one GPU:
+//   per chunk (a range of barrier phases, or of blocks of one phase):
+//     upload bytecode (__constant__) + segment table
+//     k_chunk_init -> k_generate -> k_hist -> k_digit_scan -> k_onesweep x P
+//     -> k_detect -> k_detect_fixup -> k_chunk_finish
+//   all on the caller's stream; one synchronisation at the very end.
+// Chunks are exact units because races are intra-(phase, block)
+// (R10): the canonical witness is the
+// lexicographic minimum of the per-chunk witnesses, taken on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../../include/mapcheck.h"
+#include "../compiler/compiler.h"
+#include "../devabi.h"
+
+extern "C" {
+cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cudaStream_t s);
+cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tuples,
+                                 const MapcLayout* lay, int u32_mode, unsigned long long* keys, MapcCtrl* ctrl,
+                                 int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_hist(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t n_passes,
+                             unsigned long long max_keys, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_digit_scan(MapcCtrl* ctrl, uint32_t n_passes, cudaStream_t s);
+unsigned long long mapc_sort_tile();
+cudaError_t mapc_launch_onesweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
+                                 unsigned long long* lookback, uint32_t pass, uint32_t shift,
+                                 unsigned long long epoch, unsigned long long max_keys, int n_sms, cudaStream_t s);
+unsigned long long mapc_detect_tile();
+cudaError_t mapc_launch_chunk_init(MapcCtrl* ctrl, cudaStream_t s);
+cudaError_t mapc_launch_detect(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
+                               uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
+                               MapcSegState* last_frag, unsigned long long max_keys, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_chunk_finish(const MapcCtrl* ctrl, MapcChunkResult* out, cudaStream_t s);
+}
+
+namespace {
+
+using mapc::bits_for;
+
+struct Chunk {
+  uint32_t phase_lo = 0, phase_hi = 0;      // inclusive range of phases covered
+  uint64_t b_lo = 0, b_hi = 0;              // [b_lo, b_hi)
+  MapcLayout lay{};
+  std::vector<MapcSeg> segs;
+  std::vector<MapcOp> ops;
+  uint64_t bound = 0;
+  uint64_t total_tuples = 0;
+  size_t stage_ops = 0, stage_segs = 0;     // offsets in the pinned staging buffer
+};
+
+struct Plan {
+  uint64_t cap = 0;                         // max keys of any chunk
+  std::vector<Chunk> chunks;
+  size_t max_segs = 0;
+  // scratch offsets
+  size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0;
+  size_t lb_bytes = 0, total = 0, stage_bytes = 0;
+};
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct map_program {
+  mapc::Compiled C;
+  uint64_t plan_for = ~0ull;
+  Plan plan;
+  bool have_witness = false;
+  map_witness wit{};
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* last_lookback = nullptr;
+  uint64_t epoch = 0;
+  int device = -1;
+  std::string last_error;
+};
+
+namespace {
+
+struct PhaseInfo {
+  uint32_t phase;
+  std::vector<size_t> inst;
+  uint64_t per_block = 0;
+  uint64_t ilo = ~0ull, ihi = 0;
+  size_t ops = 0;
+};
+
+bool layout_fits(const mapc::Compiled& C, uint32_t ph_span, uint64_t nb, uint64_t ilo, uint64_t ihi, MapcLayout* out) {
+  MapcLayout L{};
+  L.w_phase = bits_for(ph_span);
+  L.w_array = bits_for(C.ast.arrays.size() - 1);
+  L.w_block = bits_for(nb - 1);
+  L.w_index = ilo <= ihi ? bits_for(ihi - ilo) : 0;
+  L.w_tid = C.w_tid;
+  L.pay_bits = C.w_tid + 1;
+  L.sort_bits = L.w_phase + L.w_array + L.w_block + L.w_index;
+  L.n_passes = (L.sort_bits + 7) / 8;
+  L.idx_lo = ilo <= ihi ? ilo : 0;
+  if (L.sort_bits + L.pay_bits > 64) return false;
+  if (L.sort_bits + 2 * L.w_tid + 2 > 64) return false;
+  if (out) *out = L;
+  return true;
+}
+
+MapcOp lower_op_for_mode(MapcOp op, bool u32) {
+  const uint32_t code = op.code & MAPC_CODE_MASK;
+  if (u32 && (code == VM_DIV || code == VM_MOD) && (op.code & MAPC_B_IMM) && op.imm != 0 && op.imm < (1ull << 32)) {
+    MapcFastDiv f = mapc::make_fastdiv((uint32_t)op.imm);
+    if (!f.pow2) {
+      MapcOp r = op;
+      r.code = (uint8_t)((code == VM_DIV ? VM_DIVM : VM_MODM) | (op.code & MAPC_A_IMM));
+      r.imm = ((uint64_t)f.d << 32) | f.m;
+      r.aux = f.s;
+      return r;
+    }
+  }
+  return op;
+}
+
+void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_t i0, size_t i1, uint64_t b_lo,
+                uint64_t b_hi, const MapcLayout& L, Chunk* out) {
+  Chunk ch;
+  ch.phase_lo = ph[i0].phase;
+  ch.phase_hi = ph[i1 - 1].phase;
+  ch.b_lo = b_lo;
+  ch.b_hi = b_hi;
+  ch.lay = L;
+  const uint64_t B = C.n_threads;
+  for (size_t i = i0; i < i1; ++i) {
+    for (size_t ii : ph[i].inst) {
+      const mapc::InstanceInfo& in = C.inst[ii];
+      for (const mapc::GroupProg& g : in.groups) {
+        const uint32_t pb = (uint32_t)ch.ops.size();
+        for (const MapcOp& op : g.ops) ch.ops.push_back(lower_op_for_mode(op, C.u32_mode));
+        const uint32_t pe = (uint32_t)ch.ops.size();
+        const uint64_t tpb = g.tuples_per_block;
+        const uint64_t per_seg = std::max<uint64_t>(1, 0xFFFFFFFFull / tpb);
+        for (uint64_t b = b_lo; b < b_hi; b += per_seg) {
+          const uint64_t nb = std::min(per_seg, b_hi - b);
+          MapcSeg s{};
+          s.tuple_begin = ch.total_tuples;
+          s.n_tuples = nb * tpb;
+          s.key_hi = (uint64_t)(in.phase - ch.phase_lo) << (L.w_array + L.w_block + L.w_index);
+          s.prog_begin = pb;
+          s.prog_end = pe;
+          s.n_levels = g.n_levels;
+          s.b0 = (uint32_t)b;
+          s.lb0 = (uint32_t)(b - b_lo);
+          s.n_emits = g.n_emits;
+          s.dense = g.dense ? 1 : 0;
+          for (uint32_t l = 0; l < g.n_levels; ++l) s.trip_div[l] = mapc::make_fastdiv((uint32_t)g.trips[l]);
+          s.tid_div = mapc::make_fastdiv((uint32_t)B);
+          ch.total_tuples += s.n_tuples;
+          ch.bound += s.n_tuples * g.n_emits;
+          ch.segs.push_back(s);
+        }
+      }
+    }
+  }
+  *out = std::move(ch);
+}
+
+// Greedy plan: consecutive phases while the bound, the layout and the
+// constant-memory budget allow; an oversized phase is split by block ranges.
+map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string* why) {
+  std::vector<PhaseInfo> ph;
+  for (size_t i = 0; i < C.inst.size(); ++i) {
+    const mapc::InstanceInfo& in = C.inst[i];
+    if (ph.empty() || ph.back().phase != in.phase) {
+      ph.emplace_back();
+      ph.back().phase = in.phase;
+    }
+    PhaseInfo& p = ph.back();
+    p.inst.push_back(i);
+    p.per_block += in.bound_per_block;
+    for (auto& g : in.groups) {
+      if (g.has_emit) {
+        p.ilo = std::min(p.ilo, g.index.lo);
+        p.ihi = std::max(p.ihi, g.index.hi);
+      }
+      p.ops += g.ops.size();
+    }
+  }
+  Plan out;
+  const uint64_t G = C.n_blocks;
+  size_t i = 0;
+  while (i < ph.size()) {
+    size_t j = i;
+    uint64_t acc = 0, ilo = ~0ull, ihi = 0;
+    size_t ops = 0;
+    MapcLayout L{}, Lok{};
+    while (j < ph.size()) {
+      const unsigned __int128 nb = (unsigned __int128)ph[j].per_block * G;
+      if ((unsigned __int128)acc + nb > cap) break;
+      const uint64_t nlo = std::min(ilo, ph[j].ilo), nhi = std::max(ihi, ph[j].ihi);
+      if (!layout_fits(C, ph[j].phase - ph[i].phase, G, nlo, nhi, &L)) break;
+      if (ops + ph[j].ops > MAPC_MAX_OPS) break;
+      acc += (uint64_t)nb;
+      ilo = nlo; ihi = nhi; ops += ph[j].ops;
+      Lok = L;
+      ++j;
+    }
+    if (j > i) {
+      out.chunks.emplace_back();
+      emit_chunk(C, ph, i, j, 0, G, Lok, &out.chunks.back());
+      i = j;
+      continue;
+    }
+    // one phase does not fit whole: split its blocks
+    if (ph[i].ops > MAPC_MAX_OPS) { *why = "one phase needs more bytecode than __constant__ holds"; return MAP_E_RANGE; }
+    if (ph[i].per_block > cap) { *why = "one (phase, block) unit exceeds the chunk capacity"; return MAP_E_NOMEM; }
+    uint64_t nb = std::max<uint64_t>(1, cap / std::max<uint64_t>(ph[i].per_block, 1));
+    while (nb > 1 && !layout_fits(C, 0, nb, ph[i].ilo, ph[i].ihi, nullptr)) nb /= 2;
+    if (!layout_fits(C, 0, nb, ph[i].ilo, ph[i].ihi, &L)) {
+      *why = "the (phase, array, block, index, tid) key of one unit exceeds 64 bits";
+      return MAP_E_RANGE;
+    }
+    for (uint64_t b = 0; b < G; b += nb) {
+      const uint64_t be = std::min(G, b + nb);
+      MapcLayout Lb;
+      layout_fits(C, 0, be - b, ph[i].ilo, ph[i].ihi, &Lb);
+      out.chunks.emplace_back();
+      emit_chunk(C, ph, i, i + 1, b, be, Lb, &out.chunks.back());
+    }
+    ++i;
+  }
+  // capacities and scratch layout
+  uint64_t kcap = 1;
+  size_t stage = 0;
+  for (auto& ch : out.chunks) {
+    kcap = std::max(kcap, ch.bound);
+    out.max_segs = std::max(out.max_segs, ch.segs.size());
+    ch.stage_ops = stage;
+    stage += align_up(std::max<size_t>(1, ch.ops.size()) * sizeof(MapcOp), 64);
+    ch.stage_segs = stage;
+    stage += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg), 64);
+  }
+  for (auto& ch : out.chunks) ch.lay.cap = kcap;
+  out.cap = kcap;
+  const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
+  const uint64_t det_tiles = (kcap + mapc_detect_tile() - 1) / mapc_detect_tile();
+  size_t off = 0;
+  out.off_a = off; off += align_up(kcap * 8);
+  out.off_b = off; off += align_up(kcap * 8);
+  out.lb_bytes = sort_tiles * MAPC_RADIX * 8;
+  out.off_lb = off; off += align_up(out.lb_bytes);
+  out.off_ff = off; off += align_up(det_tiles * sizeof(MapcSegState));
+  out.off_lf = off; off += align_up(det_tiles * sizeof(MapcSegState));
+  out.off_segs = off; off += align_up(std::max<size_t>(1, out.max_segs) * sizeof(MapcSeg));
+  out.off_ctrl = off; off += align_up(sizeof(MapcCtrl));
+  out.off_res = off; off += align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult));
+  out.total = off;
+  out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
+  *P = std::move(out);
+  return MAP_OK;
+}
+
+void put_diag(const std::string& d, char* diag, size_t cap) {
+  if (!diag || !cap) return;
+  size_t n = std::min(cap - 1, d.size());
+  std::memcpy(diag, d.data(), n);
+  diag[n] = 0;
+}
+
+map_status ensure_plan(map_program* p, uint64_t cap) {
+  if (p->plan_for == cap) return MAP_OK;
+  Plan P;
+  map_status st = make_plan(p->C, cap, &P, &p->last_error);
+  if (st != MAP_OK) return st;
+  p->plan = std::move(P);
+  p->plan_for = cap;
+  return MAP_OK;
+}
+
+uint64_t default_cap(const map_program* p) {
+  // default chunk: up to 2^30 keys (16 GiB of ping-pong buffers), never less
+  // than the largest single (phase, block) unit
+  const uint64_t want = std::min<uint64_t>(p->C.max_accesses, 1ull << 30);
+  return std::max<uint64_t>({want, p->C.max_unit, 1});
+}
+
+#define CK(expr)                                           \
+  do {                                                     \
+    cudaError_t e_ = (expr);                               \
+    if (e_ != cudaSuccess) {                               \
+      p->last_error = std::string(#expr) + ": " + cudaGetErrorString(e_); \
+      return MAP_E_CUDA;                                   \
+    }                                                      \
+  } while (0)
+
+void decode(const mapc::Compiled& C, const Chunk& ch, uint64_t w, map_witness* out) {
+  const MapcLayout& L = ch.lay;
+  const uint32_t wt = L.w_tid;
+  const uint64_t tm = wt ? ((1ull << wt) - 1) : 0;
+  const uint64_t sf = (2 * wt + 2) >= 64 ? 0 : (w >> (2 * wt + 2));
+  out->tid_lo = (uint32_t)((w >> (wt + 2)) & tm);
+  out->tid_hi = (uint32_t)((w >> 2) & tm);
+  out->kind_lo = (uint8_t)((w >> 1) & 1);
+  out->kind_hi = (uint8_t)(w & 1);
+  auto field = [](uint64_t v, uint32_t lo, uint32_t bits) -> uint64_t {
+    if (bits == 0) return 0;
+    return (v >> lo) & ((bits >= 64) ? ~0ull : ((1ull << bits) - 1));
+  };
+  out->index = L.idx_lo + field(sf, 0, L.w_index);
+  out->block = (uint32_t)(ch.b_lo + field(sf, L.w_index, L.w_block));
+  out->array = (uint32_t)field(sf, L.w_index + L.w_block, L.w_array);
+  out->phase = ch.phase_lo + (uint32_t)field(sf, L.w_index + L.w_block + L.w_array, L.w_phase);
+  out->array_name = C.ast.arrays[out->array].c_str();
+}
+
+bool wit_less(const map_witness& a, const map_witness& b) {
+  auto ta = std::make_tuple(a.phase, a.array, a.block, a.index, a.tid_lo, a.tid_hi, a.kind_lo, a.kind_hi);
+  auto tb = std::make_tuple(b.phase, b.array, b.block, b.index, b.tid_lo, b.tid_hi, b.kind_lo, b.kind_hi);
+  return ta < tb;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* map_status_str(map_status s) {
+  switch (s) {
+    case MAP_OK: return "ok";
+    case MAP_E_PARSE: return "parse error";
+    case MAP_E_SCOPE: return "scope error";
+    case MAP_E_BARRIER: return "barrier placement error";
+    case MAP_E_RANGE: return "range error";
+    case MAP_E_ARITH: return "division by zero";
+    case MAP_E_CUDA: return "CUDA error";
+    case MAP_E_COMM: return "communication error";
+    case MAP_E_ARG: return "bad argument";
+    case MAP_E_NOMEM: return "scratch too small";
+  }
+  return "unknown status";
+}
+
+map_status map_compile(const char* src, size_t len, const map_instance* inst, map_program** out, char* diag,
+                       size_t diag_cap) {
+  if (!src || !inst || !out) return MAP_E_ARG;
+  if (inst->n_params && (!inst->param_names || !inst->param_values)) return MAP_E_ARG;
+  try {
+    std::vector<std::string> names;
+    std::vector<uint64_t> values;
+    for (uint32_t i = 0; i < inst->n_params; ++i) {
+      if (!inst->param_names[i]) return MAP_E_ARG;
+      names.emplace_back(inst->param_names[i]);
+      values.push_back(inst->param_values[i]);
+    }
+    std::unique_ptr<map_program> p(new map_program());
+    p->C = mapc::compile_map(std::string(src, len), inst->grid, inst->block, names, values);
+    *out = p.release();
+    put_diag("", diag, diag_cap);
+    return MAP_OK;
+  } catch (const mapc::CompileError& e) {
+    put_diag(e.msg, diag, diag_cap);
+    return (map_status)e.status;
+  } catch (const std::bad_alloc&) {
+    put_diag("out of host memory", diag, diag_cap);
+    return MAP_E_NOMEM;
+  } catch (...) {
+    put_diag("internal error", diag, diag_cap);
+    return MAP_E_ARG;
+  }
+}
+
+map_status map_info_get(const map_program* p, map_info* out) {
+  if (!p || !out) return MAP_E_ARG;
+  out->n_phases = p->C.n_phases;
+  out->n_arrays = (uint32_t)p->C.ast.arrays.size();
+  out->n_instances = (uint32_t)p->C.inst.size();
+  out->n_groups = p->C.n_groups;
+  out->max_accesses = p->C.max_accesses;
+  out->max_unit_accesses = p->C.max_unit;
+  out->u32_mode = p->C.u32_mode ? 1 : 0;
+  out->bytecode_ops = p->C.total_ops;
+  return MAP_OK;
+}
+
+size_t map_scratch_bytes(const map_program* cp, uint64_t chunk_max_accesses) {
+  if (!cp) return 0;
+  map_program* p = const_cast<map_program*>(cp);
+  const uint64_t cap = chunk_max_accesses ? chunk_max_accesses : default_cap(p);
+  if (ensure_plan(p, cap) != MAP_OK) return 0;
+  return p->plan.total;
+}
+
+map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) {
+  if (!p || !ex || !out) return MAP_E_ARG;
+  p->have_witness = false;
+  const uint64_t cap = ex->chunk_max_accesses ? ex->chunk_max_accesses : default_cap(p);
+  map_status st = ensure_plan(p, cap);
+  if (st != MAP_OK) return st;
+  Plan& P = p->plan;
+  if (!ex->scratch || ex->scratch_bytes < P.total) {
+    p->last_error = "scratch too small: need " + std::to_string(P.total) + " bytes";
+    return MAP_E_NOMEM;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    p->last_error = "no CUDA device";
+    return MAP_E_CUDA;
+  }
+  CK(cudaSetDevice(ex->device));
+  int n_sms = 0;
+  CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, ex->device));
+  cudaStream_t s = (cudaStream_t)ex->stream;
+  if (p->pinned_bytes < P.stage_bytes) {
+    if (p->pinned) cudaFreeHost(p->pinned);
+    p->pinned = nullptr;
+    p->pinned_bytes = 0;
+    CK(cudaMallocHost(&p->pinned, P.stage_bytes));
+    p->pinned_bytes = P.stage_bytes;
+  }
+  unsigned char* stage = (unsigned char*)p->pinned;
+  for (auto& ch : P.chunks) {
+    if (!ch.ops.empty()) std::memcpy(stage + ch.stage_ops, ch.ops.data(), ch.ops.size() * sizeof(MapcOp));
+    if (!ch.segs.empty()) std::memcpy(stage + ch.stage_segs, ch.segs.data(), ch.segs.size() * sizeof(MapcSeg));
+  }
+  MapcChunkResult* host_res = (MapcChunkResult*)(stage + P.stage_bytes -
+                                                 align_up(std::max<size_t>(1, P.chunks.size()) * sizeof(MapcChunkResult), 64));
+  unsigned char* base = (unsigned char*)ex->scratch;
+  auto* bufA = (unsigned long long*)(base + P.off_a);
+  auto* bufB = (unsigned long long*)(base + P.off_b);
+  auto* lookback = (unsigned long long*)(base + P.off_lb);
+  auto* ff = (MapcSegState*)(base + P.off_ff);
+  auto* lf = (MapcSegState*)(base + P.off_lf);
+  auto* segs = (MapcSeg*)(base + P.off_segs);
+  auto* ctrl = (MapcCtrl*)(base + P.off_ctrl);
+  auto* res = (MapcChunkResult*)(base + P.off_res);
+
+  uint32_t passes_total = 0;
+  for (auto& ch : P.chunks) passes_total += ch.lay.n_passes;
+  if (p->last_lookback != (void*)lookback || p->device != ex->device || p->epoch + passes_total >= 0xFFFF) {
+    CK(cudaMemsetAsync(lookback, 0, P.lb_bytes, s));
+    p->epoch = 0;
+    p->last_lookback = lookback;
+    p->device = ex->device;
+  }
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  uint32_t launches = 0;
+  for (size_t c = 0; c < P.chunks.size(); ++c) {
+    const Chunk& ch = P.chunks[c];
+    const MapcLayout& L = ch.lay;
+    CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
+    CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, s));
+    CK(mapc_launch_chunk_init(ctrl, s));
+    ++launches;
+    if (ch.total_tuples) {
+      CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tuples, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                              n_sms, s));
+      ++launches;
+    }
+    if (L.n_passes) {
+      CK(mapc_launch_hist(bufA, ctrl, L.pay_bits, L.n_passes, ch.bound, n_sms, s));
+      ++launches;
+    }
+    CK(mapc_launch_digit_scan(ctrl, L.n_passes, s));
+    ++launches;
+    for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
+      ++p->epoch;
+      CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.pay_bits + 8 * pass, p->epoch, ch.bound, n_sms, s));
+      ++launches;
+    }
+    CK(mapc_launch_detect(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.w_tid, ff, lf, ch.bound, n_sms, s));
+    launches += 2;
+    CK(mapc_launch_chunk_finish(ctrl, res + c, s));
+    ++launches;
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaMemcpyAsync(host_res, res, P.chunks.size() * sizeof(MapcChunkResult), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+
+  map_result r{};
+  r.n_chunks = (int32_t)P.chunks.size();
+  r.device_ms = ms;
+  r.gpu_launches = launches;
+  uint32_t err = 0;
+  bool have = false;
+  map_witness best{};
+  for (size_t c = 0; c < P.chunks.size(); ++c) {
+    const MapcChunkResult& cr = host_res[c];
+    r.n_accesses += cr.n;
+    r.racy_segments += cr.racy;
+    err |= cr.err;
+    if (cr.witness != ~0ull) {
+      map_witness w{};
+      decode(p->C, P.chunks[c], cr.witness, &w);
+      if (!have || wit_less(w, best)) best = w;
+      have = true;
+    }
+  }
+  if (err & MAPC_ERR_DIV0) {
+    p->last_error = "division or modulo by zero on a reached path";
+    return MAP_E_ARITH;
+  }
+  if (err) {
+    p->last_error = "internal consistency check failed (err bits " + std::to_string(err) + ")";
+    return MAP_E_RANGE;
+  }
+  r.verdict = have ? 1 : 0;
+  p->have_witness = have;
+  p->wit = best;
+  *out = r;
+  return MAP_OK;
+}
+
+map_status map_witness_get(const map_program* p, map_witness* out) {
+  if (!p || !out) return MAP_E_ARG;
+  if (!p->have_witness) return MAP_E_ARG;
+  *out = p->wit;
+  return MAP_OK;
+}
+
+void map_program_free(map_program* p) {
+  if (!p) return;
+  if (p->pinned) cudaFreeHost(p->pinned);
+  delete p;
+}
+
+// ---- stage API: implemented in a later milestone ----
+map_status map_chunk_count(const map_program* cp, uint64_t chunk_max_accesses, uint32_t* n_chunks) {
+  if (!cp || !n_chunks) return MAP_E_ARG;
+  map_program* p = const_cast<map_program*>(cp);
+  map_status st = ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p));
+  if (st != MAP_OK) return st;
+  *n_chunks = (uint32_t)p->plan.chunks.size();
+  return MAP_OK;
+}
+
+map_status map_generate_bucketed(map_program*, const map_exec*, uint32_t, uint32_t, uint32_t, void*, uint64_t*) {
+  return MAP_E_ARG;
+}
+
+map_status map_sort_detect(map_program*, const map_exec*, uint32_t, void*, uint64_t, uint64_t*, uint64_t*) {
+  return MAP_E_ARG;
+}
+
+map_status map_unpack_witness(const map_program* p, uint32_t chunk, uint64_t packed, map_witness* out) {
+  if (!p || !out || chunk >= p->plan.chunks.size() || packed == ~0ull) return MAP_E_ARG;
+  decode(p->C, p->plan.chunks[chunk], packed, out);
+  return MAP_OK;
+}
+
+// Last error text of a program (diagnostics for the Python binding).
+const char* map_last_error(const map_program* p) { return p ? p->last_error.c_str() : ""; }
+
+// Host-side self test of the invariant-divisor parameters (CPU tests).
+uint32_t mapc_test_fastdiv(uint32_t n, uint32_t d) { return mapc::fastdiv_apply(n, mapc::make_fastdiv(d)); }
+
+}  // extern "C"

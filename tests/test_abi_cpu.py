@@ -1,0 +1,116 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol the header
+declares, its host compiler agrees with the oracle on static facts and error
+classes, and the run entry point fails loudly without a GPU (no CPU fallback)."""
+import os
+import random
+import re
+
+import pytest
+
+import oracle
+import paper_2203_12878_b200 as mc
+from tests.test_oracle import CASES, n_closed
+from workloads import config, fuzz
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    with open(os.path.join(ROOT, "include", "mapcheck.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^\s*(?:map_status|size_t|void|const char \*)\s*\**\s*(map_\w+)\s*\(", text, re.M)))
+
+
+def test_header_symbols_exported():
+    names = declared_functions()
+    assert len(names) >= 10, names
+    for n in names:
+        assert hasattr(mc._lib, n), f"{n} declared in include/mapcheck.h but not exported"
+    assert set(mc.EXPORTS) <= set(names)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", mc.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings():
+    assert mc.status_str(0) == "ok"
+    assert "parse" in mc.status_str(1)
+
+
+@pytest.mark.parametrize("n,d", [(0, 1), (7, 3), (2**32 - 1, 3), (2**32 - 1, 7), (123456789, 1000),
+                                 (2**32 - 1, 2**31 + 1), (2**31, 3), (99, 100), (5, 5)])
+def test_fastdiv_edges(n, d):
+    assert mc.fastdiv_selftest(n, d) == n // d
+
+
+def test_fastdiv_random():
+    r = random.Random(1)
+    for _ in range(20000):
+        d = r.choice([r.randint(1, 100), r.randint(1, 2**16), r.randint(1, 2**32 - 1)])
+        n = r.choice([r.randint(0, 2**32 - 1), r.randint(0, 1000), d * r.randint(0, 2**32 // d) - r.randint(0, 1)])
+        n = max(0, min(n, 2**32 - 1))
+        assert mc.fastdiv_selftest(n, d) == n // d, (n, d)
+
+
+@pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
+def test_compile_bounds_cover_exact_counts(name, sizes):
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    info = p.info
+    assert info.max_accesses >= n_closed(name, inst)
+    assert p.scratch_bytes() > 0
+    assert p.n_chunks() >= (1 if n_closed(name, inst) else 0)
+
+
+def test_full_size_plans():
+    # 2^34-access stencil: one chunk per barrier phase at the default 2^30-key chunk
+    inst = config("5a")
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    assert p.info.max_accesses == 2**34
+    assert p.info.u32_mode
+    assert p.n_chunks() == 16
+    assert p.n_chunks(2**31) == 8
+
+
+@pytest.mark.parametrize("src,status", [
+    ("rd[", 1), ("forU x 0..3 { rd[x] }", 1), ("rd[x]", 2), ("rd Q[0]", 2),
+    ("forU x in 0..2 { forU x in 0..2 { rd[x] } }", 2),
+    ("if (tid = 0) { sync } else { skip }", 3), ("forU x in 0..2 { sync }", 3),
+    ("forS x in 0..tid { sync }", 3), ("rd[18446744073709551615 + 1]", 4),
+    ("forS x in 0..(1 / 0) { sync }", 5),
+])
+def test_compile_errors_match_oracle(src, status):
+    o = oracle.check(src, block=(2, 1, 1))
+    assert o.status == status
+    with pytest.raises(mc.MapError) as e:
+        mc.MapProgram(src, block=(2, 1, 1))
+    assert e.value.status == status
+
+
+def test_param_errors():
+    with pytest.raises(mc.MapError) as e:
+        mc.MapProgram("params M; rd[M]")
+    assert e.value.status == 8
+    with pytest.raises(mc.MapError) as e:
+        mc.MapProgram("rd[0]", params={"Q": 1})
+    assert e.value.status == 8
+
+
+def test_fuzz_corpus_compiles():
+    for seed in range(500):
+        inst, _ = fuzz.random_instance(seed)
+        p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+        o = oracle.check_instance(inst, threads=1)
+        assert o.status == 0
+        assert p.info.max_accesses >= o.n_accesses, (seed, inst.src)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="needs a machine without a GPU")
+def test_no_cpu_fallback():
+    p = mc.MapProgram("wr[0]", block=(2, 1, 1))
+    with pytest.raises(mc.MapError) as e:
+        p.check_races()
+    assert e.value.status == 6

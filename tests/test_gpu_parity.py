@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bit-exact agreement on verdict, canonical witness, access count (multiset) and
+racy-segment count -- integer work, so the bar is equality.
+"""
+import os
+
+import pytest
+
+import oracle
+import paper_2203_12878_b200 as mc
+from tests.test_oracle import CASES, n_closed, witness_closed
+from workloads import config, fuzz
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu(inst, chunk=0):
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    return p.check_races(chunk_max_accesses=chunk)
+
+
+def same(r, o):
+    assert o.status == 0, o.diag
+    got = (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments)
+    want = (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
+    assert got == want
+
+
+@pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
+def test_configs_scaled(name, sizes):
+    inst = config(name, **sizes)
+    same(gpu(inst), oracle.check_instance(inst))
+
+
+@pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
+def test_configs_scaled_small_chunks(name, sizes):
+    # force many chunks (phase ranges and block ranges) -> identical result
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    unit = max(1, p.info.max_unit_accesses)
+    same(p.check_races(chunk_max_accesses=unit), oracle.check_instance(inst))
+
+
+def test_fuzz_corpus():
+    n = int(os.environ.get("MAPCHECK_GPU_FUZZ", "400"))
+    bad = []
+    for seed in range(n):
+        inst, _ = fuzz.random_instance(seed)
+        o = oracle.check_instance(inst, threads=1)
+        r = gpu(inst)
+        got = (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments)
+        want = (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
+        if got != want:
+            bad.append((seed, inst.src, got, want))
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("name", ["1a", "1b", "2a", "2b", "2c", "4c", "4d"])
+def test_full_size_vs_oracle(name):
+    inst = config(name)
+    same(gpu(inst), oracle.check_instance(inst))
+
+
+@pytest.mark.parametrize("name", ["3a", "3b", "4a", "4b"])
+def test_full_size_large_vs_oracle(name):
+    inst = config(name)
+    same(gpu(inst), oracle.check_instance(inst))
+
+
+@pytest.mark.parametrize("name", ["5a", "5b"])
+def test_full_size_stencil_properties(name):
+    # 2^34 accesses: the oracle cannot enumerate them in test time; the access
+    # count and the witness have closed forms (tests/test_oracle.py, pinned
+    # there against the oracle and the brute force at smaller sizes).
+    inst = config(name)
+    r = gpu(inst)
+    assert r.n_accesses == n_closed(name, inst) == 2**34
+    w = witness_closed(name, inst)
+    assert (r.witness.as_tuple() if r.witness else None) == w
+    if name == "5b":
+        # every cell of every phase holds the owner's write and a neighbour's read
+        assert r.racy_segments > 0
+
+
+def test_long_segment_spans_many_tiles():
+    # one (phase, index) cell read by all 1024 threads 1024 times + one write
+    src = "forU x in 0..1024 { rd[0] }; wr[0]"
+    for blk in (1024, 1):
+        inst = config("1b", block=blk)
+        inst.src = src
+        same(gpu(inst), oracle.check_instance(inst))
+    src2 = "forU x in 0..4096 { rd[0] }; if (tid = 1023) { wr[0] } else { skip }"
+    r = mc.check(src2, block=(1024, 1, 1))
+    o = oracle.check(src2, block=(1024, 1, 1))
+    same(r, o)
+
+
+def test_single_segment_s0():
+    # S = 0 sort bits: every access in one segment (no sort at all)
+    for src, blk in [("wr[0]", 8), ("rd[0]", 8), ("if (tid = 3) { wr[0] } else { rd[0] }", 8), ("wr[0]", 1)]:
+        same(mc.check(src, block=(blk, 1, 1)), oracle.check(src, block=(blk, 1, 1)))
+
+
+def test_empty_programs():
+    for src in ["skip", "params M; forU x in 0..M { rd[x] }", "if (false) { wr[0] } else { skip }", "sync; sync"]:
+        r = mc.check(src, block=(4, 1, 1), params={"M": 0} if "M" in src else None)
+        assert r.verdict == 0 and r.n_accesses == 0
+
+
+def test_runtime_div_by_zero():
+    with pytest.raises(mc.MapError) as e:
+        mc.check("rd[8 / (tid - 1)]", block=(4, 1, 1))
+    assert e.value.status == 5
+    assert oracle.check("rd[8 / (tid - 1)]", block=(4, 1, 1)).status == 5
+    # guarded: never reached -> no error, same as the oracle
+    src = "if (tid > 1) { rd[8 / (tid - 1)] } else { skip }"
+    same(mc.check(src, block=(4, 1, 1)), oracle.check(src, block=(4, 1, 1)))
+
+
+def test_determinism_across_runs_and_chunkings():
+    inst = config("4b", n=1 << 14, bs=256)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    ref = p.check_races()
+    for chunk in (0, p.info.max_unit_accesses, 3 * p.info.max_unit_accesses):
+        for _ in range(3):
+            r = p.check_races(chunk_max_accesses=chunk)
+            assert (r.verdict, r.witness, r.n_accesses, r.racy_segments) == \
+                   (ref.verdict, ref.witness, ref.n_accesses, ref.racy_segments)
+
+
+def test_multi_dim_grid_and_block():
+    src = "params W; wr[(tid / W) * W + (tid + 1) % W]; sync; rd[bid % 3]"
+    for g, b in [((2, 3, 1), (4, 2, 1)), ((1, 1, 2), (2, 2, 2))]:
+        same(mc.check(src, grid=g, block=b, params={"W": 4}), oracle.check(src, g, b, {"W": 4}))
