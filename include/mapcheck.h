@@ -68,22 +68,48 @@ typedef struct {
   const uint64_t *param_values;     /* n_params naturals     */
 } map_instance;
 
+/* Per-kernel-class device timings of one map_check_races call, measured with
+ * CUDA events recorded on the caller's stream around every launch (optional:
+ * map_exec.stats == NULL disables them).  bytes = ALGORITHMIC bytes the
+ * launches had to move: generate writes 8 B per key, the
+ * histogram reads 8 B per key, an active radix pass reads + writes 8 B per
+ * key, detect reads 8 B per key. */
+enum {
+  MAP_K_GENERATE = 0,
+  MAP_K_HIST = 1,
+  MAP_K_SCAN = 2,
+  MAP_K_ONESWEEP = 3,
+  MAP_K_DETECT = 4,
+  MAP_K_OTHER = 5,
+  MAP_K_COUNT = 6
+};
+typedef struct {
+  float ms[MAP_K_COUNT];
+  uint32_t launches[MAP_K_COUNT];
+  uint64_t bytes[MAP_K_COUNT];
+} map_kernel_stats;
+
 /* Execution resources borrowed from the caller. */
 typedef struct {
   int device;                 /* CUDA device ordinal                                  */
   void *stream;               /* cudaStream_t (0 = legacy default stream)             */
   void *scratch;              /* device buffer, >= map_scratch_bytes(p, chunk)        */
   size_t scratch_bytes;
-  uint64_t chunk_max_accesses;/* accesses per chunk (0 = derive from scratch_bytes)  */
+  uint64_t chunk_max_accesses;/* accesses per chunk (0 = library default)            */
+  uint32_t rank, world;       /* shard: process chunks c with c % world == rank
+                                 (world 0 or 1 = all chunks; multi-GPU) */
+  map_kernel_stats *stats;    /* optional per-kernel timings (NULL = off)            */
 } map_exec;
 
 typedef struct {
-  int32_t verdict;            /* 0 = DRF, 1 = RACY                                    */
-  int32_t n_chunks;           /* chunks the run was split into                       */
+  int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */
+  int32_t n_chunks;           /* chunks this call processed                          */
   uint64_t n_accesses;        /* accesses enumerated, counted with multiplicity      */
   uint64_t racy_segments;     /* (phase, array, block, index) cells holding a race   */
   float device_ms;            /* device time of the whole run (CUDA events)          */
   uint32_t gpu_launches;      /* kernels launched by this call                       */
+  uint64_t h2d_bytes;         /* host->device bytes copied (bytecode, segment tables)*/
+  uint64_t d2h_bytes;         /* device->host bytes copied (per-chunk results)       */
 } map_result;
 
 typedef struct {
@@ -124,6 +150,9 @@ map_status map_check_races(map_program *p, const map_exec *ex, map_result *out);
 
 /* Canonical witness of the last racy map_check_races; MAP_E_ARG if it was DRF. */
 map_status map_witness_get(const map_program *p, map_witness *out);
+
+/* Name of array `idx` (declaration order; NULL if out of range). */
+const char *map_array_name(const map_program *p, uint32_t idx);
 
 void map_program_free(map_program *p);
 const char *map_status_str(map_status s);

@@ -38,7 +38,7 @@ STATUS = {
 EXPORTS = (
     "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
     "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
-    "map_sort_detect", "map_unpack_witness",
+    "map_sort_detect", "map_unpack_witness", "map_array_name",
 )
 
 
@@ -47,14 +47,23 @@ class _Instance(ctypes.Structure):
                 ("param_names", ctypes.POINTER(ctypes.c_char_p)), ("param_values", ctypes.POINTER(ctypes.c_uint64))]
 
 
+KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other")   # MAP_K_* order
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_float * 6), ("launches", ctypes.c_uint32 * 6), ("bytes", ctypes.c_uint64 * 6)]
+
+
 class _Exec(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("scratch", ctypes.c_void_p),
-                ("scratch_bytes", ctypes.c_size_t), ("chunk_max_accesses", ctypes.c_uint64)]
+                ("scratch_bytes", ctypes.c_size_t), ("chunk_max_accesses", ctypes.c_uint64),
+                ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32), ("stats", ctypes.POINTER(_Stats))]
 
 
 class _Result(ctypes.Structure):
     _fields_ = [("verdict", ctypes.c_int32), ("n_chunks", ctypes.c_int32), ("n_accesses", ctypes.c_uint64),
-                ("racy_segments", ctypes.c_uint64), ("device_ms", ctypes.c_float), ("gpu_launches", ctypes.c_uint32)]
+                ("racy_segments", ctypes.c_uint64), ("device_ms", ctypes.c_float), ("gpu_launches", ctypes.c_uint32),
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64)]
 
 
 class _Witness(ctypes.Structure):
@@ -90,6 +99,10 @@ _lib.map_last_error.argtypes = [_P]
 _lib.map_last_error.restype = ctypes.c_char_p
 _lib.map_chunk_count.argtypes = [_P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32)]
 _lib.map_chunk_count.restype = ctypes.c_int
+_lib.map_array_name.argtypes = [_P, ctypes.c_uint32]
+_lib.map_array_name.restype = ctypes.c_char_p
+_lib.map_debug_dump.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_debug_dump.restype = ctypes.c_size_t
 _lib.mapc_test_fastdiv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
 _lib.mapc_test_fastdiv.restype = ctypes.c_uint32
 
@@ -124,7 +137,10 @@ class Result:
     n_chunks: int
     device_ms: float
     gpu_launches: int
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
     witness: Optional[Witness] = None
+    kernels: Optional[Dict[str, Dict[str, float]]] = None   # per kernel class: ms, launches, bytes
 
     @property
     def racy(self) -> bool:
@@ -176,6 +192,21 @@ class MapProgram:
             _lib.map_program_free(h)
             self._h = None
 
+    def array_names(self):
+        out = []
+        while True:
+            n = _lib.map_array_name(self._h, len(out))
+            if n is None:
+                return out
+            out.append(n.decode())
+
+    def dump(self) -> str:
+        """Listing of the lowered bytecode (debugging)."""
+        n = _lib.map_debug_dump(self._h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        _lib.map_debug_dump(self._h, buf, n + 1)
+        return buf.value.decode()
+
     @property
     def info(self) -> Info:
         i = _Info()
@@ -196,11 +227,14 @@ class MapProgram:
             raise MapError(st, _lib.map_last_error(self._h).decode())
         return c.value
 
-    def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None) -> Result:
+    def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None,
+                    rank: int = 0, world: int = 1, profile: bool = False) -> Result:
         """Run generate -> sort -> detect on one GPU (blocking).
 
         scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
-        stream: a torch.cuda.Stream (default: the current stream)."""
+        stream: a torch.cuda.Stream (default: the current stream);
+        rank/world: process only chunks c with c % world == rank (multi-GPU sharding);
+        profile: record CUDA events around every launch and return per-kernel-class timings."""
         import torch
         if not torch.cuda.is_available():
             raise MapError(6, "no CUDA device (there is no CPU fallback)")
@@ -210,18 +244,24 @@ class MapProgram:
             scratch = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")
         if stream is None:
             stream = torch.cuda.current_stream(dev)
+        stats = _Stats() if profile else None
         ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
-                   scratch.numel() * scratch.element_size(), int(chunk_max_accesses))
+                   scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
+                   ctypes.pointer(stats) if stats is not None else None)
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:
             raise MapError(st, _lib.map_last_error(self._h).decode())
-        res = Result(r.verdict, r.n_accesses, r.racy_segments, r.n_chunks, r.device_ms, r.gpu_launches)
+        res = Result(r.verdict, r.n_accesses, r.racy_segments, r.n_chunks, r.device_ms, r.gpu_launches,
+                     r.h2d_bytes, r.d2h_bytes)
         if r.verdict:
             w = _Witness()
             if _lib.map_witness_get(self._h, ctypes.byref(w)) == 0:
                 res.witness = Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
                                       w.array_name.decode())
+        if stats is not None:
+            res.kernels = {k: {"ms": stats.ms[i], "launches": stats.launches[i], "bytes": stats.bytes[i]}
+                           for i, k in enumerate(KERNEL_CLASSES)}
         return res
 
 

@@ -24,9 +24,9 @@
 
 extern "C" {
 cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cudaStream_t s);
-cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tuples,
+cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tiles,
                                  const MapcLayout* lay, int u32_mode, unsigned long long* keys, MapcCtrl* ctrl,
-                                 int n_sms, cudaStream_t s);
+                                 int n_sms, uint32_t nreg, uint32_t max_emits, cudaStream_t s);
 cudaError_t mapc_launch_hist(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t n_passes,
                              unsigned long long max_keys, int n_sms, cudaStream_t s);
 cudaError_t mapc_launch_digit_scan(MapcCtrl* ctrl, uint32_t n_passes, cudaStream_t s);
@@ -35,11 +35,11 @@ cudaError_t mapc_launch_onesweep(unsigned long long* bufA, unsigned long long* b
                                  unsigned long long* lookback, uint32_t pass, uint32_t shift,
                                  unsigned long long epoch, unsigned long long max_keys, int n_sms, cudaStream_t s);
 unsigned long long mapc_detect_tile();
-cudaError_t mapc_launch_chunk_init(MapcCtrl* ctrl, cudaStream_t s);
+cudaError_t mapc_launch_chunk_init(MapcCtrl* ctrl, unsigned long long n0, cudaStream_t s);
 cudaError_t mapc_launch_detect(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
                                uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
                                MapcSegState* last_frag, unsigned long long max_keys, int n_sms, cudaStream_t s);
-cudaError_t mapc_launch_chunk_finish(const MapcCtrl* ctrl, MapcChunkResult* out, cudaStream_t s);
+cudaError_t mapc_launch_chunk_finish(const MapcCtrl* ctrl, uint32_t n_passes, MapcChunkResult* out, cudaStream_t s);
 }
 
 namespace {
@@ -54,6 +54,10 @@ struct Chunk {
   std::vector<MapcOp> ops;
   uint64_t bound = 0;
   uint64_t total_tuples = 0;
+  uint64_t total_tiles = 0;                 // generate tiles (segment-aligned)
+  uint64_t dense_total = 0;                 // keys of dense segments (placed directly)
+  uint32_t nreg = MAPC_REG_K0;              // VM registers used by the chunk's programs
+  uint32_t max_emits = 0;                   // largest n_emits of a non-dense segment
   size_t stage_ops = 0, stage_segs = 0;     // offsets in the pinned staging buffer
 };
 
@@ -82,6 +86,10 @@ struct map_program {
   uint64_t epoch = 0;
   int device = -1;
   std::string last_error;
+  std::vector<cudaEvent_t> events;   // pool for per-kernel timing
+  ~map_program() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+  }
 };
 
 namespace {
@@ -140,7 +148,17 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
       const mapc::InstanceInfo& in = C.inst[ii];
       for (const mapc::GroupProg& g : in.groups) {
         const uint32_t pb = (uint32_t)ch.ops.size();
-        for (const MapcOp& op : g.ops) ch.ops.push_back(lower_op_for_mode(op, C.u32_mode));
+        for (const MapcOp& op : g.ops) {
+          ch.ops.push_back(lower_op_for_mode(op, C.u32_mode));
+          const uint32_t code = op.code & MAPC_CODE_MASK;
+          auto use = [&](uint32_t r) { ch.nreg = std::max(ch.nreg, r + 1); };
+          if (code != VM_EMIT && code != VM_ACT) use(op.dst);
+          if (!(op.code & MAPC_A_IMM) && code != VM_MOVI) use(op.a);
+          const bool has_b = code != VM_BAND && code != VM_LNOT && code != VM_MOVI && code != VM_ACT && code != VM_EMIT;
+          if (has_b && !(op.code & MAPC_B_IMM)) use(op.b);
+          if (code == VM_MADK || (code == VM_TRIP && !(op.aux & MAPC_AUX_CONST))) use(op.aux);
+        }
+        ch.nreg = std::max(ch.nreg, (uint32_t)MAPC_REG_K0 + g.n_levels);
         const uint32_t pe = (uint32_t)ch.ops.size();
         const uint64_t tpb = g.tuples_per_block;
         const uint64_t per_seg = std::max<uint64_t>(1, 0xFFFFFFFFull / tpb);
@@ -149,6 +167,14 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
           MapcSeg s{};
           s.tuple_begin = ch.total_tuples;
           s.n_tuples = nb * tpb;
+          s.tile_begin = ch.total_tiles;
+          ch.total_tiles += (s.n_tuples + MAPC_GEN_TILE - 1) / MAPC_GEN_TILE;
+          if (g.dense) {
+            s.key_begin = ch.dense_total;
+            ch.dense_total += s.n_tuples * g.n_emits;
+          } else {
+            ch.max_emits = std::max(ch.max_emits, g.n_emits);
+          }
           s.key_hi = (uint64_t)(in.phase - ch.phase_lo) << (L.w_array + L.w_block + L.w_index);
           s.prog_begin = pb;
           s.prog_end = pe;
@@ -249,8 +275,8 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
   const uint64_t det_tiles = (kcap + mapc_detect_tile() - 1) / mapc_detect_tile();
   size_t off = 0;
-  out.off_a = off; off += align_up(kcap * 8);
-  out.off_b = off; off += align_up(kcap * 8);
+  out.off_a = off; off += align_up(kcap * 8 + 64);     // + slack: bulk copies round up to 16 B
+  out.off_b = off; off += align_up(kcap * 8 + 64);
   out.lb_bytes = sort_tiles * MAPC_RADIX * 8;
   out.off_lb = off; off += align_up(out.lb_bytes);
   out.off_ff = off; off += align_up(det_tiles * sizeof(MapcSegState));
@@ -445,65 +471,116 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     p->last_lookback = lookback;
     p->device = ex->device;
   }
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, s));
+  const uint32_t world = ex->world ? ex->world : 1;
+  const uint32_t rank = ex->rank;
+  if (rank >= world) return MAP_E_ARG;
+  std::vector<size_t> mine;
+  for (size_t c = 0; c < P.chunks.size(); ++c)
+    if (c % world == rank) mine.push_back(c);
+  // events: 2 per timed launch group + 2 for the whole run
+  const bool prof = ex->stats != nullptr;
+  size_t need_ev = 2 + (prof ? mine.size() * (2 * (6 + MAPC_MAX_PASSES)) : 0);
+  while (p->events.size() < need_ev) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    p->events.push_back(e);
+  }
+  struct Mark { int kind; size_t e0, e1; };
+  std::vector<Mark> marks;
+  size_t ev = 2;
   uint32_t launches = 0;
-  for (size_t c = 0; c < P.chunks.size(); ++c) {
+  map_kernel_stats st_acc{};
+  auto begin = [&](int kind) -> size_t {
+    ++launches;
+    st_acc.launches[kind]++;
+    if (!prof) return 0;
+    cudaEventRecord(p->events[ev], s);
+    marks.push_back({kind, ev, ev + 1});
+    ev += 2;
+    return ev - 1;
+  };
+  auto end = [&](size_t e1) {
+    if (prof) cudaEventRecord(p->events[e1], s);
+  };
+  uint64_t h2d = 0;
+  CK(cudaEventRecord(p->events[0], s));
+  for (size_t c : mine) {
     const Chunk& ch = P.chunks[c];
     const MapcLayout& L = ch.lay;
     CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
     CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, s));
-    CK(mapc_launch_chunk_init(ctrl, s));
-    ++launches;
-    if (ch.total_tuples) {
-      CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tuples, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
-                              n_sms, s));
-      ++launches;
+    h2d += ch.ops.size() * sizeof(MapcOp) + ch.segs.size() * sizeof(MapcSeg);
+    size_t m = begin(MAP_K_OTHER);
+    CK(mapc_launch_chunk_init(ctrl, ch.dense_total, s));
+    end(m);
+    if (ch.total_tiles) {
+      m = begin(MAP_K_GENERATE);
+      CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                              n_sms, ch.nreg, ch.max_emits, s));
+      end(m);
     }
     if (L.n_passes) {
+      m = begin(MAP_K_HIST);
       CK(mapc_launch_hist(bufA, ctrl, L.pay_bits, L.n_passes, ch.bound, n_sms, s));
-      ++launches;
+      end(m);
     }
+    m = begin(MAP_K_SCAN);
     CK(mapc_launch_digit_scan(ctrl, L.n_passes, s));
-    ++launches;
+    end(m);
     for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
       ++p->epoch;
+      m = begin(MAP_K_ONESWEEP);
       CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.pay_bits + 8 * pass, p->epoch, ch.bound, n_sms, s));
-      ++launches;
+      end(m);
     }
+    m = begin(MAP_K_DETECT);
+    ++launches;                        // detect + fixup
+    st_acc.launches[MAP_K_DETECT]++;
     CK(mapc_launch_detect(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.w_tid, ff, lf, ch.bound, n_sms, s));
-    launches += 2;
-    CK(mapc_launch_chunk_finish(ctrl, res + c, s));
-    ++launches;
+    end(m);
+    m = begin(MAP_K_OTHER);
+    CK(mapc_launch_chunk_finish(ctrl, L.n_passes, res + c, s));
+    end(m);
   }
-  CK(cudaEventRecord(e1, s));
-  CK(cudaMemcpyAsync(host_res, res, P.chunks.size() * sizeof(MapcChunkResult), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(p->events[1], s));
+  if (!P.chunks.empty())
+    CK(cudaMemcpyAsync(host_res, res, P.chunks.size() * sizeof(MapcChunkResult), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  cudaEventElapsedTime(&ms, p->events[0], p->events[1]);
 
   map_result r{};
-  r.n_chunks = (int32_t)P.chunks.size();
+  r.n_chunks = (int32_t)mine.size();
   r.device_ms = ms;
   r.gpu_launches = launches;
+  r.h2d_bytes = h2d;
+  r.d2h_bytes = P.chunks.size() * sizeof(MapcChunkResult);
   uint32_t err = 0;
   bool have = false;
   map_witness best{};
-  for (size_t c = 0; c < P.chunks.size(); ++c) {
+  for (size_t c : mine) {
     const MapcChunkResult& cr = host_res[c];
     r.n_accesses += cr.n;
     r.racy_segments += cr.racy;
     err |= cr.err;
+    st_acc.bytes[MAP_K_GENERATE] += 8 * cr.n;
+    if (P.chunks[c].lay.n_passes) st_acc.bytes[MAP_K_HIST] += 8 * cr.n;
+    st_acc.bytes[MAP_K_ONESWEEP] += 16ull * cr.n * cr.active_passes;
+    st_acc.bytes[MAP_K_DETECT] += 8 * cr.n;
     if (cr.witness != ~0ull) {
       map_witness w{};
       decode(p->C, P.chunks[c], cr.witness, &w);
       if (!have || wit_less(w, best)) best = w;
       have = true;
     }
+  }
+  if (prof) {
+    for (const Mark& mk : marks) {
+      float t = 0;
+      cudaEventElapsedTime(&t, p->events[mk.e0], p->events[mk.e1]);
+      st_acc.ms[mk.kind] += t;
+    }
+    *ex->stats = st_acc;
   }
   if (err & MAPC_ERR_DIV0) {
     p->last_error = "division or modulo by zero on a reached path";
@@ -555,6 +632,44 @@ map_status map_unpack_witness(const map_program* p, uint32_t chunk, uint64_t pac
   if (!p || !out || chunk >= p->plan.chunks.size() || packed == ~0ull) return MAP_E_ARG;
   decode(p->C, p->plan.chunks[chunk], packed, out);
   return MAP_OK;
+}
+
+const char* map_array_name(const map_program* p, uint32_t idx) {
+  if (!p || idx >= p->C.ast.arrays.size()) return nullptr;
+  return p->C.ast.arrays[idx].c_str();
+}
+
+// Human-readable listing of the lowered programs (debugging / tests).
+size_t map_debug_dump(const map_program* p, char* buf, size_t cap) {
+  if (!p) return 0;
+  static const char* names[] = {"add", "sub", "mul", "div", "mod", "shl", "shr", "min", "max", "divm", "modm",
+                                "band", "eq", "ne", "lt", "le", "gt", "ge", "land", "lor", "lnot", "trip",
+                                "madk", "act", "emit", "movi", "nop"};
+  std::string out;
+  for (size_t i = 0; i < p->C.inst.size(); ++i) {
+    const auto& in = p->C.inst[i];
+    for (size_t g = 0; g < in.groups.size(); ++g) {
+      const auto& G = in.groups[g];
+      out += "instance " + std::to_string(i) + " phase " + std::to_string(in.phase) + " group " + std::to_string(g) +
+             " levels " + std::to_string(G.n_levels) + " trips";
+      for (uint32_t l = 0; l < G.n_levels; ++l) out += " " + std::to_string(G.trips[l]);
+      out += std::string(G.dense ? " dense" : "") + " emits " + std::to_string(G.n_emits) + "\n";
+      for (const MapcOp& op : G.ops) {
+        const uint32_t c = op.code & MAPC_CODE_MASK;
+        out += "  r" + std::to_string(op.dst) + " = " + (c <= VM_NOP ? names[c] : "?") + " ";
+        out += (op.code & MAPC_A_IMM) ? ("#" + std::to_string(op.imm)) : ("r" + std::to_string(op.a));
+        out += ", ";
+        out += (op.code & MAPC_B_IMM) ? ("#" + std::to_string(op.imm)) : ("r" + std::to_string(op.b));
+        out += " aux=" + std::to_string(op.aux) + "\n";
+      }
+    }
+  }
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, out.size());
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return out.size();
 }
 
 // Last error text of a program (diagnostics for the Python binding).

@@ -23,6 +23,9 @@
 #define MAPC_REG_TID 0
 #define MAPC_REG_BID 1
 #define MAPC_REG_K0 2
+#define MAPC_GEN_THREADS 128
+#define MAPC_GEN_V 4                 // tuples per thread per VM pass
+#define MAPC_GEN_TILE (MAPC_GEN_THREADS * MAPC_GEN_V)
 
 enum MapcOpcode : uint8_t {
   VM_ADD = 0, VM_SUB,   /* monus */
@@ -72,6 +75,8 @@ struct MapcFastDiv {
 struct MapcSeg {
   uint64_t tuple_begin;               // exclusive prefix of tuples within the chunk
   uint64_t n_tuples;                  // (#blocks) * blockDim * prod(trips)
+  uint64_t tile_begin;                // exclusive prefix of generate tiles (MAPC_GEN_TILE tuples each)
+  uint64_t key_begin;                 // dense segments: first output slot (site-major layout)
   uint64_t key_hi;                    // local-phase field, already shifted to its place in the sort field
   uint32_t prog_begin, prog_end;      // op range in the chunk's constant program
   uint32_t n_levels;
@@ -116,7 +121,7 @@ struct MapcChunkResult {
   unsigned long long witness;
   unsigned long long racy;
   unsigned int err;
-  unsigned int pad;
+  unsigned int active_passes;      // radix passes that were not skipped
 };
 
 #define MAPC_ERR_DIV0 1u        // division/modulo by zero on a reached path

@@ -7,16 +7,15 @@
 // PAPER.md:506-551 with the par union of PAPER.md:579-589 made explicit as the
 // tid coordinate -- and emits one key per access whose guards hold:
 //   key = [lphase | array | lblock | index - idx_lo][tid][kind]
-// Keys of a CTA iteration are compacted in shared memory and reserved with one
-// global atomicAdd per CTA iteration (block-aggregated compaction), then
-// stored with coalesced 16-byte stores.
+// Dense segments store keys at precomputed slots; guarded segments compact
+// their keys in shared memory and reserve space with one global atomicAdd per
+// CTA iteration (block-aggregated compaction).
 #include "common.cuh"
 
 namespace mapk {
 
 __constant__ MapcOp c_ops[MAPC_MAX_OPS];
 
-constexpr int GEN_THREADS = 128;
 
 template <typename W>
 struct VmWidth;
@@ -25,124 +24,174 @@ struct VmWidth<uint32_t> { static constexpr uint32_t bits = 32; };
 template <>
 struct VmWidth<uint64_t> { static constexpr uint32_t bits = 64; };
 
+// ---- v2: segment-uniform tiles, 4 tuples per thread per VM pass ------------
+// A CTA iteration covers MAPC_GEN_TILE consecutive tuples of ONE segment, so the
+// bytecode stream is uniform across the CTA; each op is decoded once and applied
+// to V tuples per thread (dispatch cost amortised V-fold).  The shared register
+// file holds only the registers the chunk's programs use.  Dense segments
+// (no guard, no fault check: every tuple emits n_emits keys) store each key
+// at key_begin + e * n_tuples + tuple (site-major, coalesced); other segments
+// are compacted through shared memory with one global atomicAdd per tile.
 template <typename W>
-__global__ void __launch_bounds__(GEN_THREADS)
-k_generate(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long total_tuples, MapcLayout lay,
-           unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl) {
-  __shared__ W R[MAPC_NREG][GEN_THREADS];
-  __shared__ unsigned long long stage[GEN_THREADS * MAPC_MAX_EMITS];
-  __shared__ uint32_t scan_tmp[GEN_THREADS / 32 + 1];
-  __shared__ unsigned long long s_base;
+__global__ void __launch_bounds__(MAPC_GEN_THREADS)
+k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long total_tiles, MapcLayout lay,
+            unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t nreg) {
+  constexpr int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   constexpr uint32_t WB = VmWidth<W>::bits;
+  extern __shared__ __align__(16) unsigned char gsm[];
+  W* R = reinterpret_cast<W*>(gsm);                                    // [nreg][V][T]
+  unsigned long long* stage = reinterpret_cast<unsigned long long*>(gsm + ((size_t)nreg * V * T * sizeof(W) + 15) / 16 * 16);
+  __shared__ uint32_t scan_tmp[T / 32 + 1];
+  __shared__ unsigned long long s_base;
   const int me = threadIdx.x;
   uint32_t err = 0;
+#define RG(r, v) R[((size_t)(r) * V + (v)) * T + me]
 
-  for (unsigned long long base = (unsigned long long)blockIdx.x * GEN_THREADS; base < total_tuples;
-       base += (unsigned long long)gridDim.x * GEN_THREADS) {
-    const unsigned long long t = base + me;
-    uint32_t cnt = 0;
-    if (t < total_tuples) {
-      // segment lookup: last s with tuple_begin <= t
-      int lo = 0, hi = n_segs - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (segs[mid].tuple_begin <= t) lo = mid; else hi = mid - 1;
-      }
-      const MapcSeg& sg = segs[lo];
-      uint32_t rem = (uint32_t)(t - sg.tuple_begin);
-      const uint32_t L = sg.n_levels;
+  for (unsigned long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    int lo = 0, hi = n_segs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+    }
+    const MapcSeg& sg = segs[lo];
+    const uint32_t tl0 = (uint32_t)(tile - sg.tile_begin) * (uint32_t)(V * T);
+    const uint32_t L = sg.n_levels;
+    uint32_t tidv[V], lbv[V];
+    bool act[V], valid[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t t = tl0 + v * T + me;
+      valid[v] = t < sg.n_tuples;
+      uint32_t rem = valid[v] ? t : 0u;
       for (int l = (int)L - 1; l >= 0; --l) {
-        uint32_t q = fastdiv(rem, sg.trip_div[l]);
-        R[MAPC_REG_K0 + l][me] = (W)(rem - q * sg.trip_div[l].d);
+        const uint32_t q = fastdiv(rem, sg.trip_div[l]);
+        RG(MAPC_REG_K0 + l, v) = (W)(rem - q * sg.trip_div[l].d);
         rem = q;
       }
-      uint32_t q = fastdiv(rem, sg.tid_div);
-      const uint32_t tid = rem - q * sg.tid_div.d;
-      const uint32_t bid = sg.b0 + q;
-      const uint32_t lb = sg.lb0 + q;
-      R[MAPC_REG_TID][me] = (W)tid;
-      R[MAPC_REG_BID][me] = (W)bid;
-      bool act = true;
-      for (uint32_t pc = sg.prog_begin; pc < sg.prog_end; ++pc) {
-        const MapcOp op = c_ops[pc];
-        const uint32_t code = op.code & MAPC_CODE_MASK;
-        const W A = (op.code & MAPC_A_IMM) ? (W)op.imm : R[op.a][me];
-        const W B = (op.code & MAPC_B_IMM) ? (W)op.imm : R[op.b][me];
-        W d = 0;
-        switch (code) {
-          case VM_ADD: d = A + B; break;
-          case VM_SUB: d = A > B ? A - B : W(0); break;
-          case VM_MUL: d = A * B; break;
-          case VM_DIV:
-            if (B == 0) { if (act && (op.aux & MAPC_AUX_FAULT)) err |= MAPC_ERR_DIV0; d = 0; }
-            else d = A / B;
-            break;
-          case VM_MOD:
-            if (B == 0) { if (act && (op.aux & MAPC_AUX_FAULT)) err |= MAPC_ERR_DIV0; d = 0; }
-            else d = A % B;
-            break;
-          case VM_SHL: d = B >= WB ? W(0) : W(A << B); break;
-          case VM_SHR: d = B >= WB ? W(0) : W(A >> B); break;
-          case VM_MIN: d = A < B ? A : B; break;
-          case VM_MAX: d = A > B ? A : B; break;
-          case VM_DIVM:
-          case VM_MODM: {
-            const uint32_t dv = (uint32_t)(op.imm >> 32), m = (uint32_t)op.imm;
-            const uint32_t a32 = (uint32_t)A;
+      const uint32_t q = fastdiv(rem, sg.tid_div);
+      tidv[v] = rem - q * sg.tid_div.d;
+      RG(MAPC_REG_TID, v) = (W)tidv[v];
+      RG(MAPC_REG_BID, v) = (W)(sg.b0 + q);
+      lbv[v] = sg.lb0 + q;
+      act[v] = true;
+    }
+    uint32_t cnt = 0, e = 0;
+    for (uint32_t pc = sg.prog_begin; pc < sg.prog_end; ++pc) {
+      const MapcOp op = c_ops[pc];
+      const uint32_t code = op.code & MAPC_CODE_MASK;
+      const bool ai = op.code & MAPC_A_IMM, bi = op.code & MAPC_B_IMM;
+      const W im = (W)op.imm;
+#define AV(v) (ai ? im : RG(op.a, v))
+#define BV(v) (bi ? im : RG(op.b, v))
+#define VLOOP(expr)                                       \
+  _Pragma("unroll") for (int v = 0; v < V; ++v) {         \
+    const W A = AV(v), B = BV(v);                         \
+    (void)A; (void)B;                                     \
+    RG(op.dst, v) = (W)(expr);                            \
+  }                                                       \
+  break;
+      switch (code) {
+        case VM_ADD: VLOOP(A + B)
+        case VM_SUB: VLOOP(A > B ? A - B : W(0))
+        case VM_MUL: VLOOP(A * B)
+        case VM_DIV:
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const W A = AV(v), B = BV(v);
+            if (B == 0 && act[v] && valid[v] && (op.aux & MAPC_AUX_FAULT)) err |= MAPC_ERR_DIV0;
+            RG(op.dst, v) = B ? A / B : W(0);
+          }
+          break;
+        case VM_MOD:
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const W A = AV(v), B = BV(v);
+            if (B == 0 && act[v] && valid[v] && (op.aux & MAPC_AUX_FAULT)) err |= MAPC_ERR_DIV0;
+            RG(op.dst, v) = B ? A % B : W(0);
+          }
+          break;
+        case VM_SHL: VLOOP(B >= WB ? W(0) : W(A << B))
+        case VM_SHR: VLOOP(B >= WB ? W(0) : W(A >> B))
+        case VM_MIN: VLOOP(A < B ? A : B)
+        case VM_MAX: VLOOP(A > B ? A : B)
+        case VM_DIVM:
+        case VM_MODM: {
+          const uint32_t dv = (uint32_t)(op.imm >> 32), m = (uint32_t)op.imm;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const uint32_t a32 = (uint32_t)(ai ? im : RG(op.a, v));
             const uint32_t h = __umulhi(m, a32);
             const uint32_t qq = (h + ((a32 - h) >> 1)) >> op.aux;
-            d = code == VM_DIVM ? W(qq) : W(a32 - qq * dv);
-            break;
+            RG(op.dst, v) = code == VM_DIVM ? W(qq) : W(a32 - qq * dv);
           }
-          case VM_BAND: d = A & (W)op.imm; break;
-          case VM_EQ: d = A == B; break;
-          case VM_NE: d = A != B; break;
-          case VM_LT: d = A < B; break;
-          case VM_LE: d = A <= B; break;
-          case VM_GT: d = A > B; break;
-          case VM_GE: d = A >= B; break;
-          case VM_LAND: d = (A != 0) & (B != 0); break;
-          case VM_LOR: d = (A != 0) | (B != 0); break;
-          case VM_LNOT: d = A == 0; break;
-          case VM_TRIP: {
-            const W step = (op.aux & MAPC_AUX_CONST) ? (W)(op.aux & ~MAPC_AUX_CONST) : R[op.aux][me];
+          break;
+        }
+        case VM_BAND: VLOOP(A & (W)op.imm)
+        case VM_EQ: VLOOP(A == B)
+        case VM_NE: VLOOP(A != B)
+        case VM_LT: VLOOP(A < B)
+        case VM_LE: VLOOP(A <= B)
+        case VM_GT: VLOOP(A > B)
+        case VM_GE: VLOOP(A >= B)
+        case VM_LAND: VLOOP((A != 0) & (B != 0))
+        case VM_LOR: VLOOP((A != 0) | (B != 0))
+        case VM_LNOT: VLOOP(A == 0)
+        case VM_TRIP:
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const W A = AV(v), B = BV(v);
+            const W step = (op.aux & MAPC_AUX_CONST) ? (W)(op.aux & ~MAPC_AUX_CONST) : RG(op.aux, v);
             const W span = B > A ? B - A : W(0);
-            d = span == 0 ? W(0) : (step == 1 ? span : W((span - 1) / (step ? step : W(1)) + 1));
-            break;
+            RG(op.dst, v) = span == 0 ? W(0) : (step == 1 ? span : W((span - 1) / (step ? step : W(1)) + 1));
           }
-          case VM_MADK: d = A + R[op.aux][me] * B; break;
-          case VM_ACT: act = A != 0; break;
-          case VM_MOVI: d = (W)op.imm; break;
-          case VM_EMIT:
-            if (act) {
-              const unsigned long long idx = (unsigned long long)A - lay.idx_lo;
-              if (lay.w_index < 64 && (idx >> lay.w_index) != 0) err |= MAPC_ERR_LAYOUT;
-              const unsigned long long sf = sg.key_hi +
-                                            ((unsigned long long)(op.aux >> 1) << (lay.w_block + lay.w_index)) +
-                                            ((unsigned long long)lb << lay.w_index) + idx;
-              stage[cnt * GEN_THREADS + me] = (sf << lay.pay_bits) | ((unsigned long long)tid << 1) | (op.aux & 1u);
+          break;
+        case VM_MADK: VLOOP(A + RG(op.aux, v) * B)
+        case VM_MOVI: VLOOP(im)
+        case VM_ACT:
+#pragma unroll
+          for (int v = 0; v < V; ++v) act[v] = AV(v) != 0;
+          break;
+        case VM_EMIT: {
+          const unsigned long long arr = (unsigned long long)(op.aux >> 1) << (lay.w_block + lay.w_index);
+          const unsigned long long kind = op.aux & 1u;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (!(act[v] && valid[v])) continue;
+            const unsigned long long idx = (unsigned long long)AV(v) - lay.idx_lo;
+            if (lay.w_index < 64 && (idx >> lay.w_index) != 0) err |= MAPC_ERR_LAYOUT;
+            const unsigned long long sf = sg.key_hi + arr + ((unsigned long long)lbv[v] << lay.w_index) + idx;
+            const unsigned long long key = (sf << lay.pay_bits) | ((unsigned long long)tidv[v] << 1) | kind;
+            if (sg.dense) {
+              keys[sg.key_begin + (unsigned long long)e * sg.n_tuples + tl0 + v * T + me] = key;
+            } else {
+              stage[(size_t)cnt * T + me] = key;
               ++cnt;
             }
-            break;
-          default: break;
+          }
+          ++e;
+          break;
         }
-        if (code != VM_EMIT && code != VM_ACT) R[op.dst][me] = d;
+        default: break;
       }
+#undef AV
+#undef BV
+#undef VLOOP
     }
-    // block-aggregated compaction
-    uint32_t total;
-    const uint32_t excl = block_excl_scan<GEN_THREADS>(cnt, scan_tmp, &total);
-    if (me == 0) s_base = total ? atomicAdd(&ctrl->n, (unsigned long long)total) : 0ull;
-    __syncthreads();
-    const unsigned long long obase = s_base;
-    // local keys -> compacted order in `stage` is per-thread strided; write directly
-    for (uint32_t j = 0; j < cnt; ++j) {
-      const unsigned long long pos = obase + excl + j;
-      if (pos < lay.cap) keys[pos] = stage[j * GEN_THREADS + me];
-      else err |= MAPC_ERR_CAPACITY;
+    if (!sg.dense) {                                  // uniform across the CTA
+      uint32_t total;
+      const uint32_t excl = block_excl_scan<T>(cnt, scan_tmp, &total);
+      if (me == 0) s_base = total ? atomicAdd(&ctrl->n, (unsigned long long)total) : 0ull;
+      __syncthreads();
+      const unsigned long long obase = s_base;
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const unsigned long long pos = obase + excl + j;
+        if (pos < lay.cap) keys[pos] = stage[(size_t)j * T + me];
+        else err |= MAPC_ERR_CAPACITY;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
+#undef RG
   if (err) atomicOr(&ctrl->err, err);
 }
 
@@ -154,16 +203,27 @@ extern "C" cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cud
   return cudaMemcpyToSymbolAsync(mapk::c_ops, host_ops, n_ops * sizeof(MapcOp), 0, cudaMemcpyHostToDevice, s);
 }
 
-extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tuples,
+extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tiles,
                                             const MapcLayout* lay, int u32_mode, unsigned long long* keys,
-                                            MapcCtrl* ctrl, int n_sms, cudaStream_t s) {
-  if (total_tuples == 0) return cudaSuccess;
-  unsigned long long want = (total_tuples + mapk::GEN_THREADS - 1) / mapk::GEN_THREADS;
-  unsigned long long cap = (unsigned long long)n_sms * 8;
-  int grid = (int)(want < cap ? want : cap);
-  if (u32_mode)
-    mapk::k_generate<uint32_t><<<grid, mapk::GEN_THREADS, 0, s>>>(segs, n_segs, total_tuples, *lay, keys, ctrl);
-  else
-    mapk::k_generate<uint64_t><<<grid, mapk::GEN_THREADS, 0, s>>>(segs, n_segs, total_tuples, *lay, keys, ctrl);
-  return cudaGetLastError();
+                                            MapcCtrl* ctrl, int n_sms, uint32_t nreg, uint32_t max_emits,
+                                            cudaStream_t s) {
+  if (total_tiles == 0) return cudaSuccess;
+  const size_t wb = u32_mode ? 4 : 8;
+  const size_t smem = ((size_t)nreg * MAPC_GEN_V * MAPC_GEN_THREADS * wb + 15) / 16 * 16 +
+                      (size_t)MAPC_GEN_V * max_emits * MAPC_GEN_THREADS * 8;
+  const void* fn = u32_mode ? (const void*)mapk::k_generate2<uint32_t> : (const void*)mapk::k_generate2<uint64_t>;
+  static size_t attr[2] = {0, 0};
+  if (smem > 48 * 1024 && attr[u32_mode ? 0 : 1] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr[u32_mode ? 0 : 1] = smem;
+  }
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, smem);
+  if (occ < 1) occ = 1;
+  unsigned long long cap = (unsigned long long)n_sms * occ;
+  int grid = (int)(total_tiles < cap ? total_tiles : cap);
+  void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)lay, (void*)&keys, (void*)&ctrl, (void*)&nreg};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, smem, s);
+  return e;
 }
