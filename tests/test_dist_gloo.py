@@ -1,0 +1,84 @@
+"""Multi-GPU host logic on CPU: world_size-2 gloo process group.
+
+The GPU step is replaced by per-rank synthetic results (each rank would have
+processed chunks c % world == rank); what is tested is the cross-rank reduction
+of paper_2203_12878_b200.dist: summed counts and the lexicographic minimum
+witness, identical on every rank.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+CASES = {
+    # rank -> (verdict, n, racy, witness tuple or None)
+    "both_racy": {0: (1, 100, 3, (2, 0, 0, 7, 1, 4, 0, 1)), 1: (1, 50, 2, (1, 1, 0, 9, 0, 3, 1, 1))},
+    "one_racy": {0: (0, 10, 0, None), 1: (1, 20, 1, (5, 0, 3, 1, 2, 9, 1, 0))},
+    "none": {0: (0, 7, 0, None), 1: (0, 8, 0, None)},
+    "tie_on_prefix": {0: (1, 1, 1, (0, 0, 0, 4, 2, 5, 1, 1)), 1: (1, 1, 1, (0, 0, 0, 4, 2, 5, 0, 1))},
+}
+
+
+def _worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_12878_b200 import Result, Witness
+        from paper_2203_12878_b200.dist import reduce_results
+        v, n, racy, w = CASES[case][rank]
+        local = Result(verdict=v, n_accesses=n, racy_segments=racy, n_chunks=1, device_ms=1.0, gpu_launches=3)
+        if w:
+            local.witness = Witness(*w, array_name="")
+        out = reduce_results(local, ["A", "B"], device="cpu")
+        q.put((rank, out.verdict, out.n_accesses, out.racy_segments,
+               out.witness.as_tuple() if out.witness else None, out.witness.array_name if out.witness else None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_reduce_results_world2(case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rows = CASES[case]
+    wits = [w for (v, _, _, w) in rows.values() if v]
+    want_w = min(wits) if wits else None
+    want = (1 if wits else 0, sum(r[1] for r in rows.values()), sum(r[2] for r in rows.values()), want_w)
+    for (_, v, n, racy, w, name) in outs:
+        assert (v, n, racy, w) == want
+        if w:
+            assert name == ["A", "B"][w[1]]
+
+
+def test_chunk_sharding_covers_all_chunks():
+    # rank r runs chunks c with c % world == r: every chunk exactly once
+    import paper_2203_12878_b200 as mc
+    from workloads import config
+    inst = config("5a")
+    n = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).n_chunks()
+    for world in (1, 2, 4, 8):
+        seen = sorted(c for r in range(world) for c in range(n) if c % world == r)
+        assert seen == list(range(n))
+        per = [sum(1 for c in range(n) if c % world == r) for r in range(world)]
+        assert max(per) - min(per) <= 1
