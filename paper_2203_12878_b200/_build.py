@@ -15,6 +15,7 @@ SOURCES = [
     "kernels/generate.cu",
     "kernels/radix.cu",
     "kernels/detect.cu",
+    "kernels/rsweep.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh"]
 

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -40,6 +41,15 @@ cudaError_t mapc_launch_detect(const unsigned long long* bufA, const unsigned lo
                                uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
                                MapcSegState* last_frag, unsigned long long max_keys, int n_sms, cudaStream_t s);
 cudaError_t mapc_launch_chunk_finish(const MapcCtrl* ctrl, uint32_t n_passes, MapcChunkResult* out, cudaStream_t s);
+unsigned long long mapc_rsweep_tile();
+int mapc_rsweep_ranges(int n_sms);
+cudaError_t mapc_launch_hist_ranges(const unsigned long long* keys, MapcCtrl* ctrl, unsigned int* rhist,
+                                    uint32_t pay_bits, uint32_t n_passes, int G, cudaStream_t s);
+cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
+                                   unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
+int mapc_rsweep_fused();
+cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
+                               unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 }
 
 namespace {
@@ -66,7 +76,8 @@ struct Plan {
   std::vector<Chunk> chunks;
   size_t max_segs = 0;
   // scratch offsets
-  size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0;
+  size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
+  size_t rh_bytes = 0;
   size_t lb_bytes = 0, total = 0, stage_bytes = 0;
 };
 
@@ -284,6 +295,8 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_segs = off; off += align_up(std::max<size_t>(1, out.max_segs) * sizeof(MapcSeg));
   out.off_ctrl = off; off += align_up(sizeof(MapcCtrl));
   out.off_res = off; off += align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult));
+  out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
+  out.off_rh = off; off += align_up(out.rh_bytes);
   out.total = off;
   out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
   *P = std::move(out);
@@ -462,7 +475,13 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   auto* segs = (MapcSeg*)(base + P.off_segs);
   auto* ctrl = (MapcCtrl*)(base + P.off_ctrl);
   auto* res = (MapcChunkResult*)(base + P.off_res);
-
+  auto* rhist = (unsigned int*)(base + P.off_rh);
+  static int sort_mode = -1;     // 1 = static-range passes (default), 0 = decoupled look-back onesweep
+  if (sort_mode < 0) {
+    const char* e = getenv("MAPC_SORT");
+    sort_mode = (e && std::string(e) == "onesweep") ? 0 : 1;
+  }
+  const int G = mapc_rsweep_ranges(n_sms);
   uint32_t passes_total = 0;
   for (auto& ch : P.chunks) passes_total += ch.lay.n_passes;
   if (p->last_lookback != (void*)lookback || p->device != ex->device || p->epoch + passes_total >= 0xFFFF) {
@@ -519,19 +538,43 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
                               n_sms, ch.nreg, ch.max_emits, s));
       end(m);
     }
-    if (L.n_passes) {
-      m = begin(MAP_K_HIST);
-      CK(mapc_launch_hist(bufA, ctrl, L.pay_bits, L.n_passes, ch.bound, n_sms, s));
+    if (sort_mode == 1) {
+      if (L.n_passes) {
+        CK(cudaMemsetAsync(rhist, 0, P.rh_bytes, s));
+        m = begin(MAP_K_HIST);
+        CK(mapc_launch_hist_ranges(bufA, ctrl, rhist, L.pay_bits, L.n_passes, G, s));
+        end(m);
+      }
+      m = begin(MAP_K_SCAN);
+      CK(mapc_launch_digit_scan(ctrl, L.n_passes, s));
       end(m);
-    }
-    m = begin(MAP_K_SCAN);
-    CK(mapc_launch_digit_scan(ctrl, L.n_passes, s));
-    end(m);
-    for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
-      ++p->epoch;
-      m = begin(MAP_K_ONESWEEP);
-      CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.pay_bits + 8 * pass, p->epoch, ch.bound, n_sms, s));
+      for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
+        // the pass's per-range table: pass 0 from k_hist_ranges; later passes from the
+        // previous scatter (fused variants) or from one read of the pass's input
+        if (pass > 0) {
+          m = begin(MAP_K_HIST);
+          CK(mapc_launch_range_hist(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
+          end(m);
+        }
+        m = begin(MAP_K_ONESWEEP);
+        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
+        end(m);
+      }
+    } else {
+      if (L.n_passes) {
+        m = begin(MAP_K_HIST);
+        CK(mapc_launch_hist(bufA, ctrl, L.pay_bits, L.n_passes, ch.bound, n_sms, s));
+        end(m);
+      }
+      m = begin(MAP_K_SCAN);
+      CK(mapc_launch_digit_scan(ctrl, L.n_passes, s));
       end(m);
+      for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
+        ++p->epoch;
+        m = begin(MAP_K_ONESWEEP);
+        CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.pay_bits + 8 * pass, p->epoch, ch.bound, n_sms, s));
+        end(m);
+      }
     }
     m = begin(MAP_K_DETECT);
     ++launches;                        // detect + fixup

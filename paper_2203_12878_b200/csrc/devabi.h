@@ -18,6 +18,7 @@
 #define MAPC_MAX_PASSES 8        // 64-bit keys / 8-bit digits
 #define MAPC_RADIX_BITS 8
 #define MAPC_RADIX 256
+#define MAPC_MAX_RANGES 320          // static key ranges per radix pass (>= 2 x SM count)
 
 // Fixed registers: r0 = tid, r1 = bid (global block id), r2.. = k_0..k_{L-1}.
 #define MAPC_REG_TID 0
@@ -113,6 +114,11 @@ struct MapcCtrl {
   unsigned int sel[MAPC_MAX_PASSES + 1];   // buffer holding the keys before pass p (0 = A, 1 = B)
   unsigned int hist[MAPC_MAX_PASSES][MAPC_RADIX];
   unsigned long long offs[MAPC_MAX_PASSES][MAPC_RADIX];
+  // static-range radix passes (k_rsweep): CTA c owns keys [c*rng_L, (c+1)*rng_L)
+  unsigned int rng_L;
+  unsigned int first_active;                // first active pass (MAPC_MAX_PASSES if none)
+  unsigned int next_active[MAPC_MAX_PASSES];// next active pass after p (MAPC_MAX_PASSES if none)
+  MapcFastDiv rng_div;                      // divides a key position by rng_L
 };
 
 // Per-chunk result copied out by the last kernel of the chunk.

@@ -15,8 +15,6 @@
 // Segments spanning tiles: each tile records the state of its leading
 // continuation fragment and of its trailing open segment; k_detect_fixup lets
 // the tile that owns an open segment's head fold the following fragments.
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace mapk {
@@ -156,157 +154,6 @@ k_detect(const unsigned long long* __restrict__ bufA, const unsigned long long* 
   }
 }
 
-// ---- warp-streaming detect: registers + shuffles, no shared-memory tiles ----
-// Each warp owns a contiguous chunk of DW_CHUNK sorted keys and walks it 32 keys
-// per step (coalesced 256-byte loads).  Segment heads come from comparing each
-// key's sort field with its left neighbour (shfl_up); every head lane folds its
-// segment's (tid, kind) values by gathering the following lanes; the segment
-// still open at lane 31 is carried into the next step.  Chunk-spanning
-// segments use the same first/last fragment records as the tile version.
-constexpr int DW_CHUNK = 4096;
-constexpr int DW_WARPS = 8;
-
-__device__ __forceinline__ St shfl_st(const St& s, int src) {
-  St o;
-  o.m1 = __shfl_sync(0xffffffffu, s.m1, src);
-  o.m2 = __shfl_sync(0xffffffffu, s.m2, src);
-  o.w = __shfl_sync(0xffffffffu, s.w, src);
-  o.k1 = __shfl_sync(0xffffffffu, s.k1, src);
-  o.k2 = __shfl_sync(0xffffffffu, s.k2, src);
-  return o;
-}
-
-__global__ void __launch_bounds__(DW_WARPS * 32)
-k_detect_warp(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
-              MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid,
-              MapcSegState* __restrict__ first_frag, MapcSegState* __restrict__ last_frag) {
-  const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
-  const unsigned long long n = ctrl->n;
-  const unsigned long long n_chunks = (n + DW_CHUNK - 1) / DW_CHUNK;
-  const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
-  unsigned long long best = ~0ull, racy = 0;
-  const unsigned long long gw = (unsigned long long)blockIdx.x * DW_WARPS + (threadIdx.x >> 5);
-  const unsigned long long nw = (unsigned long long)gridDim.x * DW_WARPS;
-
-  for (unsigned long long c = gw; c < n_chunks; c += nw) {
-    const unsigned long long cs = c * DW_CHUNK;
-    const unsigned long long ce = min(cs + DW_CHUNK, n);
-    // state of the segment open at the start of the step (uniform across lanes)
-    St carry;
-    st_init(carry);
-    unsigned long long carry_sf = 0;
-    bool carry_is_first = false;    // carry is the chunk's leading continuation fragment
-    bool have_carry = false;
-    unsigned long long prev_sf = 0;
-    bool has_prev = cs > 0;
-    if (has_prev) prev_sf = keys[cs - 1] >> pay_bits;
-    if (lane == 0) { first_frag[c].valid = 0; last_frag[c].valid = 0; }
-    for (unsigned long long base = cs; base < ce; base += 32) {
-      const unsigned long long pos = base + lane;
-      const bool valid = pos < ce;
-      const unsigned long long key = valid ? ld_stream(keys + pos) : 0ull;
-      const unsigned long long sf = key >> pay_bits;
-      unsigned long long left = __shfl_up_sync(0xffffffffu, sf, 1);
-      if (lane == 0) left = prev_sf;
-      const bool head = valid && (((base == cs) && lane == 0) ? (!has_prev || sf != prev_sf) : (sf != left));
-      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-      const uint32_t hmask = __ballot_sync(0xffffffffu, head);
-      // pseudo-heads: real heads plus lane 0 (continuation of the carried segment)
-      const uint32_t pmask = hmask | 1u;
-      const bool phead = (pmask >> lane) & 1u;
-      const uint32_t after = pmask & ~((2u << lane) - 1u) & vmask;     // pseudo-heads after me
-      const int nxt = after ? __ffs(after) - 1 : (32 - __clz(vmask));   // end of my run (exclusive)
-      St f;
-      st_init(f);
-      const uint32_t tk = (uint32_t)(key >> 1) & tmask;
-      const uint32_t km = 1u << (key & 1u);
-      // gather-fold [lane, nxt) for pseudo-head lanes
-      int len = phead ? nxt - lane : 0;
-      int maxlen = len;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
-      for (int o = 0; o < maxlen; ++o) {
-        const uint32_t t2 = __shfl_sync(0xffffffffu, tk, (lane + o) & 31);
-        const uint32_t k2 = __shfl_sync(0xffffffffu, km, (lane + o) & 31);
-        if (o < len) st_add(f, t2, k2);
-      }
-      const bool lane0_head = hmask & 1u;
-      // lane 0's run either continues the carry or starts a new segment
-      const St f0 = shfl_st(f, 0);
-      if (lane0_head) {
-        if (have_carry) {                         // carried segment ended at this step's start
-          if (carry_is_first) {
-            if (lane == 0) to_frag(&first_frag[c], carry, carry_sf, true);
-          } else if (lane == 0) {
-            const unsigned long long wv = st_witness(carry, carry_sf, w_tid);
-            if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
-          }
-        }
-        carry = f0;
-        carry_sf = __shfl_sync(0xffffffffu, sf, 0);
-        carry_is_first = false;
-        have_carry = true;
-      } else if (vmask & 1u) {
-        if (!have_carry) {                        // chunk starts inside a segment
-          carry = f0;
-          carry_sf = __shfl_sync(0xffffffffu, sf, 0);
-          carry_is_first = true;
-          have_carry = true;
-        } else {
-          st_merge(carry, f0);
-        }
-      }
-      // segments headed at lanes > 0: complete ones are finalised here, the last (open) one becomes the carry
-      const uint32_t heads_hi = hmask & ~1u;
-      const int last_head = heads_hi ? 31 - __clz(heads_hi) : -1;
-      if (head && lane > 0 && lane != last_head) {
-        const unsigned long long wv = st_witness(f, sf, w_tid);
-        if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
-      }
-      if (last_head > 0) {
-        // the carried segment (lane 0's run) ended before last_head's... if lane 0 did not run to the end
-        if (have_carry) {
-          if (carry_is_first) {
-            if (lane == 0) to_frag(&first_frag[c], carry, carry_sf, true);
-          } else if (lane == 0) {
-            const unsigned long long wv = st_witness(carry, carry_sf, w_tid);
-            if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
-          }
-        }
-        carry = shfl_st(f, last_head);
-        carry_sf = __shfl_sync(0xffffffffu, sf, last_head);
-        carry_is_first = false;
-        have_carry = true;
-      }
-      prev_sf = __shfl_sync(0xffffffffu, sf, 31 - __clz(vmask));
-    }
-    // close the chunk: the carry continues into the next chunk iff its first key has the same sort field
-    if (have_carry) {
-      const bool cont = ce < n && (keys[ce] >> pay_bits) == carry_sf;
-      if (carry_is_first) {
-        if (lane == 0) to_frag(&first_frag[c], carry, carry_sf, !cont);
-      } else if (cont) {
-        if (lane == 0) to_frag(&last_frag[c], carry, carry_sf, false);
-      } else if (lane == 0) {
-        const unsigned long long wv = st_witness(carry, carry_sf, w_tid);
-        if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
-      }
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long ob = __shfl_down_sync(0xffffffffu, best, o);
-    const unsigned long long oc = __shfl_down_sync(0xffffffffu, racy, o);
-    best = ob < best ? ob : best;
-    racy += oc;
-  }
-  if (lane == 0) {
-    if (best != ~0ull) atomicMin(&ctrl->witness, best);
-    if (racy) atomicAdd(&ctrl->racy, racy);
-  }
-}
-
 // One thread per tile that owns an open segment head: fold continuation fragments.
 __global__ void k_detect_fixup(MapcCtrl* __restrict__ ctrl, uint32_t w_tid, const MapcSegState* __restrict__ first_frag,
                                const MapcSegState* __restrict__ last_frag, uint32_t tile) {
@@ -355,7 +202,7 @@ __global__ void k_chunk_finish(const MapcCtrl* __restrict__ ctrl, uint32_t n_pas
 
 }  // namespace mapk
 
-extern "C" unsigned long long mapc_detect_tile() { return mapk::DW_CHUNK < mapk::DT_TILE ? mapk::DW_CHUNK : mapk::DT_TILE; }
+extern "C" unsigned long long mapc_detect_tile() { return mapk::DT_TILE; }
 
 extern "C" cudaError_t mapc_launch_chunk_init(MapcCtrl* ctrl, unsigned long long n0, cudaStream_t s) {
   mapk::k_chunk_init<<<1, 256, 0, s>>>(ctrl, n0);
@@ -366,30 +213,16 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
                                           uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
                                           MapcSegState* last_frag, unsigned long long max_keys, int n_sms,
                                           cudaStream_t s) {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("MAPC_DETECT");
-    mode = e ? atoi(e) : 0;
-  }
-  const unsigned tile = mode == 1 ? (unsigned)mapk::DW_CHUNK : (unsigned)mapk::DT_TILE;
-  unsigned long long tiles = (max_keys + tile - 1) / tile;
-  if (mode == 1) {
-    unsigned long long blocks = (tiles + mapk::DW_WARPS - 1) / mapk::DW_WARPS;
-    unsigned long long cap = (unsigned long long)n_sms * 8;
-    int grid = (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
-    mapk::k_detect_warp<<<grid, mapk::DW_WARPS * 32, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid, first_frag,
-                                                            last_frag);
-  } else {
-    unsigned long long cap = (unsigned long long)n_sms * 8;
-    int grid = (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
-    mapk::k_detect<<<grid, mapk::DT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid, first_frag, last_frag);
-  }
+  const unsigned long long tiles = (max_keys + mapk::DT_TILE - 1) / mapk::DT_TILE;
+  const unsigned long long cap = (unsigned long long)n_sms * 8;
+  const int grid = (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
+  mapk::k_detect<<<grid, mapk::DT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid, first_frag, last_frag);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int g2 = (int)((tiles + 255) / 256);
   if (g2 < 1) g2 = 1;
   if (g2 > n_sms * 4) g2 = n_sms * 4;
-  mapk::k_detect_fixup<<<g2, 256, 0, s>>>(ctrl, w_tid, first_frag, last_frag, tile);
+  mapk::k_detect_fixup<<<g2, 256, 0, s>>>(ctrl, w_tid, first_frag, last_frag, (unsigned)mapk::DT_TILE);
   return cudaGetLastError();
 }
 

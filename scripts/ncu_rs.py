@@ -1,4 +1,3 @@
-"""ncu target for the radix pass: 5a at T=1, R=64 (2^28 keys, 4 passes)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2203_12878_b200 as mc
