@@ -107,6 +107,7 @@ struct MapcCtrl {
   unsigned long long n;            // keys generated
   unsigned long long witness;      // packed canonical witness (UINT64_MAX = DRF)
   unsigned long long racy;         // racy segments
+  unsigned long long racy_sf;      // smallest sort field of a racy segment (UINT64_MAX = none)
   unsigned int err;                // MAPC_ERR_* bits
   unsigned int n_sort_tiles;
   unsigned int tickets[MAPC_MAX_PASSES + 4];
@@ -135,10 +136,12 @@ struct MapcChunkResult {
 #define MAPC_ERR_LAYOUT 4u      // index outside the chunk layout (library bug guard)
 #define MAPC_ERR_WATCHDOG 8u    // look-back spin exceeded its bound (library bug guard)
 
-// Per-tile fragment state of the detect kernel.
+// Per-tile fragment state of the detect kernel: the racy test
+// of a segment only needs (has a write, min tid, max tid).
 struct MapcSegState {
-  uint32_t m1, m2, w;      // smallest tid, second smallest distinct tid, smallest writer tid
-  uint8_t k1, k2;          // kind masks of m1, m2 (bit0 rd, bit1 wr)
-  uint8_t valid, ends;     // fragment present; fragment ends inside this tile
-  unsigned long long sf;   // sort field of the fragment's segment
+  uint32_t first_tid, last_tid;  // tids of the fragment's first and last key
+  uint8_t wr;                    // fragment holds a write
+  uint8_t diff;                  // two adjacent keys of the fragment have different tids
+  uint8_t valid, ends;           // fragment present; fragment ends inside this chunk
+  unsigned long long sf;         // sort field of the fragment's segment
 };

@@ -3,14 +3,17 @@
 // A segment is a maximal run of keys with equal sort field, i.e. all access
 // values of one (phase, array, block, index) cell.  A segment is racy iff it
 // holds two DISTINCT tids and at least one write (
-// SPEC.md:423-426, 490).  Per segment the kernel folds an order-independent
-// state (m1, k1, m2, k2, w): smallest tid and its kind mask, second smallest
-// distinct tid and its mask, smallest writer tid.  Its canonical witness has a
-// closed form: t_lo = m1 always; if m1 writes, t_hi = m2 with
-// kinds the first feasible of (rd,wr),(wr,rd),(wr,wr); otherwise t_hi = w with
-// kinds (rd,wr).  Witnesses are packed so that unsigned order = lexicographic
-// order and combined with atomicMin, so the result does not depend on launch
-// or arrival order.
+// SPEC.md:423-426, 490), i.e. iff it holds a write and min tid != max tid.
+//
+// Pass 1 (k_detect + k_detect_fixup) folds only (has write, min tid, max tid)
+// per segment, counts racy segments and keeps the smallest racy sort field.
+// The canonical witness order is lexicographic with the sort field first, so
+// the witness lies in that one segment: pass 2 (k_witness, one CTA) folds the
+// full order-independent state (m1, k1, m2, k2, w) over it -- smallest tid and
+// its kind mask, second smallest distinct tid and its mask, smallest writer --
+// whose witness has a closed form: t_lo = m1; if m1 writes,
+// t_hi = m2 with kinds the first feasible of (rd,wr),(wr,rd),(wr,wr), else
+// t_hi = w with kinds (rd,wr).  Nothing depends on launch or arrival order.
 //
 // Segments spanning tiles: each tile records the state of its leading
 // continuation fragment and of its trailing open segment; k_detect_fixup lets
@@ -19,9 +22,6 @@
 
 namespace mapk {
 
-constexpr int DT_THREADS = 256;
-constexpr int DT_ITEMS = 16;
-constexpr int DT_TILE = DT_THREADS * DT_ITEMS;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 struct St {
@@ -71,37 +71,46 @@ __device__ __forceinline__ unsigned long long st_witness(const St& s, unsigned l
          (klo << 1) | khi;
 }
 
-__device__ __forceinline__ void to_frag(MapcSegState* f, const St& s, unsigned long long sf, bool ends) {
-  MapcSegState o;
-  o.m1 = s.m1; o.m2 = s.m2; o.w = s.w;
-  o.k1 = (uint8_t)s.k1; o.k2 = (uint8_t)s.k2;
-  o.valid = 1; o.ends = ends ? 1 : 0;
-  o.sf = sf;
-  *f = o;
-}
+// ---- pass 1: racy test per segment ------------------------------------------
+// racy(segment) <=> it holds a write and two distinct tids <=> it holds a write
+// and two ADJACENT keys with different tids (if all adjacent tids agree, all
+// agree).  A CTA stages a tile of sorted keys in shared memory; each head
+// position folds (first tid, last tid, adjacent-diff, write) over its segment,
+// counts racy segments and keeps the smallest racy sort field (keys are sorted,
+// and the witness order is lexicographic with the sort field first).
+constexpr int DW_CHUNK = 4096;          // keys per tile (and per fragment record)
+constexpr int DT_THREADS = 256;
 
-__device__ __forceinline__ St from_frag(const MapcSegState& f) {
-  St s;
-  s.m1 = f.m1; s.m2 = f.m2; s.w = f.w; s.k1 = f.k1; s.k2 = f.k2;
-  return s;
+struct Frag {
+  uint32_t first_tid, last_tid, wr, diff;
+  unsigned long long sf;
+};
+
+__device__ __forceinline__ void put_frag(MapcSegState* f, const Frag& c, bool ends) {
+  MapcSegState o;
+  o.first_tid = c.first_tid; o.last_tid = c.last_tid;
+  o.wr = (uint8_t)(c.wr != 0); o.diff = (uint8_t)(c.diff != 0);
+  o.valid = 1; o.ends = ends ? 1 : 0;
+  o.sf = c.sf;
+  *f = o;
 }
 
 __global__ void __launch_bounds__(DT_THREADS)
 k_detect(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
          MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid,
          MapcSegState* __restrict__ first_frag, MapcSegState* __restrict__ last_frag) {
-  __shared__ unsigned long long K[DT_TILE + 2];
-  __shared__ unsigned long long red_w[DT_THREADS / 32];
+  __shared__ unsigned long long K[DW_CHUNK + 2];
+  __shared__ unsigned long long red_s[DT_THREADS / 32];
   __shared__ unsigned long long red_c[DT_THREADS / 32];
   const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
   const unsigned long long n = ctrl->n;
-  const unsigned long long n_tiles = (n + DT_TILE - 1) / DT_TILE;
+  const unsigned long long n_tiles = (n + DW_CHUNK - 1) / DW_CHUNK;
   const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
   unsigned long long best = ~0ull, racy = 0;
 
   for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const unsigned long long tb = tile * DT_TILE;
-    const uint32_t tn = (uint32_t)min((unsigned long long)DT_TILE, n - tb);
+    const unsigned long long tb = tile * DW_CHUNK;
+    const uint32_t tn = (uint32_t)min((unsigned long long)DW_CHUNK, n - tb);
     for (uint32_t i = threadIdx.x; i < tn; i += DT_THREADS) K[i + 1] = ld_stream(keys + tb + i);
     if (threadIdx.x == 0) {
       K[0] = tb > 0 ? keys[tb - 1] : 0ull;
@@ -112,70 +121,111 @@ k_detect(const unsigned long long* __restrict__ bufA, const unsigned long long* 
     __syncthreads();
     const bool has_prev = tb > 0, has_next = tb + tn < n;
     const unsigned long long sf_next = K[tn + 1] >> pay_bits;
-    // thread-strided positions: a warp touches consecutive shared-memory words
     for (uint32_t i = threadIdx.x; i < tn; i += DT_THREADS) {
-      const unsigned long long sf = K[i + 1] >> pay_bits;
+      const unsigned long long key0 = K[i + 1];
+      const unsigned long long sf = key0 >> pay_bits;
       const bool head = (i == 0) ? (!has_prev || (K[0] >> pay_bits) != sf) : ((K[i] >> pay_bits) != sf);
       if (!head && i != 0) continue;
-      St s;
-      st_init(s);
-      uint32_t j = i;
+      Frag f;
+      f.first_tid = f.last_tid = (uint32_t)(key0 >> 1) & tmask;
+      f.wr = (uint32_t)key0 & 1u;
+      f.diff = 0;
+      f.sf = sf;
+      uint32_t j = i + 1;
       for (; j < tn; ++j) {
         const unsigned long long key = K[j + 1];
         if ((key >> pay_bits) != sf) break;
-        st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
+        const uint32_t t = (uint32_t)(key >> 1) & tmask;
+        f.diff |= (uint32_t)(t != f.last_tid);
+        f.last_tid = t;
+        f.wr |= (uint32_t)key & 1u;
       }
       const bool ends = j < tn || !has_next || sf_next != sf;
       if (head && ends) {
-        const unsigned long long wv = st_witness(s, sf, w_tid);
-        if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
+        if (f.wr && f.diff) { ++racy; best = min(best, sf); }
       } else if (head) {
-        to_frag(&last_frag[tile], s, sf, false);
+        put_frag(&last_frag[tile], f, false);
       } else {
-        to_frag(&first_frag[tile], s, sf, ends);
+        put_frag(&first_frag[tile], f, ends);
       }
     }
     __syncthreads();
   }
-  // block reduction: min witness, sum of racy segments
   for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long ob = __shfl_down_sync(0xffffffffu, best, o);
-    const unsigned long long oc = __shfl_down_sync(0xffffffffu, racy, o);
-    best = ob < best ? ob : best;
-    racy += oc;
+    best = min(best, __shfl_down_sync(0xffffffffu, best, o));
+    racy += __shfl_down_sync(0xffffffffu, racy, o);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) { red_w[w] = best; red_c[w] = racy; }
+  if (lane == 0) { red_s[w] = best; red_c[w] = racy; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int i = 1; i < DT_THREADS / 32; ++i) { best = red_w[i] < best ? red_w[i] : best; racy += red_c[i]; }
-    if (best != ~0ull) atomicMin(&ctrl->witness, best);
+    for (int i = 1; i < DT_THREADS / 32; ++i) { best = min(best, red_s[i]); racy += red_c[i]; }
+    if (best != ~0ull) atomicMin(&ctrl->racy_sf, best);
     if (racy) atomicAdd(&ctrl->racy, racy);
   }
 }
 
-// One thread per tile that owns an open segment head: fold continuation fragments.
-__global__ void k_detect_fixup(MapcCtrl* __restrict__ ctrl, uint32_t w_tid, const MapcSegState* __restrict__ first_frag,
-                               const MapcSegState* __restrict__ last_frag, uint32_t tile) {
+// One thread per chunk that owns an open segment head: fold continuation fragments.
+__global__ void k_detect_fixup(MapcCtrl* __restrict__ ctrl, const MapcSegState* __restrict__ first_frag,
+                               const MapcSegState* __restrict__ last_frag, uint32_t chunk) {
   const unsigned long long n = ctrl->n;
-  const unsigned long long n_tiles = (n + tile - 1) / tile;
+  const unsigned long long n_chunks = (n + chunk - 1) / chunk;
   unsigned long long best = ~0ull, racy = 0;
-  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks;
        t += (unsigned long long)gridDim.x * blockDim.x) {
     const MapcSegState lf = last_frag[t];
     if (!lf.valid) continue;
-    St s = from_frag(lf);
-    for (unsigned long long u = t + 1; u < n_tiles; ++u) {
+    uint32_t wr = lf.wr, diff = lf.diff, last = lf.last_tid;
+    for (unsigned long long u = t + 1; u < n_chunks; ++u) {
       const MapcSegState ff = first_frag[u];
       if (!ff.valid || ff.sf != lf.sf) { atomicOr(&ctrl->err, MAPC_ERR_LAYOUT); break; }
-      st_merge(s, from_frag(ff));
+      diff |= ff.diff | (uint32_t)(ff.first_tid != last);
+      wr |= ff.wr;
+      last = ff.last_tid;
       if (ff.ends) break;
     }
-    const unsigned long long wv = st_witness(s, lf.sf, w_tid);
-    if (wv != ~0ull) { ++racy; if (wv < best) best = wv; }
+    if (wr && diff) { ++racy; best = min(best, lf.sf); }
   }
-  if (best != ~0ull) atomicMin(&ctrl->witness, best);
+  if (best != ~0ull) atomicMin(&ctrl->racy_sf, best);
   if (racy) atomicAdd(&ctrl->racy, racy);
+}
+
+// ---- pass 2: canonical witness of the first racy segment ----------------------
+// One CTA: lower_bound of the segment in the sorted keys, then a parallel fold
+// of the full state (m1, k1, m2, k2, w) over the segment, closed-form witness.
+constexpr int WT_THREADS = 256;
+__global__ void __launch_bounds__(WT_THREADS)
+k_witness(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
+          MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid) {
+  const unsigned long long target = ctrl->racy_sf;
+  if (target == ~0ull) return;
+  const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
+  const unsigned long long n = ctrl->n;
+  const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
+  __shared__ unsigned long long s_lo;
+  __shared__ St part[WT_THREADS];
+  if (threadIdx.x == 0) {
+    unsigned long long lo = 0, hi = n;                  // first index with sf >= target
+    while (lo < hi) {
+      const unsigned long long mid = (lo + hi) >> 1;
+      if ((keys[mid] >> pay_bits) < target) lo = mid + 1; else hi = mid;
+    }
+    s_lo = lo;
+  }
+  __syncthreads();
+  St s;
+  st_init(s);
+  for (unsigned long long i = s_lo + threadIdx.x; i < n; i += WT_THREADS) {
+    const unsigned long long key = keys[i];
+    if ((key >> pay_bits) != target) break;
+    st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 1; t < WT_THREADS; ++t) st_merge(s, part[t]);
+    ctrl->witness = st_witness(s, target, w_tid);
+  }
 }
 
 __global__ void k_chunk_init(MapcCtrl* __restrict__ ctrl, unsigned long long n0) {
@@ -185,6 +235,7 @@ __global__ void k_chunk_init(MapcCtrl* __restrict__ ctrl, unsigned long long n0)
   __syncthreads();
   if (threadIdx.x == 0) {
     ctrl->witness = ~0ull;
+    ctrl->racy_sf = ~0ull;
     ctrl->n = n0;            // dense keys are placed directly; compaction appends after them
   }
 }
@@ -202,7 +253,7 @@ __global__ void k_chunk_finish(const MapcCtrl* __restrict__ ctrl, uint32_t n_pas
 
 }  // namespace mapk
 
-extern "C" unsigned long long mapc_detect_tile() { return mapk::DT_TILE; }
+extern "C" unsigned long long mapc_detect_tile() { return mapk::DW_CHUNK; }
 
 extern "C" cudaError_t mapc_launch_chunk_init(MapcCtrl* ctrl, unsigned long long n0, cudaStream_t s) {
   mapk::k_chunk_init<<<1, 256, 0, s>>>(ctrl, n0);
@@ -213,7 +264,7 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
                                           uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
                                           MapcSegState* last_frag, unsigned long long max_keys, int n_sms,
                                           cudaStream_t s) {
-  const unsigned long long tiles = (max_keys + mapk::DT_TILE - 1) / mapk::DT_TILE;
+  const unsigned long long tiles = (max_keys + mapk::DW_CHUNK - 1) / mapk::DW_CHUNK;
   const unsigned long long cap = (unsigned long long)n_sms * 8;
   const int grid = (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
   mapk::k_detect<<<grid, mapk::DT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid, first_frag, last_frag);
@@ -222,7 +273,10 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
   int g2 = (int)((tiles + 255) / 256);
   if (g2 < 1) g2 = 1;
   if (g2 > n_sms * 4) g2 = n_sms * 4;
-  mapk::k_detect_fixup<<<g2, 256, 0, s>>>(ctrl, w_tid, first_frag, last_frag, (unsigned)mapk::DT_TILE);
+  mapk::k_detect_fixup<<<g2, 256, 0, s>>>(ctrl, first_frag, last_frag, (unsigned)mapk::DW_CHUNK);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  mapk::k_witness<<<1, mapk::WT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid);
   return cudaGetLastError();
 }
 
