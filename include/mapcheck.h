@@ -99,7 +99,15 @@ typedef struct {
   uint32_t rank, world;       /* shard: process chunks c with c % world == rank
                                  (world 0 or 1 = all chunks; multi-GPU) */
   map_kernel_stats *stats;    /* optional per-kernel timings (NULL = off)            */
+  uint32_t flags;             /* MAP_GEN_* (generate path); 0 = automatic            */
 } map_exec;
+
+/* Generate path (map_exec.flags): the bytecode VM, or kernels specialised from
+ * the same bytecode with NVRTC at first use (cached per process).  AUTO picks
+ * the specialised kernels for plans of >= 2^26 accesses. */
+#define MAP_GEN_AUTO 0u
+#define MAP_GEN_VM 1u
+#define MAP_GEN_JIT 2u
 
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */

@@ -57,7 +57,10 @@ class _Stats(ctypes.Structure):
 class _Exec(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("scratch", ctypes.c_void_p),
                 ("scratch_bytes", ctypes.c_size_t), ("chunk_max_accesses", ctypes.c_uint64),
-                ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32), ("stats", ctypes.POINTER(_Stats))]
+                ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32), ("stats", ctypes.POINTER(_Stats)),
+                ("flags", ctypes.c_uint32)]
+
+GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
 
 
 class _Result(ctypes.Structure):
@@ -103,6 +106,8 @@ _lib.map_array_name.argtypes = [_P, ctypes.c_uint32]
 _lib.map_array_name.restype = ctypes.c_char_p
 _lib.map_debug_dump.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
 _lib.map_debug_dump.restype = ctypes.c_size_t
+_lib.map_debug_jit_check.argtypes = [_P, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_debug_jit_check.restype = ctypes.c_int
 _lib.mapc_test_fastdiv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
 _lib.mapc_test_fastdiv.restype = ctypes.c_uint32
 
@@ -207,6 +212,12 @@ class MapProgram:
         _lib.map_debug_dump(self._h, buf, n + 1)
         return buf.value.decode()
 
+    def jit_check(self, chunk_max_accesses: int = 0) -> str:
+        """NVRTC-compile the specialised generate module (no GPU needed); '' on success, else the log."""
+        buf = ctypes.create_string_buffer(4096)
+        r = _lib.map_debug_jit_check(self._h, int(chunk_max_accesses), buf, 4096)
+        return "" if r == 0 else (buf.value.decode(errors="replace") or f"status {r}")
+
     @property
     def info(self) -> Info:
         i = _Info()
@@ -228,13 +239,14 @@ class MapProgram:
         return c.value
 
     def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None,
-                    rank: int = 0, world: int = 1, profile: bool = False) -> Result:
+                    rank: int = 0, world: int = 1, profile: bool = False, gen: str = "auto") -> Result:
         """Run generate -> sort -> detect on one GPU (blocking).
 
         scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
         stream: a torch.cuda.Stream (default: the current stream);
         rank/world: process only chunks c with c % world == rank (multi-GPU sharding);
-        profile: record CUDA events around every launch and return per-kernel-class timings."""
+        profile: record CUDA events around every launch and return per-kernel-class timings;
+        gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised)."""
         import torch
         if not torch.cuda.is_available():
             raise MapError(6, "no CUDA device (there is no CPU fallback)")
@@ -247,7 +259,7 @@ class MapProgram:
         stats = _Stats() if profile else None
         ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
                    scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
-                   ctypes.pointer(stats) if stats is not None else None)
+                   ctypes.pointer(stats) if stats is not None else None, GEN_PATHS[gen])
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:

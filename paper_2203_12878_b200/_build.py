@@ -12,12 +12,13 @@ SOURCES = [
     "compiler/front.cpp",
     "compiler/compile.cpp",
     "capi/mapcheck.cpp",
+    "capi/jit.cpp",
     "kernels/generate.cu",
     "kernels/radix.cu",
     "kernels/detect.cu",
     "kernels/rsweep.cu",
 ]
-HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh"]
+HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "capi/jit.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -38,7 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-lcudart"]
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-lcudart", "-lnvrtc"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

@@ -1,0 +1,316 @@
+// jit.cpp -- specialised generate kernels: the chunk's bytecode lowered to
+// straight-line CUDA C and compiled with NVRTC for sm_100a at first use.
+//
+// The bytecode stays the compiler's output and the VM
+// (k_generate2) stays available (MAPC_GEN=vm).  The JIT removes the
+// interpreter's per-op dispatch and shared-memory register file: constants
+// (parameters, forS values, layout widths) become literals, divisions by
+// constants become multiply-shift sequences chosen by the compiler, and each
+// tuple's registers live in real registers.  Tuple -> key semantics, tile
+// mapping, dense slots and guarded-segment compaction are exactly those of
+// k_generate2 (generate.cu), so the key multiset is identical.
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <thread>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../devabi.h"
+#include "jit.h"
+
+namespace mapj {
+namespace {
+
+std::string lit(uint64_t v, bool u32) {
+  std::ostringstream o;
+  o << "(W)" << v << (u32 ? "u" : "ull");
+  return o.str();
+}
+
+std::string opnd(const MapcOp& op, bool a_side, bool u32) {
+  const bool imm = a_side ? (op.code & MAPC_A_IMM) : (op.code & MAPC_B_IMM);
+  if (imm) return lit(u32 ? (uint64_t)(uint32_t)op.imm : op.imm, u32);
+  return "r[" + std::to_string(a_side ? op.a : op.b) + "]";
+}
+
+// Straight-line body of one group program for one tuple (variables in scope:
+// W r[], bool act, bool valid, u32 tidv, u32 lbv, u32 e-counter, tuple index t).
+std::string program_body(const std::vector<MapcOp>& ops, bool u32) {
+  std::ostringstream s;
+  const char* WB = u32 ? "32u" : "64u";
+  for (const MapcOp& op : ops) {
+    const uint32_t c = op.code & MAPC_CODE_MASK;
+    const std::string A = opnd(op, true, u32), B = opnd(op, false, u32);
+    const std::string D = "r[" + std::to_string(op.dst) + "]";
+    switch (c) {
+      case VM_ADD: s << D << " = " << A << " + " << B << ";\n"; break;
+      case VM_SUB: s << "{ W a_ = " << A << ", b_ = " << B << "; " << D << " = a_ > b_ ? a_ - b_ : (W)0; }\n"; break;
+      case VM_MUL: s << D << " = " << A << " * " << B << ";\n"; break;
+      case VM_DIV:
+      case VM_MOD: {
+        const char* o = c == VM_DIV ? "/" : "%";
+        s << "{ W a_ = " << A << ", b_ = " << B << "; ";
+        if (op.aux & MAPC_AUX_FAULT) s << "if (b_ == 0 && act && valid) err |= " << MAPC_ERR_DIV0 << "u; ";
+        s << D << " = b_ ? (W)(a_ " << o << " b_) : (W)0; }\n";
+        break;
+      }
+      case VM_SHL: s << "{ W b_ = " << B << "; " << D << " = b_ >= " << WB << " ? (W)0 : (W)(" << A << " << b_); }\n"; break;
+      case VM_SHR: s << "{ W b_ = " << B << "; " << D << " = b_ >= " << WB << " ? (W)0 : (W)(" << A << " >> b_); }\n"; break;
+      case VM_MIN: s << "{ W a_ = " << A << ", b_ = " << B << "; " << D << " = a_ < b_ ? a_ : b_; }\n"; break;
+      case VM_MAX: s << "{ W a_ = " << A << ", b_ = " << B << "; " << D << " = a_ > b_ ? a_ : b_; }\n"; break;
+      case VM_BAND: s << D << " = " << A << " & " << lit(op.imm, u32) << ";\n"; break;
+      case VM_EQ: s << D << " = (W)(" << A << " == " << B << ");\n"; break;
+      case VM_NE: s << D << " = (W)(" << A << " != " << B << ");\n"; break;
+      case VM_LT: s << D << " = (W)(" << A << " < " << B << ");\n"; break;
+      case VM_LE: s << D << " = (W)(" << A << " <= " << B << ");\n"; break;
+      case VM_GT: s << D << " = (W)(" << A << " > " << B << ");\n"; break;
+      case VM_GE: s << D << " = (W)(" << A << " >= " << B << ");\n"; break;
+      case VM_LAND: s << D << " = (W)((" << A << " != 0) & (" << B << " != 0));\n"; break;
+      case VM_LOR: s << D << " = (W)((" << A << " != 0) | (" << B << " != 0));\n"; break;
+      case VM_LNOT: s << D << " = (W)(" << A << " == 0);\n"; break;
+      case VM_TRIP: {
+        const std::string step = (op.aux & MAPC_AUX_CONST) ? lit(op.aux & ~MAPC_AUX_CONST, u32)
+                                                           : "r[" + std::to_string(op.aux) + "]";
+        s << "{ W a_ = " << A << ", b_ = " << B << ", st_ = " << step << "; W sp_ = b_ > a_ ? b_ - a_ : (W)0; "
+          << D << " = sp_ == 0 ? (W)0 : (st_ == 1 ? sp_ : (W)((sp_ - 1) / (st_ ? st_ : (W)1) + 1)); }\n";
+        break;
+      }
+      case VM_MADK: s << D << " = " << A << " + r[" << op.aux << "] * " << B << ";\n"; break;
+      case VM_ACT: s << "act = " << A << " != 0;\n"; break;
+      case VM_MOVI: s << D << " = " << lit(op.imm, u32) << ";\n"; break;
+      case VM_EMIT:
+        s << "if (act && valid) { EMIT_KEY(" << A << ", " << (op.aux >> 1) << "ull, " << (op.aux & 1u) << "ull); }\n"
+          << "++e;\n";
+        break;
+      default: break;
+    }
+  }
+  return s.str();
+}
+
+const char* kPrelude = R"(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+struct FD { u32 d, m, s, pow2; };
+struct Seg {
+  u64 tuple_begin, n_tuples, tile_begin, key_begin, key_hi;
+  u32 prog_begin, prog_end, n_levels, b0, lb0, n_emits, dense, pad;
+  FD trip_div[8];
+  FD tid_div;
+};
+__device__ __forceinline__ u32 fdiv(u32 n, const FD& f) {
+  if (f.pow2) return n >> f.s;
+  u32 hi = __umulhi(f.m, n);
+  return (hi + ((n - hi) >> 1)) >> f.s;
+}
+template <int T>
+__device__ __forceinline__ u32 block_excl_scan(u32 v, u32* tmp, u32* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  u32 inc = v;
+  for (int o = 1; o < 32; o <<= 1) { u32 x = __shfl_up_sync(0xffffffffu, inc, o); if (lane >= o) inc += x; }
+  if (lane == 31) tmp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    u32 x = lane < T / 32 ? tmp[lane] : 0u, xi = x;
+    for (int o = 1; o < 32; o <<= 1) { u32 y = __shfl_up_sync(0xffffffffu, xi, o); if (lane >= o) xi += y; }
+    if (lane < T / 32) tmp[lane] = xi - x;
+    if (lane == T / 32 - 1) tmp[T / 32] = xi;
+  }
+  __syncthreads();
+  u32 r = tmp[w] + inc - v;
+  *total = tmp[T / 32];
+  __syncthreads();
+  return r;
+}
+)";
+
+struct Module {
+  cudaLibrary_t lib = nullptr;
+  std::vector<cudaKernel_t> kernels;
+};
+
+std::mutex g_mu;
+std::map<std::string, Module> g_cache;   // source text -> loaded module (process-wide)
+
+}  // namespace
+
+std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
+  static_assert(sizeof(MapcSeg) == 5 * 8 + 8 * 4 + 9 * 16, "Seg layout mirrored in the JIT prelude");
+  std::ostringstream s;
+  const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index
+    << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
+       "u64 cap) {\n"
+    << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
+    << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
+    << "  const u64 IDX_LO = " << ch.lay.idx_lo << "ull;\n"
+    << "  __shared__ u64 stage[" << (ch.max_emits ? ch.max_emits : 1) * V << " * " << T << "];\n"
+    << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
+    << "  __shared__ u64 s_base;\n"
+    << "  const int me = threadIdx.x;\n"
+    << "  u32 err = 0;\n"
+    << "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n"
+    << "    int lo = 0, hi = n_segs - 1;\n"
+    << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
+    << "    const Seg& sg = segs[lo];\n"
+    << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n"
+    << "    u32 cnt = 0;\n"
+    << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
+       "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
+       "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
+       "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
+       "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
+       "else { stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; } }\n"
+    << "    switch (sg.prog_begin) {\n";
+  for (const JitProgram& pg : ch.programs) {
+    s << "    case " << pg.prog_begin << "u: {\n"
+      << "#pragma unroll 1\n"
+      << "      for (int v = 0; v < " << V << "; ++v) {\n"
+      << "        const u32 t = tl0 + v * " << T << " + me;\n"
+      << "        const bool valid = t < sg.n_tuples;\n"
+      << "        u32 rem = valid ? t : 0u;\n"
+      << "        W r[" << MAPC_NREG << "];\n";
+    for (int l = (int)pg.n_levels - 1; l >= 0; --l)
+      s << "        { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
+        << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
+    s << "        const u32 qb = fdiv(rem, sg.tid_div);\n"
+      << "        const u32 tidv = rem - qb * sg.tid_div.d;\n"
+      << "        const u32 lbv = sg.lb0 + qb;\n"
+      << "        r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
+      << "        bool act = true;\n"
+      << "        u32 e = 0;\n"
+      << program_body(pg.ops, u32)
+      << "        (void)act; (void)e;\n"
+      << "      }\n"
+      << "      break; }\n";
+  }
+  s << "    default: break;\n"
+    << "    }\n"
+    << "#undef EMIT_KEY\n"
+    << "    if (!sg.dense) {\n"
+    << "      u32 total;\n"
+    << "      const u32 excl = block_excl_scan<" << T << ">(cnt, scan_tmp, &total);\n"
+    << "      if (me == 0) s_base = total ? atomicAdd(n_ctr, (u64)total) : 0ull;\n"
+    << "      __syncthreads();\n"
+    << "      const u64 obase = s_base;\n"
+    << "      for (u32 j = 0; j < cnt; ++j) { const u64 pos = obase + excl + j; "
+       "if (pos < cap) keys[pos] = stage[(size_t)j * " << T << " + me]; else err |= " << MAPC_ERR_CAPACITY << "u; }\n"
+    << "      __syncthreads();\n"
+    << "    }\n"
+    << "  }\n"
+    << "  if (err) atomicOr(err_flag, err);\n"
+    << "}\n";
+  return s.str();
+}
+
+std::string module_source(const std::vector<JitChunk>& chunks, bool u32) {
+  std::string src = kPrelude;
+  for (size_t i = 0; i < chunks.size(); ++i) src += chunk_kernel_source(chunks[i], (int)i, u32);
+  return src;
+}
+
+int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log) {
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "mapcheck_gen.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    *log = "nvrtcCreateProgram failed";
+    return 1;
+  }
+  const char* opts[] = {"-arch=sm_100a", "-default-device", "-std=c++17", "-lineinfo"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string l(n, '\0');
+    nvrtcGetProgramLog(prog, &l[0]);
+    *log = "NVRTC: " + std::string(nvrtcGetErrorString(r)) + "\n" + l.substr(0, 2000);
+    nvrtcDestroyProgram(&prog);
+    return 1;
+  }
+  size_t cubin_n = 0;
+  nvrtcGetCUBINSize(prog, &cubin_n);
+  cubin->resize(cubin_n);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  return 0;
+}
+
+// One NVRTC program per chunk, compiled in parallel; modules cached by source.
+int build_module(const std::vector<JitChunk>& chunks, bool u32, JitHandle* out, std::string* log) {
+  const size_t nc = chunks.size();
+  std::vector<std::string> srcs(nc);
+  for (size_t i = 0; i < nc; ++i) srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32);
+  std::vector<int> need;
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    for (size_t i = 0; i < nc; ++i)
+      if (!g_cache.count(srcs[i])) need.push_back((int)i);
+  }
+  std::vector<std::vector<char>> cubins(nc);
+  std::vector<std::string> logs(nc);
+  std::vector<int> rc(nc, 0);
+  {
+    std::atomic<size_t> next{0};
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < std::min<size_t>(hw, need.size()); ++w)
+      pool.emplace_back([&]() {
+        for (size_t k = next++; k < need.size(); k = next++) {
+          const int i = need[k];
+          rc[i] = compile_cubin(srcs[i], &cubins[i], &logs[i]);
+        }
+      });
+    for (auto& t : pool) t.join();
+  }
+  std::lock_guard<std::mutex> g(g_mu);
+  out->kernels.assign(nc, nullptr);
+  for (size_t i = 0; i < nc; ++i) {
+    auto it = g_cache.find(srcs[i]);
+    if (it == g_cache.end()) {
+      if (rc[i] != 0) {
+        *log = logs[i];
+        return 1;
+      }
+      Module m;
+      cudaError_t e = cudaLibraryLoadData(&m.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+      if (e != cudaSuccess) {
+        *log = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
+        return 1;
+      }
+      cudaKernel_t k;
+      e = cudaLibraryGetKernel(&k, m.lib, "gen_0");
+      if (e != cudaSuccess) {
+        *log = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e);
+        return 1;
+      }
+      m.kernels.push_back(k);
+      it = g_cache.emplace(srcs[i], std::move(m)).first;
+    }
+    out->kernels[i] = it->second.kernels[0];
+  }
+  return 0;
+}
+
+cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
+                         unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
+                         unsigned int* err_flag, unsigned long long cap, int n_sms, cudaStream_t s) {
+  if (total_tiles == 0) return cudaSuccess;
+  const void* fn = (const void*)h.kernels[chunk];
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
+  if (occ < 1) occ = 1;
+  const unsigned long long capb = (unsigned long long)n_sms * occ;
+  const int grid = (int)(total_tiles < capb ? total_tiles : capb);
+  void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
+                  (void*)&cap};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
+}
+
+}  // namespace mapj

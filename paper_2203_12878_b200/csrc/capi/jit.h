@@ -1,0 +1,37 @@
+// jit.h -- NVRTC-specialised generate kernels (see jit.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../devabi.h"
+
+namespace mapj {
+
+struct JitProgram {
+  uint32_t prog_begin;            // case label: the program's offset in the chunk's bytecode
+  uint32_t n_levels;
+  std::vector<MapcOp> ops;        // mode-independent ops (divisions by constants left to NVRTC)
+};
+
+struct JitChunk {
+  MapcLayout lay;
+  uint32_t max_emits;
+  std::vector<JitProgram> programs;
+};
+
+struct JitHandle {
+  std::vector<cudaKernel_t> kernels;   // one per chunk
+};
+
+std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32);
+std::string module_source(const std::vector<JitChunk>& chunks, bool u32);
+int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log);
+// Compile (or fetch from the process-wide cache) one module with a kernel per chunk.
+int build_module(const std::vector<JitChunk>& chunks, bool u32, JitHandle* out, std::string* log);
+cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
+                         unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
+                         unsigned int* err_flag, unsigned long long cap, int n_sms, cudaStream_t s);
+
+}  // namespace mapj

@@ -12,7 +12,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -22,6 +25,7 @@
 #include "../../../include/mapcheck.h"
 #include "../compiler/compiler.h"
 #include "../devabi.h"
+#include "jit.h"
 
 extern "C" {
 cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cudaStream_t s);
@@ -71,11 +75,14 @@ struct Chunk {
   uint32_t nreg = MAPC_REG_K0;              // VM registers used by the chunk's programs
   uint32_t max_emits = 0;                   // largest n_emits of a non-dense segment
   size_t stage_ops = 0, stage_segs = 0;     // offsets in the pinned staging buffer
+  mapj::JitChunk jit;                       // straight-line programs for the specialised generate
 };
 
 struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
+  bool jit_ready = false;
+  mapj::JitHandle jit;
   size_t max_segs = 0;
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
@@ -161,6 +168,7 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
       const mapc::InstanceInfo& in = C.inst[ii];
       for (const mapc::GroupProg& g : in.groups) {
         const uint32_t pb = (uint32_t)ch.ops.size();
+        ch.jit.programs.push_back(mapj::JitProgram{pb, g.n_levels, g.ops});
         for (const MapcOp& op : g.ops) {
           ch.ops.push_back(lower_op_for_mode(op, C.u32_mode));
           const uint32_t code = op.code & MAPC_CODE_MASK;
@@ -283,7 +291,11 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.stage_segs = stage;
     stage += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg), 64);
   }
-  for (auto& ch : out.chunks) ch.lay.cap = kcap;
+  for (auto& ch : out.chunks) {
+    ch.lay.cap = kcap;
+    ch.jit.lay = ch.lay;
+    ch.jit.max_emits = ch.max_emits;
+  }
   out.cap = kcap;
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
   const uint64_t det_tiles = (kcap + mapc_detect_tile() - 1) / mapc_detect_tile();
@@ -486,6 +498,20 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     sort_mode = (e && std::string(e) == "onesweep") ? 0 : 1;
   }
   const int G = mapc_rsweep_ranges(n_sms);
+  // generate path: NVRTC-specialised kernels for large plans (compile cost
+  // amortised), the bytecode VM otherwise (map_exec.flags, MAP_GEN_*).
+  const uint32_t gsel = ex->flags & 3u;
+  const int gen_mode = gsel == MAP_GEN_VM ? 0 : gsel == MAP_GEN_JIT ? 1 : (p->C.max_accesses >= (1ull << 26) ? 1 : 0);
+  if (gen_mode == 1 && !P.jit_ready && !P.chunks.empty()) {
+    std::vector<mapj::JitChunk> jc;
+    for (auto& ch : P.chunks) jc.push_back(ch.jit);
+    std::string log;
+    if (mapj::build_module(jc, p->C.u32_mode, &P.jit, &log) != 0) {
+      p->last_error = "specialised generate: " + log;
+      return MAP_E_CUDA;
+    }
+    P.jit_ready = true;
+  }
   uint32_t passes_total = 0;
   for (auto& ch : P.chunks) passes_total += ch.lay.n_passes;
   if (p->last_lookback != (void*)lookback || p->device != ex->device || p->epoch + passes_total >= 0xFFFF) {
@@ -538,8 +564,12 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     end(m);
     if (ch.total_tiles) {
       m = begin(MAP_K_GENERATE);
-      CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
-                              n_sms, ch.nreg, ch.max_emits, s));
+      if (gen_mode == 1)
+        CK(mapj::launch_chunk(P.jit, c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n, &ctrl->err,
+                              L.cap, n_sms, s));
+      else
+        CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                                n_sms, ch.nreg, ch.max_emits, s));
       end(m);
     }
     if (sort_mode == 1) {
@@ -717,6 +747,37 @@ size_t map_debug_dump(const map_program* p, char* buf, size_t cap) {
     buf[n] = 0;
   }
   return out.size();
+}
+
+// Generate + NVRTC-compile the specialised generate module without loading it
+// (no GPU needed): 0 on success, else writes the compiler log.  Test hook.
+int map_debug_jit_check(const map_program* cp, uint64_t chunk_max_accesses, char* log, size_t cap) {
+  map_program* p = const_cast<map_program*>(cp);
+  if (!p) return -1;
+  if (ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p)) != MAP_OK) return -1;
+  std::string l;
+  int r = 0;
+  std::vector<std::thread> pool;
+  std::mutex mu;
+  std::atomic<size_t> next{0};
+  auto& chunks = p->plan.chunks;
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  for (unsigned w = 0; w < std::min<size_t>(hw, chunks.size()); ++w)
+    pool.emplace_back([&]() {
+      for (size_t i = next++; i < chunks.size(); i = next++) {
+        std::vector<char> cubin;
+        std::string li;
+        std::vector<mapj::JitChunk> one{chunks[i].jit};
+        if (mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode), &cubin, &li) != 0) {
+          std::lock_guard<std::mutex> g(mu);
+          r = 1;
+          l = li;
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  put_diag(l, log, cap);
+  return r;
 }
 
 // Last error text of a program (diagnostics for the Python binding).

@@ -42,6 +42,28 @@ def test_configs_scaled_small_chunks(name, sizes):
     same(p.check_races(chunk_max_accesses=unit), oracle.check_instance(inst))
 
 
+@pytest.mark.parametrize("name,sizes", CASES[::2], ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES[::2])])
+def test_generate_paths_agree(name, sizes):
+    # the NVRTC-specialised generate and the bytecode VM give the same result
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    for gen in ("vm", "jit"):
+        same(p.check_races(gen=gen), o)
+
+
+def test_fuzz_corpus_jit():
+    bad = []
+    for seed in range(0, 120, 3):
+        inst, _ = fuzz.random_instance(seed)
+        o = oracle.check_instance(inst, threads=1)
+        r = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).check_races(gen="jit")
+        got = (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments)
+        if got != (o.verdict, o.witness, o.n_accesses, o.n_racy_segments):
+            bad.append((seed, inst.src))
+    assert not bad, bad[:3]
+
+
 def test_fuzz_corpus():
     n = int(os.environ.get("MAPCHECK_GPU_FUZZ", "400"))
     bad = []
