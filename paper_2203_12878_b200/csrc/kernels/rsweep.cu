@@ -65,7 +65,20 @@ k_hist_ranges(const unsigned long long* __restrict__ keys, MapcCtrl* __restrict_
     const unsigned long long cnt = r1 - r0;
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + r0);   // r0 % 2 == 0
     const unsigned long long n2 = cnt >> 1;
-    for (unsigned long long i = threadIdx.x; i < n2; i += RH_THREADS) {
+    constexpr int U = 4;                                 // loads in flight per thread
+    unsigned long long i = threadIdx.x;
+    for (; i + (U - 1) * RH_THREADS < n2; i += U * RH_THREADS) {
+      ulonglong2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream2(k2 + i + u * RH_THREADS);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        for (uint32_t p = 0; p < n_passes; ++p) {
+          atomicAdd(&h[p][(v[u].x >> (pay_bits + 8 * p)) & 0xFF], 1u);
+          atomicAdd(&h[p][(v[u].y >> (pay_bits + 8 * p)) & 0xFF], 1u);
+        }
+    }
+    for (; i < n2; i += RH_THREADS) {
       const ulonglong2 v = ld_stream2(k2 + i);
       for (uint32_t p = 0; p < n_passes; ++p) {
         atomicAdd(&h[p][(v.x >> (pay_bits + 8 * p)) & 0xFF], 1u);
@@ -117,13 +130,23 @@ k_range_hist(const unsigned long long* __restrict__ bufA, const unsigned long lo
     } else {                                         // digit bytes written by the previous pass
       const uint4* b16 = reinterpret_cast<const uint4*>(ndig + r0);   // r0 % 4096 == 0
       const unsigned long long n16 = (r1 - r0) >> 4;
-      for (unsigned long long i = threadIdx.x; i < n16; i += RH_THREADS) {
-        const uint4 v = b16[i];
-        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+      constexpr int U = 4;                               // loads in flight per thread
+      for (unsigned long long i0 = threadIdx.x; i0 < n16; i0 += U * RH_THREADS) {
+        uint4 v[U];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int u = 0; u < U; ++u) {
+          const unsigned long long i = i0 + u * RH_THREADS;
+          v[u] = i < n16 ? b16[i] : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) atomicAdd(&h[(w4[q] >> (8 * b)) & 0xFF], 1u);
+        for (int u = 0; u < U; ++u) {
+          if (i0 + u * RH_THREADS >= n16) break;
+          const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) atomicAdd(&h[(w4[q] >> (8 * b)) & 0xFF], 1u);
+        }
       }
       for (unsigned long long i = r0 + (n16 << 4) + threadIdx.x; i < r1; i += RH_THREADS) atomicAdd(&h[ndig[i]], 1u);
     }
