@@ -49,13 +49,11 @@ unsigned long long mapc_rsweep_tile();
 int mapc_rsweep_ranges(int n_sms);
 cudaError_t mapc_launch_hist_ranges(const unsigned long long* keys, MapcCtrl* ctrl, unsigned int* rhist,
                                     uint32_t pay_bits, uint32_t n_passes, int G, cudaStream_t s);
-cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB,
-                                   const unsigned char* ndig, MapcCtrl* ctrl, unsigned int* rhist, uint32_t pass,
-                                   uint32_t pay_bits, int G, cudaStream_t s);
+cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
+                                   unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 int mapc_rsweep_fused();
 cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
-                               unsigned int* rhist, unsigned char* ndig, uint32_t pass, uint32_t pay_bits, int G,
-                               cudaStream_t s);
+                               unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 }
 
 namespace {
@@ -86,7 +84,7 @@ struct Plan {
   size_t max_segs = 0;
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
-  size_t rh_bytes = 0, off_nd = 0;
+  size_t rh_bytes = 0;
   size_t lb_bytes = 0, total = 0, stage_bytes = 0;
 };
 
@@ -311,7 +309,6 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_res = off; off += align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult));
   out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
   out.off_rh = off; off += align_up(out.rh_bytes);
-  out.off_nd = off; off += align_up(kcap + 64);        // next-pass digit bytes
   out.total = off;
   out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
   *P = std::move(out);
@@ -491,7 +488,6 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   auto* ctrl = (MapcCtrl*)(base + P.off_ctrl);
   auto* res = (MapcChunkResult*)(base + P.off_res);
   auto* rhist = (unsigned int*)(base + P.off_rh);
-  auto* ndig = (unsigned char*)(base + P.off_nd);
   static int sort_mode = -1;     // 1 = static-range passes (default), 0 = decoupled look-back onesweep
   if (sort_mode < 0) {
     const char* e = getenv("MAPC_SORT");
@@ -587,11 +583,11 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         // previous scatter (fused variants) or from one read of the pass's input
         if (pass > 0) {
           m = begin(MAP_K_HIST);
-          CK(mapc_launch_range_hist(bufA, bufB, ndig, ctrl, rhist, pass, L.pay_bits, G, s));
+          CK(mapc_launch_range_hist(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
           end(m);
         }
         m = begin(MAP_K_ONESWEEP);
-        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, ndig, pass, L.pay_bits, G, s));
+        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
         end(m);
       }
     } else {

@@ -101,13 +101,15 @@ k_hist_ranges(const unsigned long long* __restrict__ keys, MapcCtrl* __restrict_
 // Per-range table of pass p, read from the pass's input buffer (pass 0's table
 // comes from k_hist_ranges).  Used when the scatter does not fuse the next
 // pass's table (2 CTAs per SM).
+// Per-range table of pass p, read from the pass's input buffer (pass 0's table
+// comes from k_hist_ranges; fused variants get later tables from the scatter).
 __global__ void __launch_bounds__(RH_THREADS)
 k_range_hist(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
-             const unsigned char* __restrict__ ndig, MapcCtrl* __restrict__ ctrl, unsigned int* __restrict__ rhist,
-             uint32_t p, uint32_t pay_bits, uint32_t fused) {
+             MapcCtrl* __restrict__ ctrl, unsigned int* __restrict__ rhist, uint32_t p, uint32_t pay_bits,
+             uint32_t fused) {
   if (p == 0 || !ctrl->active[p]) return;
-  const bool first = p == ctrl->first_active;
-  if (fused && !first) return;                       // produced by the previous active pass's scatter
+  if (fused && p != ctrl->first_active) return;      // produced by the previous active pass's scatter
+  const unsigned long long* __restrict__ keys = ctrl->sel[p] ? bufB : bufA;
   __shared__ uint32_t h[MAPC_RADIX];
   for (int i = threadIdx.x; i < MAPC_RADIX; i += RH_THREADS) h[i] = 0;
   __syncthreads();
@@ -115,41 +117,26 @@ k_range_hist(const unsigned long long* __restrict__ bufA, const unsigned long lo
   const uint32_t L = ctrl->rng_L;
   const unsigned long long r0 = (unsigned long long)blockIdx.x * L;
   const unsigned long long r1 = min(r0 + L, n);
+  const uint32_t sh = pay_bits + 8 * p;
   if (r0 < r1) {
-    if (first) {                                     // keys have not moved yet: read them
-      const unsigned long long* __restrict__ keys = ctrl->sel[p] ? bufB : bufA;
-      const uint32_t sh = pay_bits + 8 * p;
-      const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + r0);
-      const unsigned long long n2 = (r1 - r0) >> 1;
-      for (unsigned long long i = threadIdx.x; i < n2; i += RH_THREADS) {
-        const ulonglong2 v = ld_stream2(k2 + i);
-        atomicAdd(&h[(v.x >> sh) & 0xFF], 1u);
-        atomicAdd(&h[(v.y >> sh) & 0xFF], 1u);
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + r0);
+    const unsigned long long n2 = (r1 - r0) >> 1;
+    constexpr int U = 4;                                 // loads in flight per thread
+    for (unsigned long long i0 = threadIdx.x; i0 < n2; i0 += U * RH_THREADS) {
+      ulonglong2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long i = i0 + u * RH_THREADS;
+        v[u] = i < n2 ? ld_stream2(k2 + i) : make_ulonglong2(0, 0);
       }
-      if (((r1 - r0) & 1) && threadIdx.x == 0) atomicAdd(&h[(keys[r1 - 1] >> sh) & 0xFF], 1u);
-    } else {                                         // digit bytes written by the previous pass
-      const uint4* b16 = reinterpret_cast<const uint4*>(ndig + r0);   // r0 % 4096 == 0
-      const unsigned long long n16 = (r1 - r0) >> 4;
-      constexpr int U = 4;                               // loads in flight per thread
-      for (unsigned long long i0 = threadIdx.x; i0 < n16; i0 += U * RH_THREADS) {
-        uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const unsigned long long i = i0 + u * RH_THREADS;
-          v[u] = i < n16 ? b16[i] : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (i0 + u * RH_THREADS >= n16) break;
-          const uint32_t w4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) atomicAdd(&h[(w4[q] >> (8 * b)) & 0xFF], 1u);
-        }
+      for (int u = 0; u < U; ++u) {
+        if (i0 + u * RH_THREADS >= n2) break;
+        atomicAdd(&h[(v[u].x >> sh) & 0xFF], 1u);
+        atomicAdd(&h[(v[u].y >> sh) & 0xFF], 1u);
       }
-      for (unsigned long long i = r0 + (n16 << 4) + threadIdx.x; i < r1; i += RH_THREADS) atomicAdd(&h[ndig[i]], 1u);
     }
+    if (((r1 - r0) & 1) && threadIdx.x == 0) atomicAdd(&h[(keys[r1 - 1] >> sh) & 0xFF], 1u);
   }
   __syncthreads();
   if (threadIdx.x < MAPC_RADIX)
@@ -177,7 +164,7 @@ struct RsSmem {
 template <int THREADS, int ITEMS, bool FUSE_NEXT, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__ bufB, MapcCtrl* __restrict__ ctrl,
-         unsigned int* __restrict__ rhist, unsigned char* __restrict__ ndig, uint32_t pass, uint32_t pay_bits) {
+         unsigned int* __restrict__ rhist, uint32_t pass, uint32_t pay_bits) {
   using Sm = RsSmem<THREADS, ITEMS>;
   constexpr int TILE = Sm::TILE, WARPS = Sm::WARPS;
   static_assert(TILE == RS_TILE || TILE * 2 == RS_TILE || TILE == RS_TILE * 2, "range length is a multiple of RS_TILE");
@@ -189,7 +176,6 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
   const uint32_t shift = pay_bits + 8 * pass;
   const uint32_t nxt = ctrl->next_active[pass];
   const bool has_next = FUSE_NEXT && nxt < MAPC_MAX_PASSES;
-  const bool write_nd = !FUSE_NEXT && nxt < MAPC_MAX_PASSES;   // next pass's digit bytes for k_range_hist
   const uint32_t nshift = pay_bits + 8 * (nxt < MAPC_MAX_PASSES ? nxt : 0);
   const unsigned long long* __restrict__ src = ctrl->sel[pass] ? bufB : bufA;
   unsigned long long* __restrict__ dst = ctrl->sel[pass] ? bufA : bufB;
@@ -302,7 +288,6 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
       const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
       const unsigned long long p = S.gbase[d] + i;
       dst[p] = key;
-      if (write_nd) ndig[p] = (unsigned char)(key >> nshift);
       if (has_next)
         atomicAdd(&tab[fastdiv((uint32_t)p, rdiv) * MAPC_RADIX + ((uint32_t)(key >> nshift) & 0xFFu)], 1u);
     }
@@ -360,9 +345,9 @@ extern "C" cudaError_t mapc_launch_hist_ranges(const unsigned long long* keys, M
 
 // Per-pass range table when the variant does not fuse it into the previous scatter.
 extern "C" cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB,
-                                              const unsigned char* ndig, MapcCtrl* ctrl, unsigned int* rhist,
-                                              uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s) {
-  mapk::k_range_hist<<<G, mapk::RH_THREADS, 0, s>>>(bufA, bufB, ndig, ctrl, rhist, pass, pay_bits,
+                                              MapcCtrl* ctrl, unsigned int* rhist, uint32_t pass, uint32_t pay_bits,
+                                              int G, cudaStream_t s) {
+  mapk::k_range_hist<<<G, mapk::RH_THREADS, 0, s>>>(bufA, bufB, ctrl, rhist, pass, pay_bits,
                                                    mapk::rs_pick().fused ? 1u : 0u);
   return cudaGetLastError();
 }
@@ -370,8 +355,7 @@ extern "C" cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, co
 extern "C" int mapc_rsweep_fused() { return mapk::rs_pick().fused ? 1 : 0; }
 
 extern "C" cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
-                                          unsigned int* rhist, unsigned char* ndig, uint32_t pass, uint32_t pay_bits,
-                                          int G, cudaStream_t s) {
+                                          unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s) {
   const mapk::RsVariant V = mapk::rs_pick();
   const size_t smem = V.smem + (V.fused ? (size_t)G * MAPC_RADIX * 4 : 0);
   static size_t attr = 0;
@@ -380,6 +364,6 @@ extern "C" cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned lon
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  void* args[] = {&bufA, &bufB, &ctrl, &rhist, &ndig, &pass, &pay_bits};
+  void* args[] = {&bufA, &bufB, &ctrl, &rhist, &pass, &pay_bits};
   return cudaLaunchKernel(V.fn, dim3(G), dim3(V.threads), args, smem, s);
 }
