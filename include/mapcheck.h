@@ -173,6 +173,13 @@ const char *map_status_str(map_status s);
  * bound), counts_out[world] on the HOST.  Keys use the chunk layout
  * (map_chunk_count / map_key_layout). */
 map_status map_chunk_count(const map_program *p, uint64_t chunk_max_accesses, uint32_t *n_chunks);
+typedef struct {
+  uint32_t phase_lo, phase_hi;   /* inclusive range of barrier phases                 */
+  uint32_t block_lo, block_hi;   /* [block_lo, block_hi)                              */
+  uint64_t bound;                /* upper bound on the chunk's keys (key buffer size)  */
+  uint32_t sort_bits, n_passes;  /* sort-field width and radix passes                  */
+} map_chunk_desc;
+map_status map_chunk_info(const map_program *p, uint64_t chunk_max_accesses, uint32_t chunk, map_chunk_desc *out);
 map_status map_generate_bucketed(map_program *p, const map_exec *ex, uint32_t rank, uint32_t world,
                                  uint32_t chunk, void *keys_out, uint64_t *counts_out);
 /* Sort + detect n device-resident keys of chunk `chunk`; packed witness of the

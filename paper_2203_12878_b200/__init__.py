@@ -38,7 +38,7 @@ STATUS = {
 EXPORTS = (
     "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
     "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
-    "map_sort_detect", "map_unpack_witness", "map_array_name",
+    "map_sort_detect", "map_unpack_witness", "map_array_name", "map_chunk_info",
 )
 
 
@@ -75,6 +75,12 @@ class _Witness(ctypes.Structure):
                 ("kind_lo", ctypes.c_uint8), ("kind_hi", ctypes.c_uint8), ("array_name", ctypes.c_char_p)]
 
 
+class _ChunkDesc(ctypes.Structure):
+    _fields_ = [("phase_lo", ctypes.c_uint32), ("phase_hi", ctypes.c_uint32), ("block_lo", ctypes.c_uint32),
+                ("block_hi", ctypes.c_uint32), ("bound", ctypes.c_uint64), ("sort_bits", ctypes.c_uint32),
+                ("n_passes", ctypes.c_uint32)]
+
+
 class _Info(ctypes.Structure):
     _fields_ = [("n_phases", ctypes.c_uint32), ("n_arrays", ctypes.c_uint32), ("n_instances", ctypes.c_uint32),
                 ("n_groups", ctypes.c_uint32), ("max_accesses", ctypes.c_uint64),
@@ -102,6 +108,16 @@ _lib.map_last_error.argtypes = [_P]
 _lib.map_last_error.restype = ctypes.c_char_p
 _lib.map_chunk_count.argtypes = [_P, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint32)]
 _lib.map_chunk_count.restype = ctypes.c_int
+_lib.map_generate_bucketed.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                      ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
+_lib.map_generate_bucketed.restype = ctypes.c_int
+_lib.map_sort_detect.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint64,
+                                 ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+_lib.map_sort_detect.restype = ctypes.c_int
+_lib.map_unpack_witness.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint64, ctypes.POINTER(_Witness)]
+_lib.map_unpack_witness.restype = ctypes.c_int
+_lib.map_chunk_info.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_ChunkDesc)]
+_lib.map_chunk_info.restype = ctypes.c_int
 _lib.map_array_name.argtypes = [_P, ctypes.c_uint32]
 _lib.map_array_name.restype = ctypes.c_char_p
 _lib.map_debug_dump.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
@@ -196,6 +212,52 @@ class MapProgram:
         if h and _lib is not None:
             _lib.map_program_free(h)
             self._h = None
+
+    def chunk_info(self, chunk: int, chunk_max_accesses: int = 0) -> dict:
+        d = _ChunkDesc()
+        st = _lib.map_chunk_info(self._h, int(chunk_max_accesses), int(chunk), ctypes.byref(d))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        return {f: getattr(d, f) for f, _ in _ChunkDesc._fields_}
+
+    # ---- stage API (key-exchange multi-GPU mode) ------------
+    def _exec(self, scratch, stream, chunk_max_accesses):
+        import torch
+        dev = scratch.device.index if scratch.device.index is not None else torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        return _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
+                     scratch.numel() * scratch.element_size(), int(chunk_max_accesses), 0, 1, None, 0)
+
+    def generate_bucketed(self, chunk: int, rank: int, world: int, keys_out, scratch, stream=None,
+                          chunk_max_accesses: int = 0):
+        """Rank `rank` of `world` generates its slice of chunk `chunk`; keys laid out by destination
+        rank in keys_out (uint64/int64 CUDA tensor >= the chunk bound).  Returns per-destination counts."""
+        ex = self._exec(scratch, stream, chunk_max_accesses)
+        counts = (ctypes.c_uint64 * world)()
+        st = _lib.map_generate_bucketed(self._h, ctypes.byref(ex), rank, world, chunk,
+                                        ctypes.c_void_p(keys_out.data_ptr()), counts)
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        return [int(c) for c in counts]
+
+    def sort_detect(self, chunk: int, keys, n: int, scratch, stream=None, chunk_max_accesses: int = 0):
+        """Sort + detect n device keys of chunk `chunk`: (packed witness or None, racy segment count)."""
+        ex = self._exec(scratch, stream, chunk_max_accesses)
+        w, r = ctypes.c_uint64(), ctypes.c_uint64()
+        st = _lib.map_sort_detect(self._h, ctypes.byref(ex), chunk, ctypes.c_void_p(keys.data_ptr() if n else 0),
+                                  int(n), ctypes.byref(w), ctypes.byref(r))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        return (None if w.value == 2**64 - 1 else w.value), r.value
+
+    def unpack_witness(self, chunk: int, packed: int) -> Witness:
+        w = _Witness()
+        st = _lib.map_unpack_witness(self._h, chunk, packed, ctypes.byref(w))
+        if st != 0:
+            raise MapError(st, "bad packed witness")
+        return Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
+                       w.array_name.decode())
 
     def array_names(self):
         out = []

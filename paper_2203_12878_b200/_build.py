@@ -17,6 +17,7 @@ SOURCES = [
     "kernels/radix.cu",
     "kernels/detect.cu",
     "kernels/rsweep.cu",
+    "kernels/exchange.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "capi/jit.h"]
 

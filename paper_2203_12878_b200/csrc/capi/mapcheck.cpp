@@ -29,9 +29,16 @@
 
 extern "C" {
 cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cudaStream_t s);
-cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tiles,
-                                 const MapcLayout* lay, int u32_mode, unsigned long long* keys, MapcCtrl* ctrl,
-                                 int n_sms, uint32_t nreg, uint32_t max_emits, cudaStream_t s);
+cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long tile_lo,
+                                 unsigned long long tile_hi, const MapcLayout* lay, int u32_mode,
+                                 unsigned long long* keys, MapcCtrl* ctrl, int n_sms, uint32_t nreg,
+                                 uint32_t max_emits, uint32_t force_compact, cudaStream_t s);
+int mapc_bucket_max_world();
+cudaError_t mapc_launch_bucket_count(const unsigned long long* keys, const MapcCtrl* ctrl, uint32_t pay_bits,
+                                     uint32_t world, unsigned long long* counts, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_bucket_scatter(const unsigned long long* keys, const MapcCtrl* ctrl, uint32_t pay_bits,
+                                       uint32_t world, unsigned long long* cursors, unsigned long long* out,
+                                       int n_sms, cudaStream_t s);
 cudaError_t mapc_launch_hist(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t n_passes,
                              unsigned long long max_keys, int n_sms, cudaStream_t s);
 cudaError_t mapc_launch_digit_scan(MapcCtrl* ctrl, uint32_t n_passes, cudaStream_t s);
@@ -84,7 +91,7 @@ struct Plan {
   size_t max_segs = 0;
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
-  size_t rh_bytes = 0;
+  size_t rh_bytes = 0, off_xch = 0;
   size_t lb_bytes = 0, total = 0, stage_bytes = 0;
 };
 
@@ -309,6 +316,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_res = off; off += align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult));
   out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
   out.off_rh = off; off += align_up(out.rh_bytes);
+  out.off_xch = off; off += align_up(2 * 64 * sizeof(unsigned long long));   // exchange counts + cursors
   out.total = off;
   out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
   *P = std::move(out);
@@ -564,8 +572,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         CK(mapj::launch_chunk(P.jit, c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n, &ctrl->err,
                               L.cap, n_sms, s));
       else
-        CK(mapc_launch_generate(segs, (int)ch.segs.size(), ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
-                                n_sms, ch.nreg, ch.max_emits, s));
+        CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                                n_sms, ch.nreg, ch.max_emits, 0, s));
       end(m);
     }
     if (sort_mode == 1) {
@@ -693,12 +701,152 @@ map_status map_chunk_count(const map_program* cp, uint64_t chunk_max_accesses, u
   return MAP_OK;
 }
 
-map_status map_generate_bucketed(map_program*, const map_exec*, uint32_t, uint32_t, uint32_t, void*, uint64_t*) {
-  return MAP_E_ARG;
+}  // extern "C"
+
+namespace {
+
+// Device pointers of the scratch layout (shared by the stage API entry points).
+struct Dev {
+  unsigned long long *bufA, *bufB, *lookback;
+  MapcSegState *ff, *lf;
+  MapcSeg* segs;
+  MapcCtrl* ctrl;
+  MapcChunkResult* res;
+  unsigned int* rhist;
+  unsigned long long* xch;
+  int n_sms, G;
+  cudaStream_t s;
+};
+
+map_status stage_setup(map_program* p, const map_exec* ex, uint32_t chunk, Dev* d) {
+  if (!p || !ex) return MAP_E_ARG;
+  const uint64_t cap = ex->chunk_max_accesses ? ex->chunk_max_accesses : default_cap(p);
+  map_status st = ensure_plan(p, cap);
+  if (st != MAP_OK) return st;
+  Plan& P = p->plan;
+  if (chunk >= P.chunks.size()) return MAP_E_ARG;
+  if (!ex->scratch || ex->scratch_bytes < P.total) {
+    p->last_error = "scratch too small: need " + std::to_string(P.total) + " bytes";
+    return MAP_E_NOMEM;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    p->last_error = "no CUDA device";
+    return MAP_E_CUDA;
+  }
+  CK(cudaSetDevice(ex->device));
+  CK(cudaDeviceGetAttribute(&d->n_sms, cudaDevAttrMultiProcessorCount, ex->device));
+  d->G = mapc_rsweep_ranges(d->n_sms);
+  d->s = (cudaStream_t)ex->stream;
+  unsigned char* base = (unsigned char*)ex->scratch;
+  d->bufA = (unsigned long long*)(base + P.off_a);
+  d->bufB = (unsigned long long*)(base + P.off_b);
+  d->lookback = (unsigned long long*)(base + P.off_lb);
+  d->ff = (MapcSegState*)(base + P.off_ff);
+  d->lf = (MapcSegState*)(base + P.off_lf);
+  d->segs = (MapcSeg*)(base + P.off_segs);
+  d->ctrl = (MapcCtrl*)(base + P.off_ctrl);
+  d->res = (MapcChunkResult*)(base + P.off_res);
+  d->rhist = (unsigned int*)(base + P.off_rh);
+  d->xch = (unsigned long long*)(base + P.off_xch);
+  return MAP_OK;
 }
 
-map_status map_sort_detect(map_program*, const map_exec*, uint32_t, void*, uint64_t, uint64_t*, uint64_t*) {
-  return MAP_E_ARG;
+}  // namespace
+
+extern "C" {
+
+map_status map_chunk_info(const map_program* cp, uint64_t chunk_max_accesses, uint32_t chunk, map_chunk_desc* out) {
+  if (!cp || !out) return MAP_E_ARG;
+  map_program* p = const_cast<map_program*>(cp);
+  map_status st = ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p));
+  if (st != MAP_OK) return st;
+  if (chunk >= p->plan.chunks.size()) return MAP_E_ARG;
+  const Chunk& ch = p->plan.chunks[chunk];
+  out->phase_lo = ch.phase_lo;
+  out->phase_hi = ch.phase_hi;
+  out->block_lo = (uint32_t)ch.b_lo;
+  out->block_hi = (uint32_t)ch.b_hi;
+  out->bound = ch.bound;
+  out->sort_bits = ch.lay.sort_bits;
+  out->n_passes = ch.lay.n_passes;
+  return MAP_OK;
+}
+
+// Rank `rank` of `world` generates the generate tiles [rank*T/world, (rank+1)*T/world)
+// of chunk `chunk` (all keys compacted, VM path) and lays them out by destination
+// rank dest = hi64(splitmix64(sort field) * world) in keys_out (device, >= the
+// chunk's bound); counts_out[world] (host) receives the per-destination counts.
+map_status map_generate_bucketed(map_program* p, const map_exec* ex, uint32_t rank, uint32_t world, uint32_t chunk,
+                                 void* keys_out, uint64_t* counts_out) {
+  if (!keys_out || !counts_out || world == 0 || rank >= world || (int)world > mapc_bucket_max_world()) return MAP_E_ARG;
+  Dev d;
+  map_status st = stage_setup(p, ex, chunk, &d);
+  if (st != MAP_OK) return st;
+  Plan& P = p->plan;
+  const Chunk& ch = P.chunks[chunk];
+  const MapcLayout& L = ch.lay;
+  CK(cudaMemcpyAsync(d.segs, ch.segs.data(), ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, d.s));
+  CK(mapc_upload_ops(ch.ops.data(), ch.ops.size(), d.s));
+  CK(mapc_launch_chunk_init(d.ctrl, 0, d.s));
+  const uint64_t t0 = ch.total_tiles * rank / world, t1 = ch.total_tiles * (rank + 1) / world;
+  CK(mapc_launch_generate(d.segs, (int)ch.segs.size(), t0, t1, &L, p->C.u32_mode ? 1 : 0, d.bufA, d.ctrl, d.n_sms,
+                          ch.nreg, MAPC_MAX_EMITS, 1, d.s));
+  CK(cudaMemsetAsync(d.xch, 0, 2 * 64 * sizeof(unsigned long long), d.s));
+  CK(mapc_launch_bucket_count(d.bufA, d.ctrl, L.pay_bits, world, d.xch, d.n_sms, d.s));
+  std::vector<unsigned long long> cnt(world);
+  CK(cudaMemcpyAsync(cnt.data(), d.xch, world * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d.s));
+  CK(cudaStreamSynchronize(d.s));
+  std::vector<unsigned long long> cur(world);
+  unsigned long long acc = 0;
+  for (uint32_t r = 0; r < world; ++r) { cur[r] = acc; acc += cnt[r]; }
+  CK(cudaMemcpyAsync(d.xch + 64, cur.data(), world * sizeof(unsigned long long), cudaMemcpyHostToDevice, d.s));
+  CK(mapc_launch_bucket_scatter(d.bufA, d.ctrl, L.pay_bits, world, d.xch + 64, (unsigned long long*)keys_out, d.n_sms,
+                                d.s));
+  MapcChunkResult r{};
+  CK(mapc_launch_chunk_finish(d.ctrl, 0, d.res + chunk, d.s));
+  CK(cudaMemcpyAsync(&r, d.res + chunk, sizeof(r), cudaMemcpyDeviceToHost, d.s));
+  CK(cudaStreamSynchronize(d.s));
+  if (r.err & MAPC_ERR_DIV0) { p->last_error = "division or modulo by zero on a reached path"; return MAP_E_ARITH; }
+  if (r.err) { p->last_error = "internal consistency check failed"; return MAP_E_RANGE; }
+  for (uint32_t q = 0; q < world; ++q) counts_out[q] = cnt[q];
+  return MAP_OK;
+}
+
+// Sort + detect n keys (device) of chunk `chunk`, e.g. the keys a rank received
+// in the exchange; the chunk's packed canonical witness (UINT64_MAX = DRF) and
+// racy-segment count are written to the host.
+map_status map_sort_detect(map_program* p, const map_exec* ex, uint32_t chunk, void* keys, uint64_t n,
+                           uint64_t* packed_witness, uint64_t* racy_segments) {
+  if ((!keys && n) || !packed_witness || !racy_segments) return MAP_E_ARG;
+  Dev d;
+  map_status st = stage_setup(p, ex, chunk, &d);
+  if (st != MAP_OK) return st;
+  Plan& P = p->plan;
+  const Chunk& ch = P.chunks[chunk];
+  const MapcLayout& L = ch.lay;
+  if (n > P.cap) return MAP_E_NOMEM;
+  CK(mapc_launch_chunk_init(d.ctrl, n, d.s));
+  if (n) CK(cudaMemcpyAsync(d.bufA, keys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, d.s));
+  if (L.n_passes) {
+    CK(cudaMemsetAsync(d.rhist, 0, P.rh_bytes, d.s));
+    CK(mapc_launch_hist_ranges(d.bufA, d.ctrl, d.rhist, L.pay_bits, L.n_passes, d.G, d.s));
+  }
+  CK(mapc_launch_digit_scan(d.ctrl, L.n_passes, d.s));
+  for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
+    if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.pay_bits, d.G, d.s));
+    CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.pay_bits, d.G, d.s));
+  }
+  CK(mapc_launch_detect(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.w_tid, d.ff, d.lf, std::max<uint64_t>(n, 1),
+                        d.n_sms, d.s));
+  CK(mapc_launch_chunk_finish(d.ctrl, L.n_passes, d.res + chunk, d.s));
+  MapcChunkResult r{};
+  CK(cudaMemcpyAsync(&r, d.res + chunk, sizeof(r), cudaMemcpyDeviceToHost, d.s));
+  CK(cudaStreamSynchronize(d.s));
+  if (r.err) { p->last_error = "internal consistency check failed"; return MAP_E_RANGE; }
+  *packed_witness = r.witness;
+  *racy_segments = r.racy;
+  return MAP_OK;
 }
 
 map_status map_unpack_witness(const map_program* p, uint32_t chunk, uint64_t packed, map_witness* out) {

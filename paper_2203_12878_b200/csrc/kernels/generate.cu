@@ -34,8 +34,9 @@ struct VmWidth<uint64_t> { static constexpr uint32_t bits = 64; };
 // are compacted through shared memory with one global atomicAdd per tile.
 template <typename W>
 __global__ void __launch_bounds__(MAPC_GEN_THREADS)
-k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long total_tiles, MapcLayout lay,
-            unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t nreg) {
+k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long tile_lo, unsigned long long tile_hi,
+            MapcLayout lay, unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t nreg,
+            uint32_t force_compact) {
   constexpr int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   constexpr uint32_t WB = VmWidth<W>::bits;
   extern __shared__ __align__(16) unsigned char gsm[];
@@ -47,13 +48,14 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long tot
   uint32_t err = 0;
 #define RG(r, v) R[((size_t)(r) * V + (v)) * T + me]
 
-  for (unsigned long long tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+  for (unsigned long long tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
     int lo = 0, hi = n_segs - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
     }
     const MapcSeg& sg = segs[lo];
+    const bool dense = sg.dense && !force_compact;    // stage API: every key goes through compaction
     const uint32_t tl0 = (uint32_t)(tile - sg.tile_begin) * (uint32_t)(V * T);
     const uint32_t L = sg.n_levels;
     uint32_t tidv[V], lbv[V];
@@ -161,7 +163,7 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long tot
             if (lay.w_index < 64 && (idx >> lay.w_index) != 0) err |= MAPC_ERR_LAYOUT;
             const unsigned long long sf = sg.key_hi + arr + ((unsigned long long)lbv[v] << lay.w_index) + idx;
             const unsigned long long key = (sf << lay.pay_bits) | ((unsigned long long)tidv[v] << 1) | kind;
-            if (sg.dense) {
+            if (dense) {
               keys[sg.key_begin + (unsigned long long)e * sg.n_tuples + tl0 + v * T + me] = key;
             } else {
               stage[(size_t)cnt * T + me] = key;
@@ -177,7 +179,7 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long tot
 #undef BV
 #undef VLOOP
     }
-    if (!sg.dense) {                                  // uniform across the CTA
+    if (!dense) {                                     // uniform across the CTA
       uint32_t total;
       const uint32_t excl = block_excl_scan<T>(cnt, scan_tmp, &total);
       if (me == 0) s_base = total ? atomicAdd(&ctrl->n, (unsigned long long)total) : 0ull;
@@ -203,11 +205,12 @@ extern "C" cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cud
   return cudaMemcpyToSymbolAsync(mapk::c_ops, host_ops, n_ops * sizeof(MapcOp), 0, cudaMemcpyHostToDevice, s);
 }
 
-extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long total_tiles,
-                                            const MapcLayout* lay, int u32_mode, unsigned long long* keys,
-                                            MapcCtrl* ctrl, int n_sms, uint32_t nreg, uint32_t max_emits,
-                                            cudaStream_t s) {
-  if (total_tiles == 0) return cudaSuccess;
+extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long tile_lo,
+                                            unsigned long long tile_hi, const MapcLayout* lay, int u32_mode,
+                                            unsigned long long* keys, MapcCtrl* ctrl, int n_sms, uint32_t nreg,
+                                            uint32_t max_emits, uint32_t force_compact, cudaStream_t s) {
+  if (tile_hi <= tile_lo) return cudaSuccess;
+  const unsigned long long total_tiles = tile_hi - tile_lo;
   const size_t wb = u32_mode ? 4 : 8;
   const size_t smem = ((size_t)nreg * MAPC_GEN_V * MAPC_GEN_THREADS * wb + 15) / 16 * 16 +
                       (size_t)MAPC_GEN_V * max_emits * MAPC_GEN_THREADS * 8;
@@ -223,7 +226,7 @@ extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, uns
   if (occ < 1) occ = 1;
   unsigned long long cap = (unsigned long long)n_sms * occ;
   int grid = (int)(total_tiles < cap ? total_tiles : cap);
-  void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)lay, (void*)&keys, (void*)&ctrl, (void*)&nreg};
-  cudaError_t e = cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, smem, s);
-  return e;
+  void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&tile_lo, (void*)&tile_hi, (void*)lay, (void*)&keys,
+                  (void*)&ctrl, (void*)&nreg, (void*)&force_compact};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, smem, s);
 }

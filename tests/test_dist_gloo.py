@@ -82,3 +82,75 @@ def test_chunk_sharding_covers_all_chunks():
         assert seen == list(range(n))
         per = [sum(1 for c in range(n) if c % world == r) for r in range(world)]
         assert max(per) - min(per) <= 1
+
+
+# ---- key-exchange mode orchestration (dist.check_races_exchange) -------------
+
+class FakeProg:
+    """Stands in for MapProgram on CPU: chunk c of rank r generates keys
+    1000*c + 10*k + r (k < 5 + r); destination = key % world.  sort_detect
+    records what arrived and reports its minimum key as the 'witness'."""
+
+    def __init__(self, world):
+        self.world = world
+        self.received = []
+
+    def n_chunks(self, chunk_max_accesses=0):
+        return 3
+
+    def chunk_info(self, chunk, chunk_max_accesses=0):
+        return {"bound": 64}
+
+    def array_names(self):
+        return ["A"]
+
+    def generate_bucketed(self, chunk, rank, world, out, scratch, stream=None, chunk_max_accesses=0):
+        keys = [1000 * chunk + 10 * k + rank for k in range(5 + rank)]
+        by = [[x for x in keys if x % world == d] for d in range(world)]
+        flat = [x for b in by for x in b]
+        out[:len(flat)] = torch.tensor(flat, dtype=torch.int64)
+        return [len(b) for b in by]
+
+    def sort_detect(self, chunk, keys, n, scratch, stream=None, chunk_max_accesses=0):
+        got = keys[:n].tolist()
+        self.received.append((chunk, sorted(got)))
+        return (min(got) if got else None), len(got)
+
+    def unpack_witness(self, chunk, packed):
+        from paper_2203_12878_b200 import Witness
+        return Witness(chunk, 0, 0, packed, 0, 1, 0, 1, "A")
+
+
+def _xworker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2203_12878_b200.dist import check_races_exchange
+        prog = FakeProg(world)
+        out = check_races_exchange(prog, torch.empty(1))
+        q.put((rank, prog.received, out.verdict, out.n_accesses, out.racy_segments, out.witness.as_tuple()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_routing(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xworker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    total = sum(5 + r for r in range(world)) * 3
+    for rank, received, verdict, n, racy, w in outs:
+        for chunk, keys in received:
+            want = sorted(1000 * chunk + 10 * k + s for s in range(world) for k in range(5 + s)
+                          if (1000 * chunk + 10 * k + s) % world == rank)
+            assert keys == want                      # every key arrives once, at its hash owner
+        assert (verdict, n, racy) == (1, total, total)
+        assert w == (0, 0, 0, 0, 0, 1, 0, 1)         # global min over chunks and ranks

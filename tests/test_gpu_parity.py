@@ -155,3 +155,55 @@ def test_multi_dim_grid_and_block():
     src = "params W; wr[(tid / W) * W + (tid + 1) % W]; sync; rd[bid % 3]"
     for g, b in [((2, 3, 1), (4, 2, 1)), ((1, 1, 2), (2, 2, 2))]:
         same(mc.check(src, grid=g, block=b, params={"W": 4}), oracle.check(src, g, b, {"W": 4}))
+
+
+def _fake_exchange(p, world, chunk_max=0):
+    """Key-exchange mode with `world` logical ranks run one after another on
+    one GPU: each rank generates + buckets its tuple slice, the buckets for
+    each destination are concatenated (what all_to_all_single delivers), and
+    each destination sorts + detects.  Returns (verdict, witness, n, racy)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    scratch = torch.empty(p.scratch_bytes(chunk_max), dtype=torch.uint8, device=dev)
+    best, n_total, racy_total = None, 0, 0
+    for c in range(p.n_chunks(chunk_max)):
+        bound = max(1, p.chunk_info(c, chunk_max)["bound"])
+        parts = [[] for _ in range(world)]
+        for r in range(world):
+            out = torch.empty(bound, dtype=torch.int64, device=dev)
+            counts = p.generate_bucketed(c, r, world, out, scratch, chunk_max_accesses=chunk_max)
+            assert sum(counts) <= bound
+            off = 0
+            for d, k in enumerate(counts):
+                parts[d].append(out[off:off + k].clone())
+                off += k
+        for d in range(world):
+            keys = torch.cat(parts[d]) if parts[d] else torch.empty(0, dtype=torch.int64, device=dev)
+            n = keys.numel()
+            packed, racy = p.sort_detect(c, keys if n else torch.empty(1, dtype=torch.int64, device=dev), n,
+                                         scratch, chunk_max_accesses=chunk_max)
+            n_total += n
+            racy_total += racy
+            if packed is not None:
+                w = p.unpack_witness(c, packed).as_tuple()
+                best = w if best is None or w < best else best
+    return (1 if best else 0), best, n_total, racy_total
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("name", ["1a", "2b", "3b", "4b", "5b"])
+def test_exchange_mode_matches_oracle(name, world):
+    sizes = dict(CASES)[name] if name in dict(CASES) else {}
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    assert o.status == 0
+    assert _fake_exchange(p, world) == (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
+
+
+def test_exchange_mode_many_chunks():
+    inst = config("4b", n=1 << 14, bs=256)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    unit = max(1, p.info.max_unit_accesses)
+    assert _fake_exchange(p, 3, unit) == (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
