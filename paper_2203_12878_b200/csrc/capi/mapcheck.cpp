@@ -303,7 +303,8 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   }
   out.cap = kcap;
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
-  const uint64_t det_tiles = (kcap + mapc_detect_tile() - 1) / mapc_detect_tile();
+  const uint64_t det_tiles = std::max<uint64_t>((kcap + mapc_detect_tile() - 1) / mapc_detect_tile(),
+                                                MAPC_DETECT_MAX_UNITS);
   size_t off = 0;
   out.off_a = off; off += align_up(kcap * 8 + 64);     // + slack: bulk copies round up to 16 B
   out.off_b = off; off += align_up(kcap * 8 + 64);

@@ -138,6 +138,7 @@ struct MapcChunkResult {
 
 // Per-tile fragment state of the detect kernel: the racy test
 // of a segment only needs (has a write, min tid, max tid).
+#define MAPC_DETECT_MAX_UNITS 8192   /* fragment records: max(tiles, warp ranges) */
 struct MapcSegState {
   uint32_t first_tid, last_tid;  // tids of the fragment's first and last key
   uint8_t wr;                    // fragment holds a write

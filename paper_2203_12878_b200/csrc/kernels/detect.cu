@@ -18,6 +18,8 @@
 // Segments spanning tiles: each tile records the state of its leading
 // continuation fragment and of its trailing open segment; k_detect_fixup lets
 // the tile that owns an open segment's head fold the following fragments.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mapk {
@@ -190,6 +192,242 @@ __global__ void k_detect_fixup(MapcCtrl* __restrict__ ctrl, const MapcSegState* 
   if (racy) atomicAdd(&ctrl->racy, racy);
 }
 
+// ---- pass 1, warp-streaming form (default) ----------------------------------
+// Each warp owns a contiguous range of `unit` keys (a multiple of 512) and
+// streams it 32 keys per step, one key per lane, coalesced.  Per step the
+// segment structure is three ballots: H (lane starts a segment), D (lane's tid
+// differs from its predecessor's inside one segment), W (lane writes).  A head
+// lane whose segment closes inside the step owns it: racy <=> D and W meet the
+// lanes [head, next head).  The segment still open at the end of a step is
+// carried (its key, and whether it has seen a diff / a write) -- a uniform
+// update from the masks, no per-segment serial walk.  Ranges are joined by the
+// same fragment records as the tiled form (first_frag: the range's leading
+// continuation; last_frag: its trailing open segment), folded by the fixup.
+constexpr int DWS_THREADS = 256;
+constexpr int DWS_V = 4;                        // 4-key steps per lane per batch (512 keys per warp)
+
+__device__ __forceinline__ unsigned long long detect_unit(unsigned long long n, unsigned long long nw) {
+  unsigned long long u = (n + nw - 1) / nw;
+  u = (u + 511ull) & ~511ull;
+  return u < 512ull ? 512ull : u;
+}
+
+struct WsCarry {
+  unsigned long long key;      // key of the previous position
+  bool lead, diff, wr;         // open segment: range's leading continuation? seen a tid diff? a write?
+  bool lead_closed, lead_diff, lead_wr;
+  uint32_t racy;
+  unsigned long long best;
+};
+
+// One 32-key step; lanes >= nvalid hold no key.  Collectives run converged.
+template <bool FULL>
+__device__ __forceinline__ void ws_step(WsCarry& c, unsigned long long k, uint32_t nvalid, uint32_t lane,
+                                        uint32_t pay_bits, unsigned long long tmask) {
+  unsigned long long pk = __shfl_up_sync(0xFFFFFFFFu, k, 1);
+  if (lane == 0) pk = c.key;
+  const unsigned long long x = k ^ pk;
+  const bool valid = FULL || lane < nvalid;
+  const bool head = valid && (x >> pay_bits) != 0;
+  const bool diff = valid && !head && ((x >> 1) & tmask) != 0;
+  const uint32_t H = __ballot_sync(0xFFFFFFFFu, head);
+  const uint32_t D = __ballot_sync(0xFFFFFFFFu, diff);
+  const uint32_t W = __ballot_sync(0xFFFFFFFFu, valid && (k & 1ull));
+  const uint32_t V = FULL ? 0xFFFFFFFFu : (nvalid == 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u));
+  // the carried segment covers lanes [0, first head)
+  const uint32_t m0 = H ? ((H & (0u - H)) - 1u) : V;
+  const bool cd = c.diff || (D & m0) != 0, cw = c.wr || (W & m0) != 0;
+  if (H) {
+    if (c.lead) {
+      c.lead_closed = true; c.lead_diff = cd; c.lead_wr = cw; c.lead = false;
+    } else if (lane == 0 && cd && cw) {
+      ++c.racy; c.best = min(c.best, c.key >> pay_bits);
+    }
+    // head lanes whose segment closes in this step own it
+    const uint32_t upto = (2u << lane) - 1u;        // lanes <= lane (lane 31: all)
+    const uint32_t later = H & ~upto;
+    if (head && later) {
+      const uint32_t m = ((later & (0u - later)) - 1u) & ~((1u << lane) - 1u);
+      if ((D & m) && (W & m)) { ++c.racy; c.best = min(c.best, k >> pay_bits); }
+    }
+    const uint32_t o = 31u - __clz(H);            // the last segment becomes the carry
+    const uint32_t m = V & ~((1u << o) - 1u);
+    c.diff = (D & m) != 0;
+    c.wr = (W & m) != 0;
+  } else {
+    c.diff = cd; c.wr = cw;
+  }
+  c.key = __shfl_sync(0xFFFFFFFFu, k, FULL ? 31 : nvalid - 1);
+}
+
+// Four consecutive keys per lane per step (128 keys per warp): in-lane
+// segments close in registers; only segments crossing lanes use the ballots.
+// Keys are sorted by sort field, so "new segment" is one 64-bit compare:
+// sf(a) != sf(p) <=> a > (p | payload mask).
+template <bool P32>
+__device__ __forceinline__ void ws_step4(WsCarry& c, const unsigned long long (&a)[4], uint32_t lane,
+                                         uint32_t pay_bits, unsigned long long paymask, unsigned long long tmask) {
+  unsigned long long prev = __shfl_up_sync(0xFFFFFFFFu, a[3], 1);
+  if (lane == 0) prev = c.key;
+  bool in_lead = true, cd = false, cw = false, ld = false, lw = false;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long p = i ? a[i - 1] : prev;
+    const bool head = a[i] > (p | paymask);
+    const bool diff = P32 ? (((uint32_t)a[i] ^ (uint32_t)p) & ((uint32_t)tmask << 1)) != 0
+                          : (((a[i] ^ p) >> 1) & tmask) != 0;
+    const bool w = (a[i] & 1ull) != 0;
+    if (head) {
+      if (in_lead) { ld = cd; lw = cw; in_lead = false; }
+      else if (cd && cw) { ++c.racy; c.best = min(c.best, p >> pay_bits); }
+      cd = false; cw = w;
+    } else {
+      cd |= diff; cw |= w;
+    }
+  }
+  if (in_lead) { ld = cd; lw = cw; }
+  const uint32_t HL = __ballot_sync(0xFFFFFFFFu, !in_lead);
+  const uint32_t LD = __ballot_sync(0xFFFFFFFFu, ld);
+  const uint32_t LW = __ballot_sync(0xFFFFFFFFu, lw);
+  if (HL) {
+    // the carried segment covers the lead parts of lanes [0, first head lane]
+    const uint32_t m0 = ((HL & (0u - HL)) << 1) - 1u;
+    const bool ccd = c.diff || (LD & m0) != 0, ccw = c.wr || (LW & m0) != 0;
+    if (c.lead) {
+      c.lead_closed = true; c.lead_diff = ccd; c.lead_wr = ccw; c.lead = false;
+    } else if (lane == 0 && ccd && ccw) {
+      ++c.racy; c.best = min(c.best, c.key >> pay_bits);
+    }
+    // a lane's trailing segment runs through the lead parts of lanes (lane, next head lane]
+    const uint32_t upto = (2u << lane) - 1u;
+    const uint32_t later = HL & ~upto;
+    if (!in_lead && later) {
+      const uint32_t m = (((later & (0u - later)) << 1) - 1u) & ~upto;
+      if ((cd || (LD & m)) && (cw || (LW & m))) { ++c.racy; c.best = min(c.best, a[3] >> pay_bits); }
+    }
+    const uint32_t o = 31u - __clz(HL);
+    const uint32_t t = __shfl_sync(0xFFFFFFFFu, (uint32_t)cd | ((uint32_t)cw << 1), o);
+    const uint32_t rest = ~((2u << o) - 1u);
+    c.diff = (t & 1u) || (LD & rest);
+    c.wr = (t & 2u) || (LW & rest);
+  } else {
+    c.diff = c.diff || LD != 0;
+    c.wr = c.wr || LW != 0;
+  }
+  c.key = __shfl_sync(0xFFFFFFFFu, a[3], 31);
+}
+
+template <bool P32>
+__global__ void __launch_bounds__(DWS_THREADS, 4)
+k_detect_ws(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
+            MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid,
+            MapcSegState* __restrict__ first_frag, MapcSegState* __restrict__ last_frag) {
+  const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
+  const unsigned long long n = ctrl->n;
+  const uint32_t lane = threadIdx.x & 31;
+  const unsigned long long nw = (unsigned long long)gridDim.x * (DWS_THREADS / 32);
+  const unsigned long long gw = (unsigned long long)blockIdx.x * (DWS_THREADS / 32) + (threadIdx.x >> 5);
+  const unsigned long long unit = detect_unit(n, nw);
+  const unsigned long long start = gw * unit;
+  if (lane == 0) { first_frag[gw].valid = 0; last_frag[gw].valid = 0; }
+  if (start >= n) return;
+  const unsigned long long end = min(n, start + unit);
+  const unsigned long long tmask = w_tid >= 32 ? 0xFFFFFFFFull : ((1ull << w_tid) - 1ull);
+
+  WsCarry c;
+  const unsigned long long k0 = keys[start];
+  // at the chunk's first key: continuation of an empty segment, closed (and
+  // counted) like any other by lane 0
+  c.key = start > 0 ? keys[start - 1] : k0;
+  c.lead = start > 0 && ((c.key ^ k0) >> pay_bits) == 0;
+  if (c.lead) c.key = k0;                        // first position: same segment, no tid diff
+  c.diff = c.wr = false;
+  c.lead_closed = c.lead_diff = c.lead_wr = false;
+  c.racy = 0;
+  c.best = ~0ull;
+
+  constexpr unsigned long long BATCH = 128ull * DWS_V;
+  const unsigned long long paymask = (pay_bits >= 64) ? ~0ull : ((1ull << pay_bits) - 1ull);
+  const unsigned long long full_end = start + ((end - start) / BATCH) * BATCH;
+  const ulonglong2* __restrict__ p = reinterpret_cast<const ulonglong2*>(keys + start) + 2 * lane;
+  for (unsigned long long b = start; b < full_end; b += BATCH, p += BATCH / 2) {
+    ulonglong2 v[2 * DWS_V];
+#pragma unroll
+    for (int j = 0; j < DWS_V; ++j) {
+      v[2 * j] = ld_stream2(p + j * 64);
+      v[2 * j + 1] = ld_stream2(p + j * 64 + 1);
+    }
+#pragma unroll
+    for (int j = 0; j < DWS_V; ++j) {
+      const unsigned long long a4[4] = {v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y};
+      ws_step4<P32>(c, a4, lane, pay_bits, paymask, tmask);
+    }
+  }
+#pragma unroll 1
+  for (unsigned long long b = full_end; b < end; b += 32) {
+    const uint32_t nvalid = (uint32_t)min(32ull, end - b);
+    const unsigned long long k = lane < nvalid ? keys[b + lane] : 0ull;
+    ws_step<false>(c, k, nvalid, lane, pay_bits, tmask);
+  }
+  if (lane == 0) {
+    const uint32_t t0 = (uint32_t)((k0 >> 1) & tmask);
+    if (c.lead_closed) {
+      MapcSegState f;
+      f.first_tid = t0; f.last_tid = 0;
+      f.wr = c.lead_wr; f.diff = c.lead_diff; f.valid = 1; f.ends = 1; f.sf = k0 >> pay_bits;
+      first_frag[gw] = f;
+    }
+    // the segment open at the range end
+    const bool ends = end == n || ((keys[end] ^ c.key) >> pay_bits) != 0;
+    MapcSegState f;
+    f.first_tid = t0;
+    f.last_tid = (uint32_t)((c.key >> 1) & tmask);
+    f.wr = c.wr; f.diff = c.diff; f.valid = 1; f.ends = ends; f.sf = c.key >> pay_bits;
+    if (c.lead) {
+      first_frag[gw] = f;
+    } else if (ends) {
+      if (c.diff && c.wr) { ++c.racy; c.best = min(c.best, c.key >> pay_bits); }
+    } else {
+      last_frag[gw] = f;
+    }
+  }
+  unsigned long long best = c.best, racy = c.racy;
+  for (int o = 16; o > 0; o >>= 1) {
+    best = min(best, __shfl_down_sync(0xffffffffu, best, o));
+    racy += __shfl_down_sync(0xffffffffu, racy, o);
+  }
+  if (lane == 0) {
+    if (best != ~0ull) atomicMin(&ctrl->racy_sf, best);
+    if (racy) atomicAdd(&ctrl->racy, racy);
+  }
+}
+
+// Fixup over warp ranges: one thread per range that owns an open segment head.
+__global__ void k_detect_fixup_ws(MapcCtrl* __restrict__ ctrl, const MapcSegState* __restrict__ first_frag,
+                                  const MapcSegState* __restrict__ last_frag, unsigned long long nw) {
+  const unsigned long long n = ctrl->n;
+  const unsigned long long unit = detect_unit(n, nw);
+  const unsigned long long n_units = (n + unit - 1) / unit;
+  unsigned long long best = ~0ull, racy = 0;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_units;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const MapcSegState lf = last_frag[t];
+    if (!lf.valid) continue;
+    uint32_t wr = lf.wr, diff = lf.diff, last = lf.last_tid;
+    for (unsigned long long u = t + 1; u < n_units; ++u) {
+      const MapcSegState ff = first_frag[u];
+      if (!ff.valid || ff.sf != lf.sf) { atomicOr(&ctrl->err, MAPC_ERR_LAYOUT); break; }
+      diff |= ff.diff | (uint32_t)(ff.first_tid != last);
+      wr |= ff.wr;
+      last = ff.last_tid;
+      if (ff.ends) break;
+    }
+    if (wr && diff) { ++racy; best = min(best, lf.sf); }
+  }
+  if (best != ~0ull) atomicMin(&ctrl->racy_sf, best);
+  if (racy) atomicAdd(&ctrl->racy, racy);
+}
+
 // ---- pass 2: canonical witness of the first racy segment ----------------------
 // One CTA: lower_bound of the segment in the sorted keys, then a parallel fold
 // of the full state (m1, k1, m2, k2, w) over the segment, closed-form witness.
@@ -264,6 +502,29 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
                                           uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, MapcSegState* first_frag,
                                           MapcSegState* last_frag, unsigned long long max_keys, int n_sms,
                                           cudaStream_t s) {
+  static const int variant = [] { const char* e = getenv("MAPC_DETECT"); return e && e[0] == 't' ? 1 : 0; }();
+  if (variant == 0) {
+    // warp-streaming form: grid sized to the SMs (4 CTAs of 8 warps each), capped by the fragment arrays
+    unsigned long long warps = (max_keys + 511) / 512;
+    unsigned long long ctas = (warps + 7) / 8;
+    unsigned long long cap = (unsigned long long)n_sms * 4;
+    if (cap * 8 > MAPC_DETECT_MAX_UNITS) cap = MAPC_DETECT_MAX_UNITS / 8;
+    const int grid = (int)(ctas < 1 ? 1 : (ctas < cap ? ctas : cap));
+    if (pay_bits <= 32)
+      mapk::k_detect_ws<true><<<grid, mapk::DWS_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid,
+                                                                 first_frag, last_frag);
+    else
+      mapk::k_detect_ws<false><<<grid, mapk::DWS_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid,
+                                                                  first_frag, last_frag);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned long long nw = (unsigned long long)grid * (mapk::DWS_THREADS / 32);
+    mapk::k_detect_fixup_ws<<<(int)((nw + 255) / 256), 256, 0, s>>>(ctrl, first_frag, last_frag, nw);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    mapk::k_witness<<<1, mapk::WT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid);
+    return cudaGetLastError();
+  }
   const unsigned long long tiles = (max_keys + mapk::DW_CHUNK - 1) / mapk::DW_CHUNK;
   const unsigned long long cap = (unsigned long long)n_sms * 8;
   const int grid = (int)(tiles < 1 ? 1 : (tiles < cap ? tiles : cap));
