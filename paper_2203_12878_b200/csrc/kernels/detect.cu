@@ -260,35 +260,60 @@ __device__ __forceinline__ void ws_step(WsCarry& c, unsigned long long k, uint32
   c.key = __shfl_sync(0xFFFFFFFFu, k, FULL ? 31 : nvalid - 1);
 }
 
-// Four consecutive keys per lane per step (128 keys per warp): in-lane
-// segments close in registers; only segments crossing lanes use the ballots.
-// Keys are sorted by sort field, so "new segment" is one 64-bit compare:
-// sf(a) != sf(p) <=> a > (p | payload mask).
+// Four consecutive keys per lane per step (128 keys per warp).  A lane turns
+// its 4 keys into three 4-bit masks -- head (new segment), diff (tid differs
+// from the predecessor inside a segment), write -- and one lookup in a 4 KiB
+// shared table gives everything the in-lane segments decide: the lead part's
+// (diff, write), the trailing part's (diff, write), how many segments close
+// racy inside the lane and where the first one starts.  Only segments that
+// cross lanes use the ballots.  Keys are sorted by sort field, so "new
+// segment" is one 64-bit compare: sf(a) != sf(p) <=> a > (p | payload mask).
+//   table entry: bit0 lead diff, bit1 lead write, bit2 trail diff, bit3 trail
+//   write, bits4-5 racy in-lane segments, bits6-7 head position of the first.
+__device__ void ws_fill_table(uint8_t* tab) {
+  for (uint32_t idx = threadIdx.x; idx < 4096; idx += blockDim.x) {
+    const uint32_t h = idx & 15u, d = (idx >> 4) & 15u, w = idx >> 8;
+    uint32_t in_lead = 1, cd = 0, cw = 0, ld = 0, lw = 0, cnt = 0, first = 0, start = 0;
+    for (uint32_t i = 0; i < 4; ++i) {
+      const uint32_t hi = (h >> i) & 1u, di = (d >> i) & 1u, wi = (w >> i) & 1u;
+      if (hi) {
+        if (in_lead) { ld = cd; lw = cw; in_lead = 0; }
+        else if (cd && cw) { if (!cnt) first = start; ++cnt; }
+        start = i; cd = 0; cw = wi;
+      } else {
+        cd |= di; cw |= wi;
+      }
+    }
+    if (in_lead) { ld = cd; lw = cw; }
+    tab[idx] = (uint8_t)(ld | (lw << 1) | (cd << 2) | (cw << 3) | (cnt << 4) | (first << 6));
+  }
+}
+
 template <bool P32>
-__device__ __forceinline__ void ws_step4(WsCarry& c, const unsigned long long (&a)[4], uint32_t lane,
-                                         uint32_t pay_bits, unsigned long long paymask, unsigned long long tmask) {
+__device__ __forceinline__ void ws_step4(WsCarry& c, const unsigned long long (&a)[4], const uint8_t* tab,
+                                         uint32_t lane, uint32_t pay_bits, unsigned long long paymask,
+                                         unsigned long long tmask) {
   unsigned long long prev = __shfl_up_sync(0xFFFFFFFFu, a[3], 1);
   if (lane == 0) prev = c.key;
-  bool in_lead = true, cd = false, cw = false, ld = false, lw = false;
+  uint32_t h = 0, d = 0, w = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const unsigned long long p = i ? a[i - 1] : prev;
-    const bool head = a[i] > (p | paymask);
-    const bool diff = P32 ? (((uint32_t)a[i] ^ (uint32_t)p) & ((uint32_t)tmask << 1)) != 0
-                          : (((a[i] ^ p) >> 1) & tmask) != 0;
-    const bool w = (a[i] & 1ull) != 0;
-    if (head) {
-      if (in_lead) { ld = cd; lw = cw; in_lead = false; }
-      else if (cd && cw) { ++c.racy; c.best = min(c.best, p >> pay_bits); }
-      cd = false; cw = w;
-    } else {
-      cd |= diff; cw |= w;
-    }
+    h |= (uint32_t)(a[i] > (p | paymask)) << i;
+    d |= (uint32_t)(P32 ? (((uint32_t)a[i] ^ (uint32_t)p) & ((uint32_t)tmask << 1)) != 0
+                        : (((a[i] ^ p) >> 1) & tmask) != 0) << i;
+    w |= ((uint32_t)a[i] & 1u) << i;
   }
-  if (in_lead) { ld = cd; lw = cw; }
-  const uint32_t HL = __ballot_sync(0xFFFFFFFFu, !in_lead);
-  const uint32_t LD = __ballot_sync(0xFFFFFFFFu, ld);
-  const uint32_t LW = __ballot_sync(0xFFFFFFFFu, lw);
+  const uint32_t e = tab[h | ((d & ~h) << 4) | (w << 8)];
+  const uint32_t HL = __ballot_sync(0xFFFFFFFFu, h != 0);
+  const uint32_t LD = __ballot_sync(0xFFFFFFFFu, e & 1u);
+  const uint32_t LW = __ballot_sync(0xFFFFFFFFu, e & 2u);
+  if (e & 0x30u) {                               // racy segments closing inside the lane
+    c.racy += (e >> 4) & 3u;
+    const uint32_t f = e >> 6;
+    const unsigned long long k = f == 0 ? a[0] : f == 1 ? a[1] : f == 2 ? a[2] : a[3];
+    c.best = min(c.best, k >> pay_bits);
+  }
   if (HL) {
     // the carried segment covers the lead parts of lanes [0, first head lane]
     const uint32_t m0 = ((HL & (0u - HL)) << 1) - 1u;
@@ -301,15 +326,16 @@ __device__ __forceinline__ void ws_step4(WsCarry& c, const unsigned long long (&
     // a lane's trailing segment runs through the lead parts of lanes (lane, next head lane]
     const uint32_t upto = (2u << lane) - 1u;
     const uint32_t later = HL & ~upto;
-    if (!in_lead && later) {
+    if (h && later) {
       const uint32_t m = (((later & (0u - later)) << 1) - 1u) & ~upto;
-      if ((cd || (LD & m)) && (cw || (LW & m))) { ++c.racy; c.best = min(c.best, a[3] >> pay_bits); }
+      if (((e & 4u) || (LD & m)) && ((e & 8u) || (LW & m))) { ++c.racy; c.best = min(c.best, a[3] >> pay_bits); }
     }
+    const uint32_t TD = __ballot_sync(0xFFFFFFFFu, e & 4u);
+    const uint32_t TW = __ballot_sync(0xFFFFFFFFu, e & 8u);
     const uint32_t o = 31u - __clz(HL);
-    const uint32_t t = __shfl_sync(0xFFFFFFFFu, (uint32_t)cd | ((uint32_t)cw << 1), o);
     const uint32_t rest = ~((2u << o) - 1u);
-    c.diff = (t & 1u) || (LD & rest);
-    c.wr = (t & 2u) || (LW & rest);
+    c.diff = ((TD >> o) & 1u) || (LD & rest);
+    c.wr = ((TW >> o) & 1u) || (LW & rest);
   } else {
     c.diff = c.diff || LD != 0;
     c.wr = c.wr || LW != 0;
@@ -322,6 +348,9 @@ __global__ void __launch_bounds__(DWS_THREADS, 4)
 k_detect_ws(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
             MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid,
             MapcSegState* __restrict__ first_frag, MapcSegState* __restrict__ last_frag) {
+  __shared__ uint8_t tab[4096];
+  ws_fill_table(tab);
+  __syncthreads();
   const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
   const unsigned long long n = ctrl->n;
   const uint32_t lane = threadIdx.x & 31;
@@ -360,7 +389,7 @@ k_detect_ws(const unsigned long long* __restrict__ bufA, const unsigned long lon
 #pragma unroll
     for (int j = 0; j < DWS_V; ++j) {
       const unsigned long long a4[4] = {v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y};
-      ws_step4<P32>(c, a4, lane, pay_bits, paymask, tmask);
+      ws_step4<P32>(c, a4, tab, lane, pay_bits, paymask, tmask);
     }
   }
 #pragma unroll 1
