@@ -109,6 +109,21 @@ typedef struct {
 #define MAP_GEN_VM 1u
 #define MAP_GEN_JIT 2u
 
+/* Detect path (map_exec.flags, OR-ed with MAP_GEN_*).
+ *   MAP_DETECT_SORT:  full LSD radix sort on all S sort-field bits, then the
+ *                     segmented scan over equal sort fields.
+ *   MAP_DETECT_TABLE: LSD passes only on the bits above the low tb <= 13 bits
+ *                     ("buckets"), then each bucket is folded into a 2^tb-cell
+ *                     direct-address table in shared memory (min tid, max tid,
+ *                     write bit per cell).  Same verdict,
+ *                     witness, access count and racy-segment count.
+ *   MAP_DETECT_AUTO:  TABLE when the chunk holds >= 2^16 keys and at least
+ *                     2^(S-1) of them (dense sort-field space), else SORT. */
+#define MAP_DETECT_AUTO 0u
+#define MAP_DETECT_SORT 0x10u
+#define MAP_DETECT_TABLE 0x20u
+#define MAP_DETECT_MASK 0x30u
+
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */
   int32_t n_chunks;           /* chunks this call processed                          */

@@ -61,6 +61,7 @@ class _Exec(ctypes.Structure):
                 ("flags", ctypes.c_uint32)]
 
 GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
+DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20}   # MAP_DETECT_* (include/mapcheck.h)
 
 
 class _Result(ctypes.Structure):
@@ -221,13 +222,13 @@ class MapProgram:
         return {f: getattr(d, f) for f, _ in _ChunkDesc._fields_}
 
     # ---- stage API (key-exchange multi-GPU mode) ------------
-    def _exec(self, scratch, stream, chunk_max_accesses):
+    def _exec(self, scratch, stream, chunk_max_accesses, flags=0):
         import torch
         dev = scratch.device.index if scratch.device.index is not None else torch.cuda.current_device()
         if stream is None:
             stream = torch.cuda.current_stream(dev)
         return _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
-                     scratch.numel() * scratch.element_size(), int(chunk_max_accesses), 0, 1, None, 0)
+                     scratch.numel() * scratch.element_size(), int(chunk_max_accesses), 0, 1, None, flags)
 
     def generate_bucketed(self, chunk: int, rank: int, world: int, keys_out, scratch, stream=None,
                           chunk_max_accesses: int = 0):
@@ -241,9 +242,10 @@ class MapProgram:
             raise MapError(st, _lib.map_last_error(self._h).decode())
         return [int(c) for c in counts]
 
-    def sort_detect(self, chunk: int, keys, n: int, scratch, stream=None, chunk_max_accesses: int = 0):
+    def sort_detect(self, chunk: int, keys, n: int, scratch, stream=None, chunk_max_accesses: int = 0,
+                    detect: str = "auto"):
         """Sort + detect n device keys of chunk `chunk`: (packed witness or None, racy segment count)."""
-        ex = self._exec(scratch, stream, chunk_max_accesses)
+        ex = self._exec(scratch, stream, chunk_max_accesses, DETECT_PATHS[detect])
         w, r = ctypes.c_uint64(), ctypes.c_uint64()
         st = _lib.map_sort_detect(self._h, ctypes.byref(ex), chunk, ctypes.c_void_p(keys.data_ptr() if n else 0),
                                   int(n), ctypes.byref(w), ctypes.byref(r))
@@ -301,7 +303,8 @@ class MapProgram:
         return c.value
 
     def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None,
-                    rank: int = 0, world: int = 1, profile: bool = False, gen: str = "auto") -> Result:
+                    rank: int = 0, world: int = 1, profile: bool = False, gen: str = "auto",
+                    detect: str = "auto") -> Result:
         """Run generate -> sort -> detect on one GPU (blocking).
 
         scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
@@ -321,7 +324,7 @@ class MapProgram:
         stats = _Stats() if profile else None
         ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
                    scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
-                   ctypes.pointer(stats) if stats is not None else None, GEN_PATHS[gen])
+                   ctypes.pointer(stats) if stats is not None else None, GEN_PATHS[gen] | DETECT_PATHS[detect])
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:

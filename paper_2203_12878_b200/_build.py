@@ -18,6 +18,7 @@ SOURCES = [
     "kernels/detect.cu",
     "kernels/rsweep.cu",
     "kernels/exchange.cu",
+    "kernels/table.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "capi/jit.h"]
 

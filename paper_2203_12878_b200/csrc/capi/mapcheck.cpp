@@ -59,6 +59,13 @@ cudaError_t mapc_launch_hist_ranges(const unsigned long long* keys, MapcCtrl* ct
 cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
                                    unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 int mapc_rsweep_fused();
+int mapc_table_ctas(int n_sms);
+cudaError_t mapc_launch_detect_table(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
+                                     uint32_t n_passes, uint32_t pay_bits, uint32_t tb, uint32_t w_tid,
+                                     MapcTablePart* parts, uint32_t* store, unsigned long long max_keys, int n_sms,
+                                     cudaStream_t s);
+cudaError_t mapc_launch_witness(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
+                                uint32_t n_passes, uint32_t pay_bits, uint32_t tb, uint32_t w_tid, cudaStream_t s);
 cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
                                unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 }
@@ -92,6 +99,8 @@ struct Plan {
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
   size_t rh_bytes = 0, off_xch = 0;
+  size_t off_tparts = 0, off_tstore = 0;    // bucket-table detect: partial tables
+  uint32_t table_ctas = 0;
   size_t lb_bytes = 0, total = 0, stage_bytes = 0;
 };
 
@@ -138,6 +147,8 @@ bool layout_fits(const mapc::Compiled& C, uint32_t ph_span, uint64_t nb, uint64_
   L.sort_bits = L.w_phase + L.w_array + L.w_block + L.w_index;
   L.n_passes = (L.sort_bits + 7) / 8;
   L.idx_lo = ilo <= ihi ? ilo : 0;
+  L.tb = 0;
+  L.sort_lo = L.pay_bits;
   if (L.sort_bits + L.pay_bits > 64) return false;
   if (L.sort_bits + 2 * L.w_tid + 2 > 64) return false;
   if (out) *out = L;
@@ -318,10 +329,36 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
   out.off_rh = off; off += align_up(out.rh_bytes);
   out.off_xch = off; off += align_up(2 * 64 * sizeof(unsigned long long));   // exchange counts + cursors
+  out.table_ctas = (uint32_t)std::min<uint64_t>(MAPC_TABLE_MAX_CTAS, (kcap + 4095) / 4096);
+  out.off_tparts = off; off += align_up((size_t)2 * out.table_ctas * sizeof(MapcTablePart));
+  out.off_tstore = off; off += align_up((size_t)2 * out.table_ctas * MAPC_TABLE_WORDS * 4);
   out.total = off;
   out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
   *P = std::move(out);
   return MAP_OK;
+}
+
+// Detect path of a chunk (map_exec.flags, MAP_DETECT_*): the full LSD sort +
+// segmented scan, or the partial sort + bucket tables (table.cu), which needs
+// the keys to be dense enough in sf space that a bucket of 2^tb cells holds
+// about a tile of keys or more.
+MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~0ull) {
+  const uint64_t nk = n_keys == ~0ull ? ch.bound : n_keys;
+  MapcLayout L = ch.lay;
+  const uint32_t sel = flags & MAP_DETECT_MASK;
+  bool table = false;
+  if (sel == MAP_DETECT_TABLE) {
+    table = true;
+  } else if (sel == MAP_DETECT_AUTO) {
+    const uint32_t S = L.sort_bits;
+    table = nk >= (1ull << 16) && (S <= 1 || nk >= (1ull << (S - 1)));
+  }
+  if (table) {
+    L.tb = std::min<uint32_t>(MAPC_TABLE_BITS_MAX, L.sort_bits);
+    L.n_passes = (L.sort_bits - L.tb + 7) / 8;
+    L.sort_lo = L.pay_bits + L.tb;
+  }
+  return L;
 }
 
 void put_diag(const std::string& d, char* diag, size_t cap) {
@@ -497,6 +534,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   auto* ctrl = (MapcCtrl*)(base + P.off_ctrl);
   auto* res = (MapcChunkResult*)(base + P.off_res);
   auto* rhist = (unsigned int*)(base + P.off_rh);
+  auto* tparts = (MapcTablePart*)(base + P.off_tparts);
+  auto* tstore = (uint32_t*)(base + P.off_tstore);
   static int sort_mode = -1;     // 1 = static-range passes (default), 0 = decoupled look-back onesweep
   if (sort_mode < 0) {
     const char* e = getenv("MAPC_SORT");
@@ -518,7 +557,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     P.jit_ready = true;
   }
   uint32_t passes_total = 0;
-  for (auto& ch : P.chunks) passes_total += ch.lay.n_passes;
+  for (auto& ch : P.chunks) passes_total += effective_layout(ch, ex->flags).n_passes;
   if (p->last_lookback != (void*)lookback || p->device != ex->device || p->epoch + passes_total >= 0xFFFF) {
     CK(cudaMemsetAsync(lookback, 0, P.lb_bytes, s));
     p->epoch = 0;
@@ -560,7 +599,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   CK(cudaEventRecord(p->events[0], s));
   for (size_t c : mine) {
     const Chunk& ch = P.chunks[c];
-    const MapcLayout& L = ch.lay;
+    const MapcLayout L = effective_layout(ch, ex->flags);
     CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
     CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, s));
     h2d += ch.ops.size() * sizeof(MapcOp) + ch.segs.size() * sizeof(MapcSeg);
@@ -581,7 +620,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       if (L.n_passes) {
         CK(cudaMemsetAsync(rhist, 0, P.rh_bytes, s));
         m = begin(MAP_K_HIST);
-        CK(mapc_launch_hist_ranges(bufA, ctrl, rhist, L.pay_bits, L.n_passes, G, s));
+        CK(mapc_launch_hist_ranges(bufA, ctrl, rhist, L.sort_lo, L.n_passes, G, s));
         end(m);
       }
       m = begin(MAP_K_SCAN);
@@ -592,17 +631,17 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         // previous scatter (fused variants) or from one read of the pass's input
         if (pass > 0) {
           m = begin(MAP_K_HIST);
-          CK(mapc_launch_range_hist(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
+          CK(mapc_launch_range_hist(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, s));
           end(m);
         }
         m = begin(MAP_K_ONESWEEP);
-        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.pay_bits, G, s));
+        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, s));
         end(m);
       }
     } else {
       if (L.n_passes) {
         m = begin(MAP_K_HIST);
-        CK(mapc_launch_hist(bufA, ctrl, L.pay_bits, L.n_passes, ch.bound, n_sms, s));
+        CK(mapc_launch_hist(bufA, ctrl, L.sort_lo, L.n_passes, ch.bound, n_sms, s));
         end(m);
       }
       m = begin(MAP_K_SCAN);
@@ -611,14 +650,19 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
         ++p->epoch;
         m = begin(MAP_K_ONESWEEP);
-        CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.pay_bits + 8 * pass, p->epoch, ch.bound, n_sms, s));
+        CK(mapc_launch_onesweep(bufA, bufB, ctrl, lookback, pass, L.sort_lo + 8 * pass, p->epoch, ch.bound, n_sms, s));
         end(m);
       }
     }
     m = begin(MAP_K_DETECT);
     ++launches;                        // detect + fixup
     st_acc.launches[MAP_K_DETECT]++;
-    CK(mapc_launch_detect(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.w_tid, ff, lf, ch.bound, n_sms, s));
+    if (L.tb)
+      CK(mapc_launch_detect_table(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.tb, L.w_tid, tparts, tstore, ch.bound,
+                                  n_sms, s));
+    else
+      CK(mapc_launch_detect(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.w_tid, ff, lf, ch.bound, n_sms, s));
+    CK(mapc_launch_witness(bufA, bufB, ctrl, L.n_passes, L.pay_bits, L.tb, L.w_tid, s));
     end(m);
     m = begin(MAP_K_OTHER);
     CK(mapc_launch_chunk_finish(ctrl, L.n_passes, res + c, s));
@@ -715,6 +759,8 @@ struct Dev {
   MapcChunkResult* res;
   unsigned int* rhist;
   unsigned long long* xch;
+  MapcTablePart* tparts;
+  uint32_t* tstore;
   int n_sms, G;
   cudaStream_t s;
 };
@@ -750,6 +796,8 @@ map_status stage_setup(map_program* p, const map_exec* ex, uint32_t chunk, Dev* 
   d->res = (MapcChunkResult*)(base + P.off_res);
   d->rhist = (unsigned int*)(base + P.off_rh);
   d->xch = (unsigned long long*)(base + P.off_xch);
+  d->tparts = (MapcTablePart*)(base + P.off_tparts);
+  d->tstore = (uint32_t*)(base + P.off_tstore);
   return MAP_OK;
 }
 
@@ -825,21 +873,26 @@ map_status map_sort_detect(map_program* p, const map_exec* ex, uint32_t chunk, v
   if (st != MAP_OK) return st;
   Plan& P = p->plan;
   const Chunk& ch = P.chunks[chunk];
-  const MapcLayout& L = ch.lay;
+  const MapcLayout L = effective_layout(ch, ex->flags, n);
   if (n > P.cap) return MAP_E_NOMEM;
   CK(mapc_launch_chunk_init(d.ctrl, n, d.s));
   if (n) CK(cudaMemcpyAsync(d.bufA, keys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, d.s));
   if (L.n_passes) {
     CK(cudaMemsetAsync(d.rhist, 0, P.rh_bytes, d.s));
-    CK(mapc_launch_hist_ranges(d.bufA, d.ctrl, d.rhist, L.pay_bits, L.n_passes, d.G, d.s));
+    CK(mapc_launch_hist_ranges(d.bufA, d.ctrl, d.rhist, L.sort_lo, L.n_passes, d.G, d.s));
   }
   CK(mapc_launch_digit_scan(d.ctrl, L.n_passes, d.s));
   for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
-    if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.pay_bits, d.G, d.s));
-    CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.pay_bits, d.G, d.s));
+    if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
+    CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
   }
-  CK(mapc_launch_detect(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.w_tid, d.ff, d.lf, std::max<uint64_t>(n, 1),
-                        d.n_sms, d.s));
+  if (L.tb)
+    CK(mapc_launch_detect_table(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.tb, L.w_tid, d.tparts, d.tstore,
+                                std::max<uint64_t>(n, 1), d.n_sms, d.s));
+  else
+    CK(mapc_launch_detect(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.w_tid, d.ff, d.lf,
+                          std::max<uint64_t>(n, 1), d.n_sms, d.s));
+  CK(mapc_launch_witness(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.tb, L.w_tid, d.s));
   CK(mapc_launch_chunk_finish(d.ctrl, L.n_passes, d.res + chunk, d.s));
   MapcChunkResult r{};
   CK(cudaMemcpyAsync(&r, d.res + chunk, sizeof(r), cudaMemcpyDeviceToHost, d.s));

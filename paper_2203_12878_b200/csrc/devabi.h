@@ -97,9 +97,21 @@ struct MapcLayout {
   uint32_t w_tid;        // bits of tid
   uint32_t pay_bits;     // w_tid + 1
   uint32_t sort_bits;    // S = w_phase + w_array + w_block + w_index
-  uint32_t n_passes;     // ceil(S / 8)
+  uint32_t n_passes;     // radix passes: ceil((S - tb) / 8)
   uint64_t idx_lo;
   uint64_t cap;          // key buffer capacity (keys)
+  uint32_t tb;           // bucket-table detect: low sf bits resolved in a table (0 = full sort)
+  uint32_t sort_lo;      // lowest key bit the radix passes sort on: pay_bits + tb
+};
+
+// Bucket-table detect (table.cu): partial tables of buckets crossing ranges.
+#define MAPC_TABLE_BITS_MAX 13
+#define MAPC_TABLE_WORDS (2 * (1 << MAPC_TABLE_BITS_MAX) + (1 << MAPC_TABLE_BITS_MAX) / 32)
+#define MAPC_TABLE_MAX_CTAS 448
+struct MapcTablePart {
+  unsigned long long bucket;
+  uint32_t ends;         // the bucket ends inside this range (head partials)
+  uint32_t valid;
 };
 
 // Per-chunk device control block (reset by the init kernel).

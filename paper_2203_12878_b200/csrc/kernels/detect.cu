@@ -460,22 +460,26 @@ __global__ void k_detect_fixup_ws(MapcCtrl* __restrict__ ctrl, const MapcSegStat
 // ---- pass 2: canonical witness of the first racy segment ----------------------
 // One CTA: lower_bound of the segment in the sorted keys, then a parallel fold
 // of the full state (m1, k1, m2, k2, w) over the segment, closed-form witness.
+// With the bucket-table detect (table.cu) the keys are sorted only by bucket
+// = sf >> tb: the fold then walks the target's bucket and takes its keys.
 constexpr int WT_THREADS = 256;
 __global__ void __launch_bounds__(WT_THREADS)
 k_witness(const unsigned long long* __restrict__ bufA, const unsigned long long* __restrict__ bufB,
-          MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid) {
+          MapcCtrl* __restrict__ ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t tb, uint32_t w_tid) {
   const unsigned long long target = ctrl->racy_sf;
   if (target == ~0ull) return;
   const unsigned long long* __restrict__ keys = ctrl->sel[n_passes] ? bufB : bufA;
   const unsigned long long n = ctrl->n;
   const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
+  const uint32_t bsh = pay_bits + tb;
+  const unsigned long long tbucket = target >> tb;
   __shared__ unsigned long long s_lo;
   __shared__ St part[WT_THREADS];
   if (threadIdx.x == 0) {
-    unsigned long long lo = 0, hi = n;                  // first index with sf >= target
+    unsigned long long lo = 0, hi = n;                  // first index with bucket >= target's
     while (lo < hi) {
       const unsigned long long mid = (lo + hi) >> 1;
-      if ((keys[mid] >> pay_bits) < target) lo = mid + 1; else hi = mid;
+      if ((keys[mid] >> bsh) < tbucket) lo = mid + 1; else hi = mid;
     }
     s_lo = lo;
   }
@@ -484,8 +488,8 @@ k_witness(const unsigned long long* __restrict__ bufA, const unsigned long long*
   st_init(s);
   for (unsigned long long i = s_lo + threadIdx.x; i < n; i += WT_THREADS) {
     const unsigned long long key = keys[i];
-    if ((key >> pay_bits) != target) break;
-    st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
+    if ((key >> bsh) != tbucket) break;
+    if ((key >> pay_bits) == target) st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
   }
   part[threadIdx.x] = s;
   __syncthreads();
@@ -551,7 +555,6 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
     mapk::k_detect_fixup_ws<<<(int)((nw + 255) / 256), 256, 0, s>>>(ctrl, first_frag, last_frag, nw);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    mapk::k_witness<<<1, mapk::WT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid);
     return cudaGetLastError();
   }
   const unsigned long long tiles = (max_keys + mapk::DW_CHUNK - 1) / mapk::DW_CHUNK;
@@ -564,9 +567,14 @@ extern "C" cudaError_t mapc_launch_detect(const unsigned long long* bufA, const 
   if (g2 < 1) g2 = 1;
   if (g2 > n_sms * 4) g2 = n_sms * 4;
   mapk::k_detect_fixup<<<g2, 256, 0, s>>>(ctrl, first_frag, last_frag, (unsigned)mapk::DW_CHUNK);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  mapk::k_witness<<<1, mapk::WT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, w_tid);
+  return cudaGetLastError();
+}
+
+// Canonical witness of the smallest racy segment (no-op when the chunk is DRF).
+extern "C" cudaError_t mapc_launch_witness(const unsigned long long* bufA, const unsigned long long* bufB,
+                                           MapcCtrl* ctrl, uint32_t n_passes, uint32_t pay_bits, uint32_t tb,
+                                           uint32_t w_tid, cudaStream_t s) {
+  mapk::k_witness<<<1, mapk::WT_THREADS, 0, s>>>(bufA, bufB, ctrl, n_passes, pay_bits, tb, w_tid);
   return cudaGetLastError();
 }
 

@@ -207,3 +207,50 @@ def test_exchange_mode_many_chunks():
     o = oracle.check_instance(inst)
     unit = max(1, p.info.max_unit_accesses)
     assert _fake_exchange(p, 3, unit) == (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
+
+
+# ---- detect paths: full sort + segmented scan vs partial sort + bucket tables ----
+
+@pytest.mark.parametrize("detect", ["sort", "table"])
+@pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
+def test_detect_paths_match_oracle(name, sizes, detect):
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    same(p.check_races(detect=detect), o)
+    unit = max(1, p.info.max_unit_accesses)
+    same(p.check_races(chunk_max_accesses=unit, detect=detect), o)
+
+
+def test_fuzz_corpus_table_detect():
+    bad = []
+    for seed in range(0, 400, 2):
+        inst, _ = fuzz.random_instance(seed)
+        o = oracle.check_instance(inst, threads=1)
+        r = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).check_races(detect="table")
+        got = (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments)
+        if got != (o.verdict, o.witness, o.n_accesses, o.n_racy_segments):
+            bad.append((seed, inst.src, got))
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("detect", ["sort", "table"])
+def test_one_bucket_across_all_ranges(detect):
+    # few distinct cells, millions of keys: with the table path every range of the
+    # detect kernel sees the same bucket, so the partial tables chain end to end
+    for src in ["params N; forU x in 0..N { rd[x % 8] }; wr[tid % 4]",
+                "params N; forU x in 0..N { rd[x % 8] }; if (tid = 5) { wr[3] } else { skip }",
+                "params N; forU x in 0..N { rd[x % 8]; wr[8 + tid] }"]:
+        r = mc.check(src, block=(1024, 1, 1), params={"N": 4096}, detect=detect)
+        o = oracle.check(src, block=(1024, 1, 1), params={"N": 4096})
+        same(r, o)
+
+
+@pytest.mark.parametrize("name", ["3b", "4b", "5b"])
+def test_full_size_detect_paths_agree(name):
+    sizes = {"5b": {"T": 2}}.get(name, {})
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    a = p.check_races(detect="sort")
+    b = p.check_races(detect="table")
+    assert (a.verdict, a.witness, a.n_accesses, a.racy_segments) == (b.verdict, b.witness, b.n_accesses, b.racy_segments)
