@@ -126,37 +126,52 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
 
   for (unsigned long long t0 = r0; t0 < r1; t0 += TB_TILE) {
     const uint32_t tn = (uint32_t)min((unsigned long long)TB_TILE, r1 - t0);
-    const unsigned long long bf = keys[t0] >> bsh, bl = keys[t0 + tn - 1] >> bsh;
-    if (bf == cur && bl == cur) {
-      // common case: the whole tile continues the open bucket
-      unsigned long long k[TB_ITEMS];
+    // the tile's keys and its first / last bucket are loaded together (one round trip)
+    unsigned long long k[TB_ITEMS];
 #pragma unroll
-      for (int j = 0; j < TB_ITEMS; ++j) {
-        const uint32_t li = j * TB_THREADS + threadIdx.x;
-        k[j] = li < tn ? ld_stream(keys + t0 + li) : 0ull;
-      }
+    for (int j = 0; j < TB_ITEMS; ++j) {
+      const uint32_t li = j * TB_THREADS + threadIdx.x;
+      k[j] = li < tn ? ld_stream(keys + t0 + li) : 0ull;
+    }
+    const unsigned long long bf = keys[t0] >> bsh, bl = keys[t0 + tn - 1] >> bsh;
+    if (bf != cur) {
+      // the open bucket ended exactly at the tile boundary
+      __syncthreads();
+      close_bucket(true);
+      __syncthreads();
+      cur = bf;
+    }
+    if (bl == cur) {
+      // common case: the whole tile belongs to the open bucket
 #pragma unroll
       for (int j = 0; j < TB_ITEMS; ++j)
         if (j * TB_THREADS + threadIdx.x < tn) table_add(S, k[j], pay_bits, cmask, tmask);
       continue;
     }
-    // the tile closes one or more buckets: one sweep per bucket present (keys re-read, L1/L2)
+    // the tile closes one or more buckets: one sweep per bucket present (keys re-read from L2)
 #pragma unroll 1
     while (true) {
-#pragma unroll 1
-      for (uint32_t li = threadIdx.x; li < tn; li += TB_THREADS) {
-        const unsigned long long key = keys[t0 + li];
-        if ((key >> bsh) == cur) table_add(S, key, pay_bits, cmask, tmask);
+      unsigned long long nb = ~0ull;
+      {
+        unsigned long long kk[TB_ITEMS];
+#pragma unroll
+        for (int j = 0; j < TB_ITEMS; ++j) {
+          const uint32_t li = j * TB_THREADS + threadIdx.x;
+          kk[j] = li < tn ? keys[t0 + li] : ~0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < TB_ITEMS; ++j) {
+          const uint32_t li = j * TB_THREADS + threadIdx.x;
+          const unsigned long long b = kk[j] >> bsh;
+          if (li < tn) {
+            if (b == cur) table_add(S, kk[j], pay_bits, cmask, tmask);
+            else if (b > cur) nb = min(nb, b);
+          }
+        }
       }
       if (cur == bl) break;
       if (threadIdx.x == 0) S.next_bucket = ~0ull;
       __syncthreads();
-      unsigned long long nb = ~0ull;
-#pragma unroll 1
-      for (uint32_t li = threadIdx.x; li < tn; li += TB_THREADS) {
-        const unsigned long long b = keys[t0 + li] >> bsh;
-        if (b > cur) nb = min(nb, b);
-      }
       if (nb != ~0ull) atomicMin(&S.next_bucket, nb);
       close_bucket(true);
       __syncthreads();
