@@ -106,7 +106,7 @@ struct MapcLayout {
 
 // Bucket-table detect (table.cu): partial tables of buckets crossing ranges.
 #define MAPC_TABLE_BITS_MAX 13
-#define MAPC_TABLE_WORDS (2 * (1 << MAPC_TABLE_BITS_MAX) + (1 << MAPC_TABLE_BITS_MAX) / 32)
+#define MAPC_TABLE_WORDS (2 * (1 << MAPC_TABLE_BITS_MAX) + (1 << MAPC_TABLE_BITS_MAX) / 4)
 #define MAPC_TABLE_MAX_CTAS 448
 struct MapcTablePart {
   unsigned long long bucket;

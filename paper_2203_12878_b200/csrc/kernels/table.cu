@@ -32,7 +32,9 @@ constexpr uint32_t TB_EMPTY = 0xFFFFFFFFu;
 struct TableSmem {
   uint32_t mn[TB_CELLS];                           // min tid (TB_EMPTY = no access)
   uint32_t mx[TB_CELLS];                           // max tid
-  uint32_t wb[TB_CELLS / 32];                      // write bits
+  uint32_t wf[TB_CELLS / 4];                       // write flags, one byte per cell (plain stores:
+                                                   // a warp writing 32 neighbouring cells must not
+                                                   // serialise on one word as atomicOr would)
   unsigned long long next_bucket;
   unsigned long long best;
   unsigned long long racy;
@@ -40,9 +42,14 @@ struct TableSmem {
   uint32_t head_open;
 };
 
+// Cells are stored at a swizzled slot: the low 5 bits (the bank) are XORed
+// with bits 5-9 and 10-14, a bijection that keeps cells one or more 1 KiB
+// rows apart (stencil neighbours, transposes) out of each other's bank.
+__device__ __forceinline__ uint32_t cell_slot(uint32_t cell) { return cell ^ (((cell >> 5) ^ (cell >> 10)) & 31u); }
+
 __device__ __forceinline__ void table_reset(TableSmem& S) {
   for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) { S.mn[i] = TB_EMPTY; S.mx[i] = 0; }
-  for (int i = threadIdx.x; i < TB_CELLS / 32; i += TB_THREADS) S.wb[i] = 0;
+  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) S.wf[i] = 0;
 }
 
 // Scan a complete bucket's table: racy cells -> count and smallest sf.  Resets it.
@@ -50,37 +57,37 @@ __device__ __forceinline__ void table_flush(TableSmem& S, unsigned long long buc
                                             unsigned long long& racy, unsigned long long& best) {
   for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) {
     const uint32_t m = S.mn[i], x = S.mx[i];
-    const bool w = (S.wb[i >> 5] >> (i & 31)) & 1u;
+    const bool w = reinterpret_cast<const uint8_t*>(S.wf)[i] != 0;
     if (m != TB_EMPTY && w && m != x) {
       ++racy;
-      best = min(best, (bucket << tb) | (unsigned long long)i);
+      best = min(best, (bucket << tb) | (unsigned long long)cell_slot(i));    // slot -> cell (involution)
     }
     S.mn[i] = TB_EMPTY;
     S.mx[i] = 0;
   }
-  __syncthreads();                                 // every cell has read its write bit
-  for (int i = threadIdx.x; i < TB_CELLS / 32; i += TB_THREADS) S.wb[i] = 0;
+  __syncthreads();                                 // every cell has read its write flag
+  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) S.wf[i] = 0;
 }
 
 __device__ __forceinline__ void table_add(TableSmem& S, unsigned long long key, uint32_t pay_bits, uint32_t cmask,
                                           uint32_t tmask) {
-  const uint32_t cell = (uint32_t)(key >> pay_bits) & cmask;
+  const uint32_t cell = cell_slot((uint32_t)(key >> pay_bits) & cmask);
   const uint32_t t = (uint32_t)(key >> 1) & tmask;
   atomicMin(&S.mn[cell], t);
   atomicMax(&S.mx[cell], t);
-  if (key & 1ull) atomicOr(&S.wb[cell >> 5], 1u << (cell & 31));
+  if (key & 1ull) reinterpret_cast<volatile uint8_t*>(S.wf)[cell] = 1;
 }
 
 __device__ __forceinline__ void table_spill(TableSmem& S, MapcTablePart* part, uint32_t* store,
                                             unsigned long long bucket, uint32_t ends) {
   uint32_t* mn = store;
   uint32_t* mx = store + TB_CELLS;
-  uint32_t* wb = store + 2 * TB_CELLS;
+  uint32_t* wf = store + 2 * TB_CELLS;
   for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) {
     mn[i] = S.mn[i]; mx[i] = S.mx[i];
     S.mn[i] = TB_EMPTY; S.mx[i] = 0;
   }
-  for (int i = threadIdx.x; i < TB_CELLS / 32; i += TB_THREADS) { wb[i] = S.wb[i]; S.wb[i] = 0; }
+  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) { wf[i] = S.wf[i]; S.wf[i] = 0; }
   if (threadIdx.x == 0) { part->bucket = bucket; part->ends = ends; part->valid = 1; }
 }
 
@@ -214,7 +221,7 @@ k_table_merge(MapcCtrl* __restrict__ ctrl, const MapcTablePart* __restrict__ par
   unsigned long long racy = 0, best = ~0ull;
   for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) {
     uint32_t m = T[i], x = T[TB_CELLS + i];
-    bool w = (T[2 * TB_CELLS + (i >> 5)] >> (i & 31)) & 1u;
+    bool w = reinterpret_cast<const uint8_t*>(T + 2 * TB_CELLS)[i] != 0;
     bool closed = false;
     for (uint32_t u = c + 1; u < G; ++u) {
       const MapcTablePart hp = parts[2 * u];
@@ -222,13 +229,13 @@ k_table_merge(MapcCtrl* __restrict__ ctrl, const MapcTablePart* __restrict__ par
       const uint32_t* H = store + (size_t)(2 * u) * MAPC_TABLE_WORDS;
       m = min(m, H[i]);
       x = max(x, H[TB_CELLS + i]);
-      w = w || ((H[2 * TB_CELLS + (i >> 5)] >> (i & 31)) & 1u);
+      w = w || reinterpret_cast<const uint8_t*>(H + 2 * TB_CELLS)[i] != 0;
       if (hp.ends) { closed = true; break; }
     }
     if (!closed) continue;
     if (m != TB_EMPTY && w && m != x) {
       ++racy;
-      best = min(best, (tp.bucket << tb) | (unsigned long long)i);
+      best = min(best, (tp.bucket << tb) | (unsigned long long)cell_slot(i));
     }
   }
   if (best != ~0ull) atomicMin(&s_best, best);
