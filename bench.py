@@ -6,6 +6,10 @@ synthetic 3-deep loop stencil MAP of SURVEY.md §8d, 2^34 accesses
 (blockDim 1024, T=16 barrier phases, R=256 rows/thread, C=1024 columns,
 ping-pong buffers -> DRF), checked exhaustively: one step = generate + radix
 sort + detect over every access of every phase (all of §8 rows a1-a3).
+The detect path is the library's automatic choice (for 5a: LSD passes on the
+bucket bits sf >> 13, then the shared-memory bucket tables, SURVEY.md §8f
+NEXT-3); `--detect sort` forces the full LSD sort + segmented scan, and the
+line also reports that path's throughput on the same run ("detect_paths").
 
 Contract: `python bench.py --gpus N --steps K --warmup W` (torchrun for N>1,
 one rank per GPU; chunks are dealt round-robin to ranks, strong scaling on the
@@ -39,9 +43,11 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="5a")
     ap.add_argument("--chunk", type=int, default=0, help="chunk_max_accesses (0 = library default, 2^30)")
-    ap.add_argument("--cpu-rows", type=int, default=16, help="R of the oracle's bounded sample of the workload")
+    ap.add_argument("--cpu-rows", type=int, default=64, help="R of the oracle's bounded sample of the workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--detect", choices=["auto", "sort", "table"], default="auto")
+    ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect path")
     return ap.parse_args()
 
 
@@ -167,7 +173,7 @@ def measured_peak():
 
 def ncu_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_onesweep_traffic.json")
+    path = os.path.join(ROOT, "profiles", "ncu_rsweep_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -203,9 +209,9 @@ def main():
     stream = torch.cuda.current_stream()
     n_chunks = prog.n_chunks(args.chunk)
 
-    def step(profile=False):
+    def step(profile=False, detect=args.detect):
         r = prog.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank,
-                             world=world, profile=profile)
+                             world=world, profile=profile, detect=detect)
         if world > 1:
             r = reduce_results(r, names, device=torch.device("cuda", local))
         return r
@@ -265,7 +271,8 @@ def main():
         e_res = []
         for _ in range(args.steps):
             p2 = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
-            r = p2.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank, world=world)
+            r = p2.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank, world=world,
+                               detect=args.detect)
             if world > 1:
                 r = reduce_results(r, names, device=torch.device("cuda", local))
             e_res.append(r)
@@ -278,6 +285,28 @@ def main():
         e2e = {"value": sum(r.n_accesses for r in e_res) / wall / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": results[0].h2d_bytes, "d2h_bytes_per_step": results[0].d2h_bytes,
                "includes": "map_compile from MAP text + map_check_races (bytecode/segment H2D, result D2H)"}
+
+    # the other detect path on the same workload, for context (same timing rules)
+    alt = None
+    if not args.no_alt_path:
+        alt_mode = "sort" if args.detect != "sort" else "table"
+        step(detect=alt_mode)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        a_res = [step(detect=alt_mode) for _ in range(args.steps)]
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        same = all((x.verdict, x.witness, x.n_accesses, x.racy_segments) ==
+                   (results[0].verdict, results[0].witness, results[0].n_accesses, results[0].racy_segments)
+                   for x in a_res)
+        alt = {alt_mode: sum(x.n_accesses for x in a_res) / (float(ta.item()) / 1e3) / 1e9,
+               "identical_result": same}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -298,11 +327,14 @@ def main():
                        "l2": "inputs larger than L2: 8 GiB of keys per chunk vs 126 MB L2",
                        "verdict": "racy" if r0.verdict else "drf",
                        "witness": list(r0.witness.as_tuple()) if r0.witness else None},
-            "roofline": {"bound": "hbm", "kernel": "k_onesweep (radix pass)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": "k_rsweep (static-range LSD radix pass)", "achieved": achieved,
+                         "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if peak else None,
                          "traffic": ncu_traffic(),
                          "bytes_model": "16 B per key per active pass (8 read + 8 write)"},
             "kernels": kernels_out,
+            "detect_path": args.detect if args.detect != "auto" else "auto (table for dense chunks)",
+            "detect_paths": alt,
             "pipeline_bytes_per_access": sum(v["bytes"] for v in kern.values()) / max(1, total_acc),
             "gpu_launches": launches,
             "e2e": e2e,
