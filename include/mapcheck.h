@@ -180,13 +180,15 @@ const char *map_array_name(const map_program *p, uint32_t idx);
 void map_program_free(map_program *p);
 const char *map_status_str(map_status s);
 
-/* ---- stage API (multi-GPU orchestration from Python; NCCL via torch) -----
- * Shard `rank` of `world` owns the access keys whose sort field hashes to it
- * (SURVEY.md §8e).  map_generate_bucketed enumerates this rank's slice of the
- * tuple space (tuples t with t % world == rank) for chunk `chunk` and writes
- * keys grouped by destination rank into keys_out (capacity = the chunk's
- * bound), counts_out[world] on the HOST.  Keys use the chunk layout
- * (map_chunk_count / map_key_layout). */
+/* ---- stage API (multi-GPU key exchange; NCCL via torch) ----
+ * The hot path split at the exchange point, for a (phase, block) unit too
+ * large for one GPU: every rank generates a slice of a chunk's tuples, the keys
+ * are routed to the rank that owns their sort field (hash), and every rank
+ * sorts + detects what it received; a segment never straddles ranks, so the
+ * racy counts add up and the global witness is the minimum of the ranks'.
+ *
+ * map_chunk_count / map_chunk_info: the plan's chunks (same plan as
+ * map_check_races for the same chunk_max_accesses; 0 = library default). */
 map_status map_chunk_count(const map_program *p, uint64_t chunk_max_accesses, uint32_t *n_chunks);
 typedef struct {
   uint32_t phase_lo, phase_hi;   /* inclusive range of barrier phases                 */
@@ -195,10 +197,23 @@ typedef struct {
   uint32_t sort_bits, n_passes;  /* sort-field width and radix passes                  */
 } map_chunk_desc;
 map_status map_chunk_info(const map_program *p, uint64_t chunk_max_accesses, uint32_t chunk, map_chunk_desc *out);
+/* map_generate_bucketed: rank `rank` of `world` (world <= 64) generates the
+ * generate tiles [T*rank/world, T*(rank+1)/world) of chunk `chunk` (T = the
+ * chunk's tile count; every key compacted, bytecode VM) and writes them to
+ * keys_out (DEVICE, u64[>= map_chunk_desc.bound], caller-owned) grouped by
+ * destination d = hi64(splitmix64(sort field) * world), in order of d;
+ * counts_out[world] (HOST) receives the per-destination counts.  Uses ex's
+ * scratch and stream and synchronises the stream.  Errors: MAP_E_ARG (bad
+ * rank/world/chunk/pointers), MAP_E_NOMEM (scratch), MAP_E_ARITH (division by
+ * zero reached), MAP_E_CUDA. */
 map_status map_generate_bucketed(map_program *p, const map_exec *ex, uint32_t rank, uint32_t world,
                                  uint32_t chunk, void *keys_out, uint64_t *counts_out);
-/* Sort + detect n device-resident keys of chunk `chunk`; packed witness of the
- * chunk (UINT64_MAX = DRF) and its racy-segment count are written to the HOST. */
+/* map_sort_detect: sort + detect n DEVICE-resident keys of chunk `chunk` (e.g.
+ * the keys a rank received; n <= the plan's capacity, keys not modified, copied
+ * into scratch); the detect path follows ex->flags (MAP_DETECT_*).  The
+ * chunk's packed canonical witness (UINT64_MAX = DRF; decode with
+ * map_unpack_witness) and racy-segment count are written to the HOST.  Errors:
+ * MAP_E_ARG, MAP_E_NOMEM (n too large / scratch), MAP_E_CUDA. */
 map_status map_sort_detect(map_program *p, const map_exec *ex, uint32_t chunk, void *keys, uint64_t n,
                            uint64_t *packed_witness, uint64_t *racy_segments);
 map_status map_unpack_witness(const map_program *p, uint32_t chunk, uint64_t packed, map_witness *out);
