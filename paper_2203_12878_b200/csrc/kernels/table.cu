@@ -29,7 +29,7 @@ constexpr int TB_ITEMS = 8;
 constexpr int TB_TILE = TB_THREADS * TB_ITEMS;
 constexpr uint32_t TB_EMPTY = 0xFFFFFFFFu;
 
-struct TableSmem {
+struct __align__(16) TableSmem {
   uint32_t mn[TB_CELLS];                           // min tid (TB_EMPTY = no access)
   uint32_t mx[TB_CELLS];                           // max tid
   uint32_t wf[TB_CELLS / 4];                       // write flags, one byte per cell (plain stores:
@@ -48,46 +48,67 @@ struct TableSmem {
 __device__ __forceinline__ uint32_t cell_slot(uint32_t cell) { return cell ^ (((cell >> 5) ^ (cell >> 10)) & 31u); }
 
 __device__ __forceinline__ void table_reset(TableSmem& S) {
-  for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) { S.mn[i] = TB_EMPTY; S.mx[i] = 0; }
-  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) S.wf[i] = 0;
+  for (int g = threadIdx.x; g < TB_CELLS / 4; g += TB_THREADS) {
+    reinterpret_cast<uint4*>(S.mn)[g] = make_uint4(TB_EMPTY, TB_EMPTY, TB_EMPTY, TB_EMPTY);
+    reinterpret_cast<uint4*>(S.mx)[g] = make_uint4(0, 0, 0, 0);
+    S.wf[g] = 0;
+  }
 }
 
 // Scan a complete bucket's table: racy cells -> count and smallest sf.  Resets it.
 __device__ __forceinline__ void table_flush(TableSmem& S, unsigned long long bucket, uint32_t tb,
                                             unsigned long long& racy, unsigned long long& best) {
-  for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) {
-    const uint32_t m = S.mn[i], x = S.mx[i];
-    const bool w = reinterpret_cast<const uint8_t*>(S.wf)[i] != 0;
-    if (m != TB_EMPTY && w && m != x) {
-      ++racy;
-      best = min(best, (bucket << tb) | (unsigned long long)cell_slot(i));    // slot -> cell (involution)
+  // four consecutive slots per thread: 16-byte loads and stores, and one word of
+  // write flags -- a group without writes cannot hold a race
+  uint4* mn4 = reinterpret_cast<uint4*>(S.mn);
+  uint4* mx4 = reinterpret_cast<uint4*>(S.mx);
+  for (int g = threadIdx.x; g < TB_CELLS / 4; g += TB_THREADS) {
+    const uint32_t wf = S.wf[g];
+    if (wf) {
+      const uint4 m = mn4[g], x = mx4[g];
+      const uint32_t mm[4] = {m.x, m.y, m.z, m.w}, xx[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (((wf >> (8 * j)) & 0xFFu) && mm[j] != TB_EMPTY && mm[j] != xx[j]) {
+          ++racy;
+          best = min(best, (bucket << tb) | (unsigned long long)cell_slot(4 * g + j));   // slot -> cell
+        }
+      }
+      S.wf[g] = 0;
     }
-    S.mn[i] = TB_EMPTY;
-    S.mx[i] = 0;
+    mn4[g] = make_uint4(TB_EMPTY, TB_EMPTY, TB_EMPTY, TB_EMPTY);
+    mx4[g] = make_uint4(0, 0, 0, 0);
   }
-  __syncthreads();                                 // every cell has read its write flag
-  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) S.wf[i] = 0;
 }
 
-__device__ __forceinline__ void table_add(TableSmem& S, unsigned long long key, uint32_t pay_bits, uint32_t cmask,
-                                          uint32_t tmask) {
+// One key into the table: two fire-and-forget shared reductions and, for a
+// write, a byte store.  32-bit shared-window addresses computed once per CTA.
+struct TableAddr {
+  uint32_t mn, mx, wf;
+};
+
+__device__ __forceinline__ void table_add(const TableAddr& A, unsigned long long key, uint32_t pay_bits,
+                                          uint32_t cmask, uint32_t tmask) {
   const uint32_t cell = cell_slot((uint32_t)(key >> pay_bits) & cmask);
   const uint32_t t = (uint32_t)(key >> 1) & tmask;
-  atomicMin(&S.mn[cell], t);
-  atomicMax(&S.mx[cell], t);
-  if (key & 1ull) reinterpret_cast<volatile uint8_t*>(S.wf)[cell] = 1;
+  asm volatile("red.shared.min.u32 [%0], %1;" :: "r"(A.mn + 4 * cell), "r"(t));
+  asm volatile("red.shared.max.u32 [%0], %1;" :: "r"(A.mx + 4 * cell), "r"(t));
+  if (key & 1ull) asm volatile("st.shared.u8 [%0], %1;" :: "r"(A.wf + cell), "r"(1u));
 }
 
 __device__ __forceinline__ void table_spill(TableSmem& S, MapcTablePart* part, uint32_t* store,
                                             unsigned long long bucket, uint32_t ends) {
-  uint32_t* mn = store;
-  uint32_t* mx = store + TB_CELLS;
+  uint4* mn = reinterpret_cast<uint4*>(store);
+  uint4* mx = reinterpret_cast<uint4*>(store + TB_CELLS);
   uint32_t* wf = store + 2 * TB_CELLS;
-  for (int i = threadIdx.x; i < TB_CELLS; i += TB_THREADS) {
-    mn[i] = S.mn[i]; mx[i] = S.mx[i];
-    S.mn[i] = TB_EMPTY; S.mx[i] = 0;
+  for (int g = threadIdx.x; g < TB_CELLS / 4; g += TB_THREADS) {
+    mn[g] = reinterpret_cast<const uint4*>(S.mn)[g];
+    mx[g] = reinterpret_cast<const uint4*>(S.mx)[g];
+    wf[g] = S.wf[g];
+    reinterpret_cast<uint4*>(S.mn)[g] = make_uint4(TB_EMPTY, TB_EMPTY, TB_EMPTY, TB_EMPTY);
+    reinterpret_cast<uint4*>(S.mx)[g] = make_uint4(0, 0, 0, 0);
+    S.wf[g] = 0;
   }
-  for (int i = threadIdx.x; i < TB_CELLS / 4; i += TB_THREADS) { wf[i] = S.wf[i]; S.wf[i] = 0; }
   if (threadIdx.x == 0) { part->bucket = bucket; part->ends = ends; part->valid = 1; }
 }
 
@@ -117,6 +138,8 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
   }
   table_reset(S);
   unsigned long long racy = 0, best = ~0ull;
+  const TableAddr A{(uint32_t)__cvta_generic_to_shared(S.mn), (uint32_t)__cvta_generic_to_shared(S.mx),
+                    (uint32_t)__cvta_generic_to_shared(S.wf)};
   __syncthreads();
   unsigned long long cur = S.b_first;
 
@@ -152,7 +175,7 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
       // common case: the whole tile belongs to the open bucket
 #pragma unroll
       for (int j = 0; j < TB_ITEMS; ++j)
-        if (j * TB_THREADS + threadIdx.x < tn) table_add(S, k[j], pay_bits, cmask, tmask);
+        if (j * TB_THREADS + threadIdx.x < tn) table_add(A, k[j], pay_bits, cmask, tmask);
       continue;
     }
     // the tile closes one or more buckets: one sweep per bucket present (keys re-read from L2)
@@ -171,7 +194,7 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
           const uint32_t li = j * TB_THREADS + threadIdx.x;
           const unsigned long long b = kk[j] >> bsh;
           if (li < tn) {
-            if (b == cur) table_add(S, kk[j], pay_bits, cmask, tmask);
+            if (b == cur) table_add(A, kk[j], pay_bits, cmask, tmask);
             else if (b > cur) nb = min(nb, b);
           }
         }
