@@ -157,7 +157,8 @@ struct RsSmem {
   uint32_t pos[WARPS][MAPC_RADIX];                 // running tile position per (warp, digit)
   uint32_t mask[WARPS][MAPC_RADIX];                // early counts, then peer masks
   unsigned long long running[MAPC_RADIX];          // global output cursor per digit
-  unsigned long long gbase[MAPC_RADIX];
+  unsigned long long gbase[MAPC_RADIX];           // output index of tile position 0 for digit d
+  unsigned long long gaddr[MAPC_RADIX];           // the same as a byte address in dst (mod 2^64)
   uint32_t scan_tmp[WARPS + 1];
 };
 
@@ -253,6 +254,7 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
         S.mask[ww][d] = 0;
       }
       S.gbase[d] = S.running[d] - dex;
+      S.gaddr[d] = reinterpret_cast<unsigned long long>(dst) + 8ull * (S.running[d] - dex);
       S.running[d] += count;
     }
     __syncthreads();
@@ -289,13 +291,24 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
     }
     __syncthreads();
     load_tile(tb + TILE, k);                             // in flight during the write-out
-    for (uint32_t i = threadIdx.x; i < tile_n; i += THREADS) {
-      const unsigned long long key = S.keys[kslot(i)];
-      const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
-      const unsigned long long p = S.gbase[d] + i;
-      dst[p] = key;
-      if (has_next)
-        atomicAdd(&tab[fastdiv((uint32_t)p, rdiv) * MAPC_RADIX + ((uint32_t)(key >> nshift) & 0xFFu)], 1u);
+    if (!FUSE_NEXT && tile_n == TILE) {
+      // full tile: key i of the tile goes to byte address gaddr[digit] + 8 i
+#pragma unroll
+      for (int u = 0; u < ITEMS; ++u) {
+        const uint32_t i = u * THREADS + threadIdx.x;
+        const unsigned long long key = S.keys[kslot(i)];
+        const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
+        *reinterpret_cast<unsigned long long*>(S.gaddr[d] + 8ull * i) = key;
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < tile_n; i += THREADS) {
+        const unsigned long long key = S.keys[kslot(i)];
+        const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
+        const unsigned long long p = S.gbase[d] + i;
+        dst[p] = key;
+        if (has_next)
+          atomicAdd(&tab[fastdiv((uint32_t)p, rdiv) * MAPC_RADIX + ((uint32_t)(key >> nshift) & 0xFFu)], 1u);
+      }
     }
   }
   if (has_next) {
