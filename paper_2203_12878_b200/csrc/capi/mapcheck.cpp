@@ -951,6 +951,18 @@ size_t map_debug_dump(const map_program* p, char* buf, size_t cap) {
 
 // Generate + NVRTC-compile the specialised generate module without loading it
 // (no GPU needed): 0 on success, else writes the compiler log.  Test hook.
+// The specialised generate source of one chunk (debugging / SASS inspection).
+size_t map_debug_jit_source(const map_program* cp, uint64_t chunk_max_accesses, uint32_t chunk, char* out,
+                            size_t cap) {
+  map_program* p = const_cast<map_program*>(cp);
+  if (!p || ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p)) != MAP_OK) return 0;
+  if (chunk >= p->plan.chunks.size()) return 0;
+  std::vector<mapj::JitChunk> one{p->plan.chunks[chunk].jit};
+  const std::string src = mapj::module_source(one, p->C.u32_mode);
+  put_diag(src, out, cap);
+  return src.size();
+}
+
 int map_debug_jit_check(const map_program* cp, uint64_t chunk_max_accesses, char* log, size_t cap) {
   map_program* p = const_cast<map_program*>(cp);
   if (!p) return -1;

@@ -207,6 +207,10 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
       __syncthreads();
       cur = S.next_bucket;
       __syncthreads();
+      if (cur == ~0ull) {                 // no later bucket in the tile: unsorted input (flagged, not looped on)
+        if (threadIdx.x == 0) atomicOr(&ctrl->err, MAPC_ERR_LAYOUT);
+        break;
+      }
     }
   }
   __syncthreads();

@@ -254,3 +254,16 @@ def test_full_size_detect_paths_agree(name):
     a = p.check_races(detect="sort")
     b = p.check_races(detect="table")
     assert (a.verdict, a.witness, a.n_accesses, a.racy_segments) == (b.verdict, b.witness, b.n_accesses, b.racy_segments)
+
+
+@pytest.mark.parametrize("detect", ["sort", "table"])
+@pytest.mark.parametrize("name,sizes", [("5a", dict(T=3, R=8, C=64)), ("5b", dict(T=2, R=4, C=96)),
+                                        ("5b", dict(T=1, R=3, C=40)), ("1a", dict(M=4096))])
+def test_jit_single_segment_chunks(name, sizes, detect):
+    # one phase per chunk, JIT generate: a single all-dense segment per chunk
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    unit = max(1, p.info.max_unit_accesses)
+    for chunk in (0, unit):
+        same(p.check_races(gen="jit", chunk_max_accesses=chunk, detect=detect), o)
