@@ -158,10 +158,15 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
     const uint32_t tn = (uint32_t)min((unsigned long long)TB_TILE, r1 - t0);
     // the tile's keys and its first / last bucket are loaded together (one round trip)
     unsigned long long k[TB_ITEMS];
+    if (tn == TB_TILE) {
 #pragma unroll
-    for (int j = 0; j < TB_ITEMS; ++j) {
-      const uint32_t li = j * TB_THREADS + threadIdx.x;
-      k[j] = li < tn ? ld_stream(keys + t0 + li) : 0ull;
+      for (int j = 0; j < TB_ITEMS; ++j) k[j] = ld_stream(keys + t0 + j * TB_THREADS + threadIdx.x);
+    } else {
+#pragma unroll
+      for (int j = 0; j < TB_ITEMS; ++j) {
+        const uint32_t li = j * TB_THREADS + threadIdx.x;
+        k[j] = li < tn ? ld_stream(keys + t0 + li) : 0ull;
+      }
     }
     const unsigned long long bf = keys[t0] >> bsh, bl = keys[t0 + tn - 1] >> bsh;
     if (bf != cur) {
@@ -173,9 +178,14 @@ k_detect_table(const unsigned long long* __restrict__ bufA, const unsigned long 
     }
     if (bl == cur) {
       // common case: the whole tile belongs to the open bucket
+      if (tn == TB_TILE) {
 #pragma unroll
-      for (int j = 0; j < TB_ITEMS; ++j)
-        if (j * TB_THREADS + threadIdx.x < tn) table_add(A, k[j], pay_bits, cmask, tmask);
+        for (int j = 0; j < TB_ITEMS; ++j) table_add(A, k[j], pay_bits, cmask, tmask);
+      } else {
+#pragma unroll
+        for (int j = 0; j < TB_ITEMS; ++j)
+          if (j * TB_THREADS + threadIdx.x < tn) table_add(A, k[j], pay_bits, cmask, tmask);
+      }
       continue;
     }
     // the tile closes one or more buckets: one sweep per bucket present (keys re-read from L2)
