@@ -43,7 +43,9 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="5a")
     ap.add_argument("--chunk", type=int, default=0, help="chunk_max_accesses (0 = library default, 2^30)")
-    ap.add_argument("--cpu-rows", type=int, default=64, help="R of the oracle's bounded sample of the workload")
+    ap.add_argument("--cpu-rows", type=int, default=64, help="R of the oracle's bounded sample (cpu_baseline leg)")
+    ap.add_argument("--ref-rows", type=int, default=16,
+                    help="R of the oracle's bounded sample per step of --impl reference (K+W steps must fit minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--detect", choices=["auto", "sort", "table"], default="auto")
@@ -140,7 +142,7 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return
     inst = config(args.config)
-    samp = oracle_sample(inst, args.cpu_rows)
+    samp = oracle_sample(inst, args.ref_rows)
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
         run_oracle(samp, cores)
@@ -310,7 +312,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        samp = oracle_sample(inst, args.cpu_rows)
+        samp = oracle_sample(inst, args.ref_rows)
         cores = os.cpu_count() or 1
         orc, dt = run_oracle(samp, cores)
         cpu = {"value": orc.n_accesses / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
