@@ -312,7 +312,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        samp = oracle_sample(inst, args.ref_rows)
+        samp = oracle_sample(inst, args.cpu_rows)
         cores = os.cpu_count() or 1
         orc, dt = run_oracle(samp, cores)
         cpu = {"value": orc.n_accesses / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
