@@ -59,6 +59,8 @@ def _load():
                                          ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint64,
                                          ctypes.c_char_p, ctypes.c_size_t]
         lib.oracle_enumerate.restype = ctypes.c_int64
+        lib.oracle_list_races.argtypes = lib.oracle_enumerate.argtypes
+        lib.oracle_list_races.restype = ctypes.c_int64
         lib.oracle_arrays.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]
         lib.oracle_arrays.restype = ctypes.c_int
         _lib = lib
@@ -128,6 +130,27 @@ def enumerate_accesses(src: str, grid=(1, 1, 1), block=(1, 1, 1), params=None, t
     lib.oracle_enumerate(src.encode(), g, b, n, cn, cv, threads,
                          buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cnt, diag, 512)
     return buf[:cnt]
+
+
+def list_races(src: str, grid=(1, 1, 1), block=(1, 1, 1), params=None, threads: int = 0):
+    """Every racy segment's minimal pair (phase, array, block, index, t_lo, t_hi, k_lo, k_hi),
+    in canonical order (the per-segment form of SPEC.md:434-437 races_of)."""
+    lib = _load()
+    params = params or {}
+    g, b, n, cn, cv = _args(grid, block, params)
+    diag = ctypes.create_string_buffer(512)
+    nt = threads if threads > 0 else (os.cpu_count() or 1)
+    cnt = lib.oracle_list_races(src.encode(), g, b, n, cn, cv, nt, None, 0, diag, 512)
+    if cnt < 0:
+        raise ValueError(f"oracle status {STATUS.get(-cnt, -cnt)}: {diag.value.decode()}")
+    buf = np.zeros((max(cnt, 1), 8), dtype=np.uint64)
+    lib.oracle_list_races(src.encode(), g, b, n, cn, cv, nt,
+                          buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cnt, diag, 512)
+    return [tuple(int(x) for x in row) for row in buf[:cnt]]
+
+
+def list_races_instance(inst, threads: int = 0):
+    return list_races(inst.src, inst.grid, inst.block, inst.params, threads)
 
 
 def array_names(src: str):

@@ -40,6 +40,7 @@
 // 8 bad argument.
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cctype>
 #include <cstdint>
@@ -618,8 +619,9 @@ bool rec_eq(const Record& x, const Record& y) {
          x.tid == y.tid && x.wr == y.wr;
 }
 
-// Steps 3-5.
-void races(std::vector<Record>& recs, int nt, Result& r) {
+// Steps 3-5.  `list` (optional): every racy bucket's minimal pair, in bucket
+// order -- the per-segment form of SPEC.md:434-437 races_of.
+void races(std::vector<Record>& recs, int nt, Result& r, std::vector<std::array<uint64_t, 8>>* list = nullptr) {
   r.n_accesses = recs.size();
   uint32_t maxphase = 0;
   for (auto& x : recs) maxphase = std::max(maxphase, x.phase);
@@ -659,6 +661,9 @@ void races(std::vector<Record>& recs, int nt, Result& r) {
       }
     if (racy) {
       ++r.n_racy_segments;
+      if (list)
+        list->push_back({recs[i].phase, recs[i].array, recs[i].block, recs[i].index, best[0], best[1], best[2],
+                         best[3]});
       if (!have) {     // buckets are visited in lexicographic order: first is min
         have = true;
         r.phase = recs[i].phase; r.array = recs[i].array; r.block = recs[i].block; r.index = recs[i].index;
@@ -739,6 +744,27 @@ int64_t oracle_enumerate(const char* src, const uint32_t grid[3], const uint32_t
     o[0] = x.phase; o[1] = x.array; o[2] = x.block; o[3] = x.index; o[4] = x.tid; o[5] = x.wr;
   }
   return (int64_t)recs.size();
+}
+
+// Every racy segment's minimal pair (phase, array, block, index, t_lo, t_hi,
+// k_lo, k_hi) as 8 x u64, in canonical order; returns the number of racy
+// segments (or -status), writes at most `cap` of them.
+int64_t oracle_list_races(const char* src, const uint32_t grid[3], const uint32_t blk[3], uint32_t n_params,
+                          const char* const* names, const uint64_t* values, int n_threads, uint64_t* out,
+                          uint64_t cap, char* diag, size_t diag_cap) {
+  Setup S;
+  std::string d;
+  int st = setup(src, grid, blk, n_params, names, values, S, d);
+  std::vector<Record> recs;
+  if (st == OK) st = enumerate(S, n_threads, recs, d);
+  put_diag(d, diag, diag_cap);
+  if (st != OK) return -(int64_t)st;
+  Result r;
+  std::vector<std::array<uint64_t, 8>> list;
+  races(recs, n_threads, r, &list);
+  for (uint64_t i = 0; i < list.size() && i < cap; ++i)
+    for (int f = 0; f < 8; ++f) out[8 * i + f] = list[i][f];
+  return (int64_t)list.size();
 }
 
 // Array names in declaration order (array ids); returns count.

@@ -47,6 +47,27 @@ def races(records):
     return (1 if best is not None else 0), best, racy_segments, n
 
 
+def race_list(records):
+    """Every racy (phase, array, block, index) cell's minimal pair, sorted: the
+    per-segment listing of SPEC.md:434-437 races_of, by naive pair testing."""
+    groups = defaultdict(set)
+    for (ph, ar, bl, ix, t, k) in records:
+        groups[(ph, ar, bl, ix)].add((t, k))
+    out = []
+    for key, vals in groups.items():
+        best = None
+        for (t1, k1), (t2, k2) in itertools.combinations(sorted(vals), 2):
+            if t1 == t2 or (k1 == RD and k2 == RD):
+                continue
+            lo, hi = ((t1, k1), (t2, k2)) if t1 < t2 else ((t2, k2), (t1, k1))
+            cand = key + (lo[0], hi[0], lo[1], hi[1])
+            if best is None or cand < best:
+                best = cand
+        if best is not None:
+            out.append(best)
+    return sorted(out)
+
+
 def races_all_pairs(records):
     """Same verdict/witness by testing every pair of the whole multiset (O(N^2))."""
     best = None

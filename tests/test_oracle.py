@@ -182,6 +182,40 @@ def test_fuzz_vs_brute():
     assert 0.1 * N_FUZZ < n_racy < 0.9 * N_FUZZ
 
 
+# ------------------------------------------- race listing (NEXT-4) ---------
+@pytest.mark.parametrize("name,sizes", BRUTE_CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(BRUTE_CASES)])
+def test_race_list_vs_hand_loops(name, sizes):
+    # SPEC.md:434-437 races_of, one minimal pair per racy segment: the oracle's list
+    # equals the naive per-cell pair test over the hand-written loops
+    inst = config(name, **sizes)
+    recs = brute.config_records(inst)
+    assert oracle.list_races_instance(inst) == brute.race_list(recs)
+
+
+def test_race_list_fuzz_vs_brute():
+    bad = []
+    for seed in range(0, N_FUZZ, 3):
+        inst, prog = fuzz.random_instance(seed)
+        recs = brute.eval_ast(prog, inst.grid, inst.block, inst.params)
+        got = oracle.list_races_instance(inst, threads=1)
+        if got != brute.race_list(recs):
+            bad.append((seed, inst.src))
+    assert not bad, bad[:3]
+
+
+def test_race_list_invariants():
+    for name, sizes in [("2b", dict(block=64)), ("3b", dict(ts=8, rw=2, grid=3)), ("4b", dict(n=256, bs=16)),
+                        ("5b", dict(block=8, T=2, R=2, C=8)), ("2a", dict(block=64))]:
+        inst = config(name, **sizes)
+        r = oracle.check_instance(inst)
+        lst = oracle.list_races_instance(inst)
+        assert len(lst) == r.n_racy_segments
+        assert lst == sorted(lst) and len(set(x[:4] for x in lst)) == len(lst)   # one entry per cell
+        assert (lst[0] if lst else None) == r.witness
+        for (_, _, _, _, tlo, thi, klo, khi) in lst:
+            assert tlo < thi and (klo == 1 or khi == 1)
+
+
 # ------------------------------------------------------------ invariants ----
 def test_thread_count_independence():
     for name, sizes in [("3b", dict(ts=8, rw=2, grid=5)), ("4d", dict(n=256, bs=16)), ("5b", dict(block=16, T=2, R=2, C=4))]:
