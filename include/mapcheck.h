@@ -174,6 +174,16 @@ map_status map_check_races(map_program *p, const map_exec *ex, map_result *out);
 /* Canonical witness of the last racy map_check_races; MAP_E_ARG if it was DRF. */
 map_status map_witness_get(const map_program *p, map_witness *out);
 
+/* Full race listing (SPEC.md:434-437 races_of, one entry
+ * per racy (phase, array, block, index) segment): the canonical witness of
+ * every racy segment, in canonical (lexicographic) order.  Runs the whole
+ * pipeline with the full sort on every chunk of the plan (ex->rank/world and
+ * the MAP_DETECT_* flags are ignored).  out[cap] (HOST, caller-owned) receives
+ * the min(cap, *n_total) smallest; *n_total = the number of racy segments (the
+ * racy_segments of map_check_races).  array_name pointers stay valid until
+ * map_program_free.  Errors as map_check_races. */
+map_status map_list_races(map_program *p, const map_exec *ex, map_witness *out, uint64_t cap, uint64_t *n_total);
+
 /* Name of array `idx` (declaration order; NULL if out of range). */
 const char *map_array_name(const map_program *p, uint32_t idx);
 

@@ -38,7 +38,7 @@ STATUS = {
 EXPORTS = (
     "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
     "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
-    "map_sort_detect", "map_unpack_witness", "map_array_name", "map_chunk_info",
+    "map_sort_detect", "map_unpack_witness", "map_array_name", "map_chunk_info", "map_list_races",
 )
 
 
@@ -119,6 +119,9 @@ _lib.map_unpack_witness.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint64, ctypes
 _lib.map_unpack_witness.restype = ctypes.c_int
 _lib.map_chunk_info.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_ChunkDesc)]
 _lib.map_chunk_info.restype = ctypes.c_int
+_lib.map_list_races.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.POINTER(_Witness), ctypes.c_uint64,
+                               ctypes.POINTER(ctypes.c_uint64)]
+_lib.map_list_races.restype = ctypes.c_int
 _lib.map_array_name.argtypes = [_P, ctypes.c_uint32]
 _lib.map_array_name.restype = ctypes.c_char_p
 _lib.map_debug_dump.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
@@ -260,6 +263,21 @@ class MapProgram:
             raise MapError(st, "bad packed witness")
         return Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
                        w.array_name.decode())
+
+    def list_races(self, cap: int = 1 << 20, scratch=None, stream=None, chunk_max_accesses: int = 0):
+        """All racy segments (NEXT-4): (total count, canonical witnesses of the `cap` smallest, in order)."""
+        import torch
+        if scratch is None:
+            scratch = torch.empty(self.scratch_bytes(chunk_max_accesses), dtype=torch.uint8, device="cuda")
+        ex = self._exec(scratch, stream, chunk_max_accesses)
+        buf = (_Witness * max(1, cap))()
+        total = ctypes.c_uint64()
+        st = _lib.map_list_races(self._h, ctypes.byref(ex), buf, int(cap), ctypes.byref(total))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        k = min(cap, total.value)
+        return total.value, [Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
+                                     w.array_name.decode()) for w in buf[:k]]
 
     def array_names(self):
         out = []

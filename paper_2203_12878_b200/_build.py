@@ -19,8 +19,10 @@ SOURCES = [
     "kernels/rsweep.cu",
     "kernels/exchange.cu",
     "kernels/table.cu",
+    "kernels/listing.cu",
 ]
-HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "capi/jit.h"]
+HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "kernels/segstate.cuh",
+           "capi/jit.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -60,6 +60,10 @@ cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigne
                                    unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 int mapc_rsweep_fused();
 int mapc_table_ctas(int n_sms);
+cudaError_t mapc_launch_list_racy(const unsigned long long* bufA, const unsigned long long* bufB, const MapcCtrl* ctrl,
+                                  uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, unsigned long long* counts,
+                                  unsigned int max_warps, unsigned long long* out, unsigned long long cap,
+                                  unsigned long long* total, unsigned long long max_keys, int n_sms, cudaStream_t s);
 cudaError_t mapc_launch_detect_table(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
                                      uint32_t n_passes, uint32_t pay_bits, uint32_t tb, uint32_t w_tid,
                                      MapcTablePart* parts, uint32_t* store, unsigned long long max_keys, int n_sms,
@@ -902,6 +906,81 @@ map_status map_sort_detect(map_program* p, const map_exec* ex, uint32_t chunk, v
   if (r.err) { p->last_error = "internal consistency check failed"; return MAP_E_RANGE; }
   *packed_witness = r.witness;
   *racy_segments = r.racy;
+  return MAP_OK;
+}
+
+// All racy segments (NEXT-4): per chunk, generate (bytecode VM) + full LSD sort,
+// then two listing passes write every racy segment's packed canonical witness
+// in sort-field order into the chunk's free key buffer; the host decodes them
+// and merges the chunks' lists in canonical order (a phase split by block
+// ranges interleaves arrays, so chunk order alone is not canonical).
+map_status map_list_races(map_program* p, const map_exec* ex, map_witness* out, uint64_t cap, uint64_t* n_total) {
+  if (!p || !ex || !n_total || (cap && !out)) return MAP_E_ARG;
+  Dev d0;
+  map_status st = stage_setup(p, ex, 0, &d0);
+  if (st == MAP_E_ARG && p->plan.chunks.empty()) {          // no accesses at all
+    *n_total = 0;
+    return MAP_OK;
+  }
+  if (st != MAP_OK) return st;
+  Plan& P = p->plan;
+  std::vector<map_witness> all;
+  uint64_t total = 0;
+  for (uint32_t c = 0; c < P.chunks.size(); ++c) {
+    Dev d;
+    st = stage_setup(p, ex, c, &d);
+    if (st != MAP_OK) return st;
+    const Chunk& ch = P.chunks[c];
+    const MapcLayout L = effective_layout(ch, MAP_DETECT_SORT);
+    CK(mapc_upload_ops(ch.ops.data(), ch.ops.size(), d.s));
+    CK(cudaMemcpyAsync(d.segs, ch.segs.data(), ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, d.s));
+    CK(mapc_launch_chunk_init(d.ctrl, ch.dense_total, d.s));
+    if (ch.total_tiles)
+      CK(mapc_launch_generate(d.segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, d.bufA,
+                              d.ctrl, d.n_sms, ch.nreg, ch.max_emits, 0, d.s));
+    if (L.n_passes) {
+      CK(cudaMemsetAsync(d.rhist, 0, P.rh_bytes, d.s));
+      CK(mapc_launch_hist_ranges(d.bufA, d.ctrl, d.rhist, L.sort_lo, L.n_passes, d.G, d.s));
+    }
+    CK(mapc_launch_digit_scan(d.ctrl, L.n_passes, d.s));
+    for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
+      if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
+      CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
+    }
+    CK(mapc_launch_chunk_finish(d.ctrl, L.n_passes, d.res + c, d.s));
+    MapcChunkResult r{};
+    unsigned int sel = 0;
+    CK(cudaMemcpyAsync(&r, d.res + c, sizeof(r), cudaMemcpyDeviceToHost, d.s));
+    CK(cudaMemcpyAsync(&sel, &d.ctrl->sel[L.n_passes], sizeof(sel), cudaMemcpyDeviceToHost, d.s));
+    CK(cudaStreamSynchronize(d.s));
+    if (r.err & MAPC_ERR_DIV0) { p->last_error = "division or modulo by zero on a reached path"; return MAP_E_ARITH; }
+    if (r.err) { p->last_error = "internal consistency check failed"; return MAP_E_RANGE; }
+    if (r.n == 0) continue;
+    unsigned long long* free_buf = sel ? d.bufA : d.bufB;       // the buffer not holding the sorted keys
+    const uint64_t dev_cap = std::min<uint64_t>(cap, P.cap);
+    auto* counts = reinterpret_cast<unsigned long long*>(d.ff);
+    CK(mapc_launch_list_racy(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.w_tid, counts, MAPC_DETECT_MAX_UNITS,
+                             free_buf, dev_cap, d.xch, r.n, d.n_sms, d.s));
+    unsigned long long nr = 0;
+    CK(cudaMemcpyAsync(&nr, d.xch, sizeof(nr), cudaMemcpyDeviceToHost, d.s));
+    CK(cudaStreamSynchronize(d.s));
+    total += nr;
+    const uint64_t take = std::min<uint64_t>(nr, dev_cap);
+    std::vector<unsigned long long> packed(take);
+    if (take) {
+      CK(cudaMemcpyAsync(packed.data(), free_buf, take * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d.s));
+      CK(cudaStreamSynchronize(d.s));
+    }
+    for (unsigned long long w : packed) {
+      map_witness mw{};
+      decode(p->C, ch, w, &mw);
+      all.push_back(mw);
+    }
+  }
+  std::sort(all.begin(), all.end(), wit_less);
+  const uint64_t k = std::min<uint64_t>(cap, all.size());
+  for (uint64_t i = 0; i < k; ++i) out[i] = all[i];
+  *n_total = total;
   return MAP_OK;
 }
 

@@ -267,3 +267,51 @@ def test_jit_single_segment_chunks(name, sizes, detect):
     unit = max(1, p.info.max_unit_accesses)
     for chunk in (0, unit):
         same(p.check_races(gen="jit", chunk_max_accesses=chunk, detect=detect), o)
+
+
+# ---- full race listing (NEXT-4) ----------------------------------------------
+
+@pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
+def test_race_list_matches_oracle(name, sizes):
+    inst = config(name, **sizes)
+    want = oracle.list_races_instance(inst)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    total, got = p.list_races(cap=len(want) + 10)
+    assert total == len(want)
+    assert [w.as_tuple() for w in got] == want
+    # chunks forced to one (phase, block) unit: the merged lists stay canonical
+    unit = max(1, p.info.max_unit_accesses)
+    total, got = p.list_races(cap=len(want) + 10, chunk_max_accesses=unit)
+    assert total == len(want) and [w.as_tuple() for w in got] == want
+
+
+def test_race_list_prefix_and_fuzz():
+    bad = []
+    for seed in range(0, 300, 3):
+        inst, _ = fuzz.random_instance(seed)
+        want = oracle.list_races_instance(inst, threads=1)
+        p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+        for cap in (0, 1, 3, len(want) + 1):
+            total, got = p.list_races(cap=cap)
+            if total != len(want) or [w.as_tuple() for w in got] != want[:cap]:
+                bad.append((seed, cap, inst.src))
+    assert not bad, bad[:3]
+
+
+def test_race_list_long_segments():
+    src = "params N; forU x in 0..N { rd[x % 8] }; wr[tid % 4]"
+    want = oracle.list_races(src, block=(1024, 1, 1), params={"N": 4096})
+    total, got = mc.MapProgram(src, (1, 1, 1), (1024, 1, 1), {"N": 4096}).list_races(cap=100)
+    assert total == len(want) and [w.as_tuple() for w in got] == want
+
+
+@pytest.mark.parametrize("name", ["3b", "4b"])
+def test_race_list_full_size_properties(name):
+    inst = config(name)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    r = p.check_races()
+    total, got = p.list_races(cap=4096)
+    assert total == r.racy_segments
+    assert got[0].as_tuple() == r.witness.as_tuple()
+    tuples = [w.as_tuple() for w in got]
+    assert tuples == sorted(tuples) and len(set(t[:4] for t in tuples)) == len(tuples)
