@@ -71,7 +71,8 @@ cudaError_t mapc_launch_detect_table(const unsigned long long* bufA, const unsig
 cudaError_t mapc_launch_witness(const unsigned long long* bufA, const unsigned long long* bufB, MapcCtrl* ctrl,
                                 uint32_t n_passes, uint32_t pay_bits, uint32_t tb, uint32_t w_tid, cudaStream_t s);
 cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
-                               unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
+                               unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, int red_next,
+                               cudaStream_t s);
 }
 
 namespace {
@@ -365,6 +366,14 @@ MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~
   return L;
 }
 
+// Whether a radix pass also accumulates the next pass's range table (k_rsweep
+// RED_NEXT): on the bucket-table path the digits are high sort-field bits, which
+// dense MAPs keep warp-uniform; the kernel falls back by itself otherwise.
+int red_next(const MapcLayout& L) {
+  static const bool off = getenv("MAPC_RED_NEXT") && getenv("MAPC_RED_NEXT")[0] == '0';
+  return (!off && L.tb > 0) ? 1 : 0;
+}
+
 void put_diag(const std::string& d, char* diag, size_t cap) {
   if (!diag || !cap) return;
   size_t n = std::min(cap - 1, d.size());
@@ -639,7 +648,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
           end(m);
         }
         m = begin(MAP_K_ONESWEEP);
-        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, s));
+        CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, red_next(L), s));
         end(m);
       }
     } else {
@@ -890,7 +899,7 @@ map_status map_sort_detect(map_program* p, const map_exec* ex, uint32_t chunk, v
   CK(mapc_launch_digit_scan(d.ctrl, L.n_passes, d.s));
   for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
     if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
-    CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
+    CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, red_next(L), d.s));
   }
   if (L.tb)
     CK(mapc_launch_detect_table(d.bufA, d.bufB, d.ctrl, L.n_passes, L.pay_bits, L.tb, L.w_tid, d.tparts, d.tstore,
@@ -945,7 +954,7 @@ map_status map_list_races(map_program* p, const map_exec* ex, map_witness* out, 
     CK(mapc_launch_digit_scan(d.ctrl, L.n_passes, d.s));
     for (uint32_t pass = 0; pass < L.n_passes; ++pass) {
       if (pass > 0) CK(mapc_launch_range_hist(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
-      CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, d.s));
+      CK(mapc_launch_rsweep(d.bufA, d.bufB, d.ctrl, d.rhist, pass, L.sort_lo, d.G, red_next(L), d.s));
     }
     CK(mapc_launch_chunk_finish(d.ctrl, L.n_passes, d.res + c, d.s));
     MapcChunkResult r{};

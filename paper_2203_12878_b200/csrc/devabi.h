@@ -131,6 +131,8 @@ struct MapcCtrl {
   unsigned int rng_L;
   unsigned int first_active;                // first active pass (MAPC_MAX_PASSES if none)
   unsigned int next_active[MAPC_MAX_PASSES];// next active pass after p (MAPC_MAX_PASSES if none)
+  unsigned int rt_done[MAPC_MAX_PASSES];    // pass p's range table accumulated by the previous scatter
+  unsigned int rt_bad[MAPC_MAX_PASSES];     // ... but abandoned (digits not warp-uniform): recompute
   MapcFastDiv rng_div;                      // divides a key position by rng_L
 };
 

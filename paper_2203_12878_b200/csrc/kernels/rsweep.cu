@@ -108,7 +108,8 @@ k_range_hist(const unsigned long long* __restrict__ bufA, const unsigned long lo
              MapcCtrl* __restrict__ ctrl, unsigned int* __restrict__ rhist, uint32_t p, uint32_t pay_bits,
              uint32_t fused) {
   if (p == 0 || !ctrl->active[p]) return;
-  if (fused && p != ctrl->first_active) return;      // produced by the previous active pass's scatter
+  if (ctrl->rt_done[p] && !ctrl->rt_bad[p]) return;  // accumulated by the previous pass's scatter
+  (void)fused;
   const unsigned long long* __restrict__ keys = ctrl->sel[p] ? bufB : bufA;
   __shared__ uint32_t h[MAPC_RADIX];
   for (int i = threadIdx.x; i < MAPC_RADIX; i += RH_THREADS) h[i] = 0;
@@ -162,7 +163,13 @@ struct RsSmem {
   uint32_t scan_tmp[WARPS + 1];
 };
 
-template <int THREADS, int ITEMS, bool FUSE_NEXT, int MINB>
+// RED_NEXT: the scatter also accumulates the NEXT active pass's range table:
+// an output position fixes its range, so each warp row of 32 consecutive
+// outputs adds (range, next digit) to rhist -- once, +32, when the row is
+// uniform (bucket digits of dense MAPs: the common case), else per key.  A CTA
+// whose rows turn out mostly non-uniform abandons (rt_bad) and k_range_hist
+// recomputes the table from one read, as without fusion.
+template <int THREADS, int ITEMS, bool RED_NEXT, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
 k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__ bufB, MapcCtrl* __restrict__ ctrl,
          unsigned int* __restrict__ rhist, uint32_t pass, uint32_t pay_bits) {
@@ -171,11 +178,14 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
   if (!ctrl->active[pass]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
-  uint32_t* tab = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Sm));   // [G][256]
   const uint32_t G = gridDim.x;
   const uint32_t shift = pay_bits + 8 * pass;
   const uint32_t nxt = ctrl->next_active[pass];
-  const bool has_next = FUSE_NEXT && nxt < MAPC_MAX_PASSES;
+  bool fuse_on = RED_NEXT && nxt < MAPC_MAX_PASSES && !ctrl->rt_bad[nxt];
+  unsigned int* __restrict__ next_tab = rhist + (size_t)(nxt < MAPC_MAX_PASSES ? nxt : 0) * MAPC_MAX_RANGES * MAPC_RADIX;
+  if (RED_NEXT && fuse_on && blockIdx.x == 0 && threadIdx.x == 0) ctrl->rt_done[nxt] = 1;
+  uint32_t rows = 0, nonuni = 0;
+  uint32_t vcur = 0xFFFFFFFFu, vcnt = 0;                 // warp-uniform running (range, next digit) count
   const uint32_t nshift = pay_bits + 8 * (nxt < MAPC_MAX_PASSES ? nxt : 0);
   const unsigned long long* __restrict__ src = ctrl->sel[pass] ? bufB : bufA;
   unsigned long long* __restrict__ dst = ctrl->sel[pass] ? bufA : bufB;
@@ -189,8 +199,6 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
   const unsigned long long r0 = (unsigned long long)blockIdx.x * L;
   const unsigned long long r1 = min(r0 + L, n);
 
-  if (has_next)
-    for (uint32_t i = threadIdx.x; i < G * MAPC_RADIX; i += THREADS) tab[i] = 0;
   if (threadIdx.x < MAPC_RADIX) {
     const int d = threadIdx.x;
     const unsigned int* col = rhist + (size_t)pass * MAPC_MAX_RANGES * MAPC_RADIX + d;
@@ -291,14 +299,32 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
     }
     __syncthreads();
     load_tile(tb + TILE, k);                             // in flight during the write-out
-    if (!FUSE_NEXT && tile_n == TILE) {
+    if (tile_n == TILE) {
       // full tile: key i of the tile goes to byte address gaddr[digit] + 8 i
 #pragma unroll
       for (int u = 0; u < ITEMS; ++u) {
         const uint32_t i = u * THREADS + threadIdx.x;
         const unsigned long long key = S.keys[kslot(i)];
         const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
-        *reinterpret_cast<unsigned long long*>(S.gaddr[d] + 8ull * i) = key;
+        const unsigned long long a = S.gaddr[d] + 8ull * i;
+        *reinterpret_cast<unsigned long long*>(a) = key;
+        if (RED_NEXT && fuse_on) {
+          const uint32_t pidx = (uint32_t)((a - reinterpret_cast<unsigned long long>(dst)) >> 3);
+          const uint32_t v = (fastdiv(pidx, rdiv) << 8) | ((uint32_t)(key >> nshift) & 0xFFu);
+          const uint32_t v0 = __shfl_sync(0xffffffffu, v, 0);
+          ++rows;
+          if (__all_sync(0xffffffffu, v == v0)) {     // uniform row: into the warp's running entry
+            if (v0 != vcur) {
+              if (vcnt && lane == 0) atomicAdd(&next_tab[vcur], vcnt);
+              vcur = v0;
+              vcnt = 0;
+            }
+            vcnt += 32;
+          } else {
+            atomicAdd(&next_tab[v], 1u);
+            ++nonuni;
+          }
+        }
       }
     } else {
       for (uint32_t i = threadIdx.x; i < tile_n; i += THREADS) {
@@ -306,32 +332,30 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
         const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
         const unsigned long long p = S.gbase[d] + i;
         dst[p] = key;
-        if (has_next)
-          atomicAdd(&tab[fastdiv((uint32_t)p, rdiv) * MAPC_RADIX + ((uint32_t)(key >> nshift) & 0xFFu)], 1u);
+        if (RED_NEXT && fuse_on)
+          atomicAdd(&next_tab[(fastdiv((uint32_t)p, rdiv) << 8) | ((uint32_t)(key >> nshift) & 0xFFu)], 1u);
       }
     }
-  }
-  if (has_next) {
-    __syncthreads();
-    unsigned int* out = rhist + (size_t)nxt * MAPC_MAX_RANGES * MAPC_RADIX;
-    for (uint32_t i = threadIdx.x; i < G * MAPC_RADIX; i += THREADS) {
-      const uint32_t v = tab[i];
-      if (v) atomicAdd(&out[i], v);
+    if (RED_NEXT && fuse_on && nonuni > 8 + rows / 8) {   // mostly non-uniform rows: give the table up
+      fuse_on = false;
+      atomicOr(&ctrl->rt_bad[nxt], 1u);
     }
   }
+  if (RED_NEXT && vcnt && lane == 0) atomicAdd(&next_tab[vcur], vcnt);
 }
 
 struct RsVariant {
-  const void* fn;
+  const void* fn;          // plain pass
+  const void* fn_next;     // pass that also accumulates the next pass's range table
   int threads;
   size_t smem;
-  bool fused;
   int per_sm;
 };
 
-template <int T, int I, bool F, int B>
+template <int T, int I, int B>
 RsVariant rs_variant() {
-  return RsVariant{(const void*)k_rsweep<T, I, F, B>, T, sizeof(RsSmem<T, I>), F, B};
+  return RsVariant{(const void*)k_rsweep<T, I, false, B>, (const void*)k_rsweep<T, I, true, B>, T,
+                   sizeof(RsSmem<T, I>), B};
 }
 
 RsVariant rs_pick() {
@@ -341,14 +365,11 @@ RsVariant rs_pick() {
     v = e ? atoi(e) : 7;
   }
   // 7 (default): 256 threads x 12 keys, 4 CTAs/SM (592 ranges) -- measured best
-  //    on B200 (5.46 TB/s per pass on 5a vs 4.83 for 2: 512 x 8, 2 CTAs/SM);
-  // 1: the next pass's range table fused into the scatter (G x 256 in shared
-  //    memory, one CTA/SM) -- saves the read, loses occupancy.
-  if (v == 1) return rs_variant<512, 8, true, 1>();
-  if (v == 2) return rs_variant<512, 8, false, 2>();
-  if (v == 3) return rs_variant<512, 12, false, 2>();
-  if (v == 6) return rs_variant<256, 8, false, 4>();
-  return rs_variant<256, 12, false, 4>();
+  //    on B200 (5.46 TB/s per pass on 5a vs 4.83 for 2: 512 x 8, 2 CTAs/SM)
+  if (v == 2) return rs_variant<512, 8, 2>();
+  if (v == 3) return rs_variant<512, 12, 2>();
+  if (v == 6) return rs_variant<256, 8, 4>();
+  return rs_variant<256, 12, 4>();
 }
 
 }  // namespace mapk
@@ -370,23 +391,24 @@ extern "C" cudaError_t mapc_launch_hist_ranges(const unsigned long long* keys, M
 extern "C" cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigned long long* bufB,
                                               MapcCtrl* ctrl, unsigned int* rhist, uint32_t pass, uint32_t pay_bits,
                                               int G, cudaStream_t s) {
-  mapk::k_range_hist<<<G, mapk::RH_THREADS, 0, s>>>(bufA, bufB, ctrl, rhist, pass, pay_bits,
-                                                   mapk::rs_pick().fused ? 1u : 0u);
+  mapk::k_range_hist<<<G, mapk::RH_THREADS, 0, s>>>(bufA, bufB, ctrl, rhist, pass, pay_bits, 0u);
   return cudaGetLastError();
 }
 
-extern "C" int mapc_rsweep_fused() { return mapk::rs_pick().fused ? 1 : 0; }
+extern "C" int mapc_rsweep_fused() { return 0; }
 
 extern "C" cudaError_t mapc_launch_rsweep(unsigned long long* bufA, unsigned long long* bufB, MapcCtrl* ctrl,
-                                          unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s) {
+                                          unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, int red_next,
+                                          cudaStream_t s) {
   const mapk::RsVariant V = mapk::rs_pick();
-  const size_t smem = V.smem + (V.fused ? (size_t)G * MAPC_RADIX * 4 : 0);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaError_t e = cudaFuncSetAttribute(V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const void* fn = red_next ? V.fn_next : V.fn;
+  const size_t smem = V.smem;
+  static size_t attr[2] = {0, 0};
+  if (attr[red_next ? 1 : 0] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[red_next ? 1 : 0] = smem;
   }
   void* args[] = {&bufA, &bufB, &ctrl, &rhist, &pass, &pay_bits};
-  return cudaLaunchKernel(V.fn, dim3(G), dim3(V.threads), args, smem, s);
+  return cudaLaunchKernel(fn, dim3(G), dim3(V.threads), args, smem, s);
 }

@@ -315,3 +315,15 @@ def test_race_list_full_size_properties(name):
     assert got[0].as_tuple() == r.witness.as_tuple()
     tuples = [w.as_tuple() for w in got]
     assert tuples == sorted(tuples) and len(set(t[:4] for t in tuples)) == len(tuples)
+
+
+@pytest.mark.parametrize("detect", ["table", "sort"])
+def test_scattered_indices_two_bucket_passes(detect):
+    # 2^21 accesses over a 2^22-cell index space, scattered by the index expression:
+    # two radix passes on the bucket bits whose next-pass digits are not warp-uniform,
+    # so the scatter's range-table accumulation gives up and k_range_hist recomputes it
+    src = "params N, M; forU x in 0..N { rd[(x * 7919 + tid * 104729) % M] }; if (tid = 7) { wr[5] } else { skip }"
+    params = {"N": 2048, "M": 1 << 22}
+    r = mc.check(src, block=(1024, 1, 1), params=params, detect=detect)
+    o = oracle.check(src, block=(1024, 1, 1), params=params)
+    same(r, o)
