@@ -160,51 +160,83 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
     << "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n"
     << "    int lo = 0, hi = n_segs - 1;\n"
     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
-    << "    const Seg& sg = segs[lo];\n"
-    << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n"
-    << "    u32 cnt = 0;\n"
-    << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
-       "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
-       "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
-       "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
-       "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
-       "else { stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; } }\n"
-    << "    switch (sg.prog_begin) {\n";
-  for (const JitProgram& pg : ch.programs) {
-    s << "    case " << pg.prog_begin << "u: {\n"
-      << "#pragma unroll 1\n"
-      << "      for (int v = 0; v < " << V << "; ++v) {\n"
-      << "        const u32 t = tl0 + v * " << T << " + me;\n"
-      << "        const bool valid = t < sg.n_tuples;\n"
-      << "        u32 rem = valid ? t : 0u;\n"
-      << "        W r[" << MAPC_NREG << "];\n";
-    for (int l = (int)pg.n_levels - 1; l >= 0; --l)
-      s << "        { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
-        << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
-    s << "        const u32 qb = fdiv(rem, sg.tid_div);\n"
-      << "        const u32 tidv = rem - qb * sg.tid_div.d;\n"
-      << "        const u32 lbv = sg.lb0 + qb;\n"
-      << "        r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
-      << "        bool act = true;\n"
-      << "        u32 e = 0;\n"
-      << program_body(pg.ops, u32)
-      << "        (void)act; (void)e;\n"
-      << "      }\n"
-      << "      break; }\n";
+    ;
+  // the per-tile body, emitted once per baked segment (fields as literals) and
+  // once generic (fields loaded from segs[])
+  auto tile_body = [&](std::ostringstream& s) {
+    s << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n"
+      << "    u32 cnt = 0;\n"
+      << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
+         "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
+         "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
+         "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
+         "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
+         "else { stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; } }\n"
+      << "    switch (sg.prog_begin) {\n";
+    for (const JitProgram& pg : ch.programs) {
+      s << "    case " << pg.prog_begin << "u: {\n"
+        << "#pragma unroll 1\n"
+        << "      for (int v = 0; v < " << V << "; ++v) {\n"
+        << "        const u32 t = tl0 + v * " << T << " + me;\n"
+        << "        const bool valid = t < sg.n_tuples;\n"
+        << "        u32 rem = valid ? t : 0u;\n"
+        << "        W r[" << MAPC_NREG << "];\n";
+      for (int l = (int)pg.n_levels - 1; l >= 0; --l)
+        s << "        { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
+          << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
+      s << "        const u32 qb = fdiv(rem, sg.tid_div);\n"
+        << "        const u32 tidv = rem - qb * sg.tid_div.d;\n"
+        << "        const u32 lbv = sg.lb0 + qb;\n"
+        << "        r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
+        << "        bool act = true;\n"
+        << "        u32 e = 0;\n"
+        << program_body(pg.ops, u32)
+        << "        (void)act; (void)e;\n"
+        << "      }\n"
+        << "      break; }\n";
+    }
+    s << "    default: break;\n"
+      << "    }\n"
+      << "#undef EMIT_KEY\n"
+      << "    if (!sg.dense) {\n"
+      << "      u32 total;\n"
+      << "      const u32 excl = block_excl_scan<" << T << ">(cnt, scan_tmp, &total);\n"
+      << "      if (me == 0) s_base = total ? atomicAdd(n_ctr, (u64)total) : 0ull;\n"
+      << "      __syncthreads();\n"
+      << "      const u64 obase = s_base;\n"
+      << "      for (u32 j = 0; j < cnt; ++j) { const u64 pos = obase + excl + j; "
+         "if (pos < cap) keys[pos] = stage[(size_t)j * " << T << " + me]; else err |= " << MAPC_ERR_CAPACITY << "u; }\n"
+      << "      __syncthreads();\n"
+      << "    }\n";
+  };
+  auto fd = [](const MapcFastDiv& f) {
+    std::ostringstream o;
+    o << "{" << f.d << "u, " << f.m << "u, " << f.s << "u, " << f.pow2 << "u}";
+    return o.str();
+  };
+  if (!ch.segs.empty()) {
+    s << "    switch (lo) {\n";
+    for (size_t i = 0; i < ch.segs.size(); ++i) {
+      const MapcSeg& g = ch.segs[i];
+      s << "    case " << i << ": {\n"
+        << "    const Seg sg = {" << g.tuple_begin << "ull, " << g.n_tuples << "ull, " << g.tile_begin << "ull, "
+        << g.key_begin << "ull, " << g.key_hi << "ull, " << g.prog_begin << "u, " << g.prog_end << "u, " << g.n_levels
+        << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, 0u, {";
+      for (int l = 0; l < 8; ++l) s << (l ? ", " : "") << fd(g.trip_div[l]);
+      s << "}, " << fd(g.tid_div) << "};\n";
+      tile_body(s);
+      s << "    break; }\n";
+    }
+    s << "    default: {\n"
+      << "    const Seg& sg = segs[lo];\n";
+    tile_body(s);
+    s << "    break; }\n"
+      << "    }\n";
+  } else {
+    s << "    const Seg& sg = segs[lo];\n";
+    tile_body(s);
   }
-  s << "    default: break;\n"
-    << "    }\n"
-    << "#undef EMIT_KEY\n"
-    << "    if (!sg.dense) {\n"
-    << "      u32 total;\n"
-    << "      const u32 excl = block_excl_scan<" << T << ">(cnt, scan_tmp, &total);\n"
-    << "      if (me == 0) s_base = total ? atomicAdd(n_ctr, (u64)total) : 0ull;\n"
-    << "      __syncthreads();\n"
-    << "      const u64 obase = s_base;\n"
-    << "      for (u32 j = 0; j < cnt; ++j) { const u64 pos = obase + excl + j; "
-       "if (pos < cap) keys[pos] = stage[(size_t)j * " << T << " + me]; else err |= " << MAPC_ERR_CAPACITY << "u; }\n"
-    << "      __syncthreads();\n"
-    << "    }\n"
+  s
     << "  }\n"
     << "  if (err) atomicOr(err_flag, err);\n"
     << "}\n";

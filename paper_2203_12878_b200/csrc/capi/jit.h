@@ -19,6 +19,7 @@ struct JitChunk {
   MapcLayout lay;
   uint32_t max_emits;
   std::vector<JitProgram> programs;
+  std::vector<MapcSeg> segs;      // baked as literals when few (tuple decode and slots fold to constants)
 };
 
 struct JitHandle {

@@ -316,6 +316,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.lay.cap = kcap;
     ch.jit.lay = ch.lay;
     ch.jit.max_emits = ch.max_emits;
+    if (ch.segs.size() <= 4) ch.jit.segs = ch.segs;
   }
   out.cap = kcap;
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
