@@ -704,9 +704,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     r.racy_segments += cr.racy;
     err |= cr.err;
     st_acc.bytes[MAP_K_GENERATE] += 8 * cr.n;
-    // one histogram read per active pass (k_hist_ranges, then k_range_hist for each later pass)
-    if (effective_layout(P.chunks[c], ex->flags).n_passes)
-      st_acc.bytes[MAP_K_HIST] += 8 * cr.n * std::max<uint32_t>(1, cr.active_passes);
+    // the histogram reads that ran: k_hist_ranges, and k_range_hist per later pass
+    // whose table the previous scatter did not accumulate
+    st_acc.bytes[MAP_K_HIST] += 8 * cr.n * cr.table_reads;
     st_acc.bytes[MAP_K_ONESWEEP] += 16ull * cr.n * cr.active_passes;
     st_acc.bytes[MAP_K_DETECT] += 8 * cr.n;
     if (cr.witness != ~0ull) {

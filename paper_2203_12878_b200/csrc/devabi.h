@@ -143,6 +143,8 @@ struct MapcChunkResult {
   unsigned long long racy;
   unsigned int err;
   unsigned int active_passes;      // radix passes that were not skipped
+  unsigned int table_reads;        // range-table reads of the keys (k_hist_ranges + k_range_hist that ran)
+  unsigned int pad;
 };
 
 #define MAPC_ERR_DIV0 1u        // division/modulo by zero on a reached path
