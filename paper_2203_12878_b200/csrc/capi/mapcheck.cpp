@@ -60,6 +60,7 @@ cudaError_t mapc_launch_range_hist(const unsigned long long* bufA, const unsigne
                                    unsigned int* rhist, uint32_t pass, uint32_t pay_bits, int G, cudaStream_t s);
 int mapc_rsweep_fused();
 int mapc_table_ctas(int n_sms);
+unsigned long long mapc_table_tile();
 cudaError_t mapc_launch_list_racy(const unsigned long long* bufA, const unsigned long long* bufB, const MapcCtrl* ctrl,
                                   uint32_t n_passes, uint32_t pay_bits, uint32_t w_tid, unsigned long long* counts,
                                   unsigned int max_warps, unsigned long long* out, unsigned long long cap,
@@ -335,7 +336,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
   out.off_rh = off; off += align_up(out.rh_bytes);
   out.off_xch = off; off += align_up(2 * 64 * sizeof(unsigned long long));   // exchange counts + cursors
-  out.table_ctas = (uint32_t)std::min<uint64_t>(MAPC_TABLE_MAX_CTAS, (kcap + 4095) / 4096);
+  out.table_ctas = (uint32_t)std::min<uint64_t>(MAPC_TABLE_MAX_CTAS, (kcap + mapc_table_tile() - 1) / mapc_table_tile());
   out.off_tparts = off; off += align_up((size_t)2 * out.table_ctas * sizeof(MapcTablePart));
   out.off_tstore = off; off += align_up((size_t)2 * out.table_ctas * MAPC_TABLE_WORDS * 4);
   out.total = off;

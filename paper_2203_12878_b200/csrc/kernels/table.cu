@@ -288,6 +288,8 @@ k_table_merge(MapcCtrl* __restrict__ ctrl, const MapcTablePart* __restrict__ par
 
 extern "C" uint32_t mapc_table_bits_max() { return mapk::TB_MAX; }
 
+extern "C" unsigned long long mapc_table_tile() { return mapk::TB_TILE; }
+
 extern "C" int mapc_table_ctas(int n_sms) {
   const int g = n_sms * 3;
   return g < MAPC_TABLE_MAX_CTAS ? g : MAPC_TABLE_MAX_CTAS;
