@@ -255,9 +255,15 @@ def main():
             d["bytes"] += v["bytes"]
     launches = sum(r.gpu_launches for r in results)
     peak, peak_kind = measured_peak()
-    os_k = kern.get("onesweep", {"ms": 0, "bytes": 0, "launches": 0})
-    active_launches = max(1, os_k["launches"])
+    # the dominant kernel: the radix pass (k_rsweep), both launch forms together --
+    # plain passes and passes that also build the next pass's range table
+    z = {"ms": 0, "bytes": 0, "launches": 0}
+    os_plain, os_next = kern.get("onesweep", z), kern.get("onesweep_next", z)
+    os_k = {f: os_plain[f] + os_next[f] for f in ("ms", "bytes", "launches")}
     achieved = (os_k["bytes"] / (os_k["ms"] / 1e3) / 1e9) if os_k["ms"] > 0 else 0.0
+    gbs = lambda d: (d["bytes"] / (d["ms"] / 1e3) / 1e9) if d["ms"] > 0 else None
+    radix_parts = {"plain_pass_GB_s": gbs(os_plain), "next_table_pass_GB_s": gbs(os_next),
+                   "plain_launches": os_plain["launches"], "next_table_launches": os_next["launches"]}
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
     kernels_out = {k: {"ms_per_step": v["ms"] / len(results), "share": v["ms"] / kern_total,
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,
@@ -333,7 +339,8 @@ def main():
                          "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if peak else None,
                          "traffic": ncu_traffic(),
-                         "bytes_model": "16 B per key per active pass (8 read + 8 write)"},
+                         "bytes_model": "16 B per key per active pass (8 read + 8 write)",
+                         "parts": radix_parts},
             "kernels": kernels_out,
             "detect_path": args.detect if args.detect != "auto" else "auto (table for dense chunks)",
             "detect_paths": alt,

@@ -81,7 +81,8 @@ enum {
   MAP_K_ONESWEEP = 3,
   MAP_K_DETECT = 4,
   MAP_K_OTHER = 5,
-  MAP_K_COUNT = 6
+  MAP_K_SORT_NEXT = 6,      /* radix passes that also build the next pass's range table */
+  MAP_K_COUNT = 7
 };
 typedef struct {
   float ms[MAP_K_COUNT];

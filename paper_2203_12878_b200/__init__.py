@@ -47,11 +47,11 @@ class _Instance(ctypes.Structure):
                 ("param_names", ctypes.POINTER(ctypes.c_char_p)), ("param_values", ctypes.POINTER(ctypes.c_uint64))]
 
 
-KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other")   # MAP_K_* order
+KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other", "onesweep_next")   # MAP_K_* order
 
 
 class _Stats(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_float * 6), ("launches", ctypes.c_uint32 * 6), ("bytes", ctypes.c_uint64 * 6)]
+    _fields_ = [("ms", ctypes.c_float * 7), ("launches", ctypes.c_uint32 * 7), ("bytes", ctypes.c_uint64 * 7)]
 
 
 class _Exec(ctypes.Structure):

@@ -649,7 +649,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
           CK(mapc_launch_range_hist(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, s));
           end(m);
         }
-        m = begin(MAP_K_ONESWEEP);
+        m = begin(red_next(L) && pass + 1 < L.n_passes ? MAP_K_SORT_NEXT : MAP_K_ONESWEEP);
         CK(mapc_launch_rsweep(bufA, bufB, ctrl, rhist, pass, L.sort_lo, G, red_next(L), s));
         end(m);
       }
@@ -708,7 +708,15 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     // the histogram reads that ran: k_hist_ranges, and k_range_hist per later pass
     // whose table the previous scatter did not accumulate
     st_acc.bytes[MAP_K_HIST] += 8 * cr.n * cr.table_reads;
-    st_acc.bytes[MAP_K_ONESWEEP] += 16ull * cr.n * cr.active_passes;
+    // a pass builds the next pass's range table only when a later pass is active
+    {
+      const MapcLayout Lc = effective_layout(P.chunks[c], ex->flags);
+      for (uint32_t q = 0; q < Lc.n_passes; ++q) {
+        if (!((cr.active_mask >> q) & 1u)) continue;
+        const bool later = (cr.active_mask >> (q + 1)) != 0;
+        st_acc.bytes[red_next(Lc) && later ? MAP_K_SORT_NEXT : MAP_K_ONESWEEP] += 16ull * cr.n;
+      }
+    }
     st_acc.bytes[MAP_K_DETECT] += 8 * cr.n;
     if (cr.witness != ~0ull) {
       map_witness w{};

@@ -144,7 +144,7 @@ struct MapcChunkResult {
   unsigned int err;
   unsigned int active_passes;      // radix passes that were not skipped
   unsigned int table_reads;        // range-table reads of the keys (k_hist_ranges + k_range_hist that ran)
-  unsigned int pad;
+  unsigned int active_mask;        // bit p: radix pass p ran
 };
 
 #define MAPC_ERR_DIV0 1u        // division/modulo by zero on a reached path

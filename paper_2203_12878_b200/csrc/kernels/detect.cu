@@ -471,15 +471,16 @@ __global__ void k_chunk_finish(const MapcCtrl* __restrict__ ctrl, uint32_t n_pas
   r.err = ctrl->err;
   r.active_passes = 0;
   r.table_reads = 0;
+  r.active_mask = 0;
   for (uint32_t p = 0; p < n_passes; ++p) {
     if (!ctrl->active[p]) continue;
     r.active_passes += 1;
+    r.active_mask |= 1u << p;
     // the first active pass's table comes from k_hist_ranges' read; a later one from
     // k_range_hist's, unless the previous scatter accumulated it
     if (p == ctrl->first_active || !(ctrl->rt_done[p] && !ctrl->rt_bad[p])) r.table_reads += 1;
   }
   if (n_passes && !r.active_passes) r.table_reads = 1;   // the histogram read found every pass single-bin
-  r.pad = 0;
   *out = r;
 }
 
