@@ -18,7 +18,7 @@
 #define MAPC_MAX_PASSES 8        // 64-bit keys / 8-bit digits
 #define MAPC_RADIX_BITS 8
 #define MAPC_RADIX 256
-#define MAPC_MAX_RANGES 640          // static key ranges per radix pass (>= 2 x SM count)
+#define MAPC_MAX_RANGES 768          // static key ranges per radix pass (>= 2 x SM count)
 
 // Fixed registers: r0 = tid, r1 = bid (global block id), r2.. = k_0..k_{L-1}.
 #define MAPC_REG_TID 0
