@@ -6,10 +6,13 @@ synthetic 3-deep loop stencil MAP of SURVEY.md §8d, 2^34 accesses
 (blockDim 1024, T=16 barrier phases, R=256 rows/thread, C=1024 columns,
 ping-pong buffers -> DRF), checked exhaustively: one step = generate + radix
 sort + detect over every access of every phase (all of §8 rows a1-a3).
-The detect path is the library's automatic choice (for 5a: LSD passes on the
-bucket bits sf >> 13, then the shared-memory bucket tables, SURVEY.md §8f
-NEXT-3); `--detect sort` forces the full LSD sort + segmented scan, and the
-line also reports that path's throughput on the same run ("detect_paths").
+The detect path is the library's automatic choice (for 5a: the sort-free
+direct-address table, SURVEY.md §8f NEXT-3 -- every access folded into its
+cell with one atomic OR, the table scanned once); `--detect table|sort` forces
+the bucket-table path (partial LSD sort + shared-memory tables) or the full LSD
+sort + segmented scan (the north_star's generate -> sort -> detect), and the
+line also reports both of those paths' throughput on the same run
+("detect_paths") and the radix pass's roofline ("roofline_sort_path").
 
 Contract: `python bench.py --gpus N --steps K --warmup W` (torchrun for N>1,
 one rank per GPU; chunks are dealt round-robin to ranks, strong scaling on the
@@ -48,8 +51,8 @@ def parse_args():
                     help="R of the oracle's bounded sample per step of --impl reference (K+W steps must fit minutes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--detect", choices=["auto", "sort", "table"], default="auto")
-    ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect path")
+    ap.add_argument("--detect", choices=["auto", "direct", "sort", "table"], default="auto")
+    ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect paths")
     return ap.parse_args()
 
 
@@ -173,14 +176,58 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_rsweep_traffic.json")
+def ncu_traffic(which):
+    """dram bytes per launch of a kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{which}_traffic.json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+# Roofline models of the kernels that can dominate a step (all HBM-bound; the
+# library reports their algorithmic bytes per launch, DESIGN.md §5.7).
+ROOFLINE_MODELS = {
+    "direct": ("generate fused with the direct-address table reductions (gen_0, mode direct)", "direct",
+               "2 x table bytes per launch: every cell of the 2^S-cell table read and written once "
+               "(the per-access red.or are served by L2)"),
+    "onesweep": ("k_rsweep (static-range LSD radix pass)", "rsweep", "16 B per key per active pass (8 read + 8 write)"),
+}
+
+
+def kernel_roofline(kern, cls, peak, peak_kind):
+    """achieved = the class's algorithmic bytes / its CUDA-event time; for the radix
+    pass both launch forms (plain, and building the next pass's range table) together."""
+    z = {"ms": 0, "bytes": 0, "launches": 0}
+    parts = None
+    if cls == "onesweep":
+        a, b = kern.get("onesweep", z), kern.get("onesweep_next", z)
+        k = {f: a[f] + b[f] for f in ("ms", "bytes", "launches")}
+        gbs = lambda d: (d["bytes"] / (d["ms"] / 1e3) / 1e9) if d["ms"] > 0 else None
+        parts = {"plain_pass_GB_s": gbs(a), "next_table_pass_GB_s": gbs(b), "plain_launches": a["launches"],
+                 "next_table_launches": b["launches"]}
+    else:
+        k = kern.get(cls, z)
+    achieved = (k["bytes"] / (k["ms"] / 1e3) / 1e9) if k["ms"] > 0 else 0.0
+    name, tag, model = ROOFLINE_MODELS[cls]
+    out = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+           "unit": "GB/s", "frac": achieved / peak if peak else None, "traffic": ncu_traffic(tag),
+           "bytes_model": model, "launches": k["launches"]}
+    if parts:
+        out["parts"] = parts
+    return out
+
+
+def kernel_table(results):
+    kern = {}
+    for r in results:
+        for k, v in (r.kernels or {}).items():
+            d = kern.setdefault(k, {"ms": 0.0, "launches": 0, "bytes": 0})
+            d["ms"] += v["ms"]
+            d["launches"] += v["launches"]
+            d["bytes"] += v["bytes"]
+    return kern
 
 
 def main():
@@ -246,25 +293,15 @@ def main():
     value = total_acc / (ms_max / 1e3) / 1e9
 
     # per-kernel-class device time (this rank) over the timed steps
-    kern = {}
-    for r in results:
-        for k, v in (r.kernels or {}).items():
-            d = kern.setdefault(k, {"ms": 0.0, "launches": 0, "bytes": 0})
-            d["ms"] += v["ms"]
-            d["launches"] += v["launches"]
-            d["bytes"] += v["bytes"]
+    kern = kernel_table(results)
     launches = sum(r.gpu_launches for r in results)
     peak, peak_kind = measured_peak()
-    # the dominant kernel: the radix pass (k_rsweep), both launch forms together --
-    # plain passes and passes that also build the next pass's range table
-    z = {"ms": 0, "bytes": 0, "launches": 0}
-    os_plain, os_next = kern.get("onesweep", z), kern.get("onesweep_next", z)
-    os_k = {f: os_plain[f] + os_next[f] for f in ("ms", "bytes", "launches")}
-    achieved = (os_k["bytes"] / (os_k["ms"] / 1e3) / 1e9) if os_k["ms"] > 0 else 0.0
-    gbs = lambda d: (d["bytes"] / (d["ms"] / 1e3) / 1e9) if d["ms"] > 0 else None
-    radix_parts = {"plain_pass_GB_s": gbs(os_plain), "next_table_pass_GB_s": gbs(os_next),
-                   "plain_launches": os_plain["launches"], "next_table_launches": os_next["launches"]}
+    # the dominant kernel of the path that ran: the fused direct generate, or the radix pass
+    ms_of = lambda c: kern.get(c, {}).get("ms", 0) + (kern.get("onesweep_next", {}).get("ms", 0) if c == "onesweep" else 0)
+    dominant = max(ROOFLINE_MODELS, key=ms_of)
+    roofline = kernel_roofline(kern, dominant, peak, peak_kind)
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
+    pipe_bytes = sum(v["bytes"] for v in kern.values())
     kernels_out = {k: {"ms_per_step": v["ms"] / len(results), "share": v["ms"] / kern_total,
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,
                        "launches_per_step": v["launches"] / len(results)} for k, v in kern.items()}
@@ -294,27 +331,33 @@ def main():
                "h2d_bytes_per_step": results[0].h2d_bytes, "d2h_bytes_per_step": results[0].d2h_bytes,
                "includes": "map_compile from MAP text + map_check_races (bytecode/segment H2D, result D2H)"}
 
-    # the other detect path on the same workload, for context (same timing rules)
-    alt = None
+    # the other detect paths on the same workload, for context (same timing rules):
+    # the bucket-table path and the full sort (the north_star's generate -> sort -> detect)
+    alt, roof_sort = None, None
     if not args.no_alt_path:
-        alt_mode = "sort" if args.detect != "sort" else "table"
-        step(detect=alt_mode)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        a_res = [step(detect=alt_mode) for _ in range(args.steps)]
-        a1.record(stream)
-        torch.cuda.synchronize()
-        ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
-        same = all((x.verdict, x.witness, x.n_accesses, x.racy_segments) ==
-                   (results[0].verdict, results[0].witness, results[0].n_accesses, results[0].racy_segments)
-                   for x in a_res)
-        alt = {alt_mode: sum(x.n_accesses for x in a_res) / (float(ta.item()) / 1e3) / 1e9,
-               "identical_result": same}
+        alt = {"identical_result": True}
+        for alt_mode in [m for m in ("table", "sort") if m != args.detect]:
+            step(detect=alt_mode)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            a_res = [step(profile=True, detect=alt_mode) for _ in range(args.steps)]
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+            same = all((x.verdict, x.witness, x.n_accesses, x.racy_segments) ==
+                       (results[0].verdict, results[0].witness, results[0].n_accesses, results[0].racy_segments)
+                       for x in a_res)
+            alt[alt_mode] = sum(x.n_accesses for x in a_res) / (float(ta.item()) / 1e3) / 1e9
+            alt["identical_result"] = alt["identical_result"] and same
+            if alt_mode == "table":
+                k_alt = kernel_table(a_res)
+                roof_sort = kernel_roofline(k_alt, "onesweep", peak, peak_kind)
+                roof_sort["path"] = "table (partial LSD sort + bucket tables)"
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -332,19 +375,19 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": workload_desc(inst), "n_accesses": r0.n_accesses, "chunks": n_chunks,
                        "chunk_max_accesses": args.chunk or "default (2^30)", "parallelism": f"chunks dealt over {world} GPU(s)",
-                       "l2": "inputs larger than L2: 8 GiB of keys per chunk vs 126 MB L2",
+                       "l2": "inputs larger than L2: a 2 GiB direct-address table (or 8 GiB of keys) per chunk "
+                             "vs 126 MB L2; no flush needed",
                        "verdict": "racy" if r0.verdict else "drf",
                        "witness": list(r0.witness.as_tuple()) if r0.witness else None},
-            "roofline": {"bound": "hbm", "kernel": "k_rsweep (static-range LSD radix pass)", "achieved": achieved,
-                         "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak if peak else None,
-                         "traffic": ncu_traffic(),
-                         "bytes_model": "16 B per key per active pass (8 read + 8 write)",
-                         "parts": radix_parts},
+            "roofline": roofline,
+            "roofline_sort_path": roof_sort,
             "kernels": kernels_out,
-            "detect_path": args.detect if args.detect != "auto" else "auto (table for dense chunks)",
+            "detect_path": args.detect if args.detect != "auto" else "auto (direct-address table for dense chunks)",
             "detect_paths": alt,
-            "pipeline_bytes_per_access": sum(v["bytes"] for v in kern.values()) / max(1, total_acc),
+            "pipeline_bytes_per_access": pipe_bytes / max(1, total_acc),
+            "pipeline_hbm": {"achieved": pipe_bytes / (kern_total / 1e3) / 1e9, "peak": peak,
+                             "frac": pipe_bytes / (kern_total / 1e3) / 1e9 / peak if peak else None,
+                             "note": "algorithmic bytes of every kernel of the step / their summed device time"},
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -73,7 +73,11 @@ typedef struct {
  * map_exec.stats == NULL disables them).  bytes = ALGORITHMIC bytes the
  * launches had to move: generate writes 8 B per key, the
  * histogram reads 8 B per key, an active radix pass reads + writes 8 B per
- * key, detect reads 8 B per key. */
+ * key, detect reads 8 B per key.  Direct-address detect (table of 2^S cells
+ * of 4 or 8 B, larger than L2 at the bench sizes): the fused generate
+ * (MAP_K_DIRECT) reads and writes every cell once (its per-access reductions
+ * are served by L2), the clear (MAP_K_CLEAR) writes and the scan
+ * (MAP_K_DETECT) reads every cell once. */
 enum {
   MAP_K_GENERATE = 0,
   MAP_K_HIST = 1,
@@ -82,7 +86,9 @@ enum {
   MAP_K_DETECT = 4,
   MAP_K_OTHER = 5,
   MAP_K_SORT_NEXT = 6,      /* radix passes that also build the next pass's range table */
-  MAP_K_COUNT = 7
+  MAP_K_DIRECT = 7,         /* generate fused with the direct-address table reductions  */
+  MAP_K_CLEAR = 8,          /* direct-address table clear                               */
+  MAP_K_COUNT = 9
 };
 typedef struct {
   float ms[MAP_K_COUNT];
@@ -118,12 +124,26 @@ typedef struct {
  *                     direct-address table in shared memory (min tid, max tid,
  *                     write bit per cell).  Same verdict,
  *                     witness, access count and racy-segment count.
- *   MAP_DETECT_AUTO:  TABLE when the chunk holds >= 2^16 keys and at least
- *                     2^(S-1) of them (dense sort-field space), else SORT. */
+ *   MAP_DETECT_DIRECT: no keys and no sort: every access is folded into its
+ *                     cell of a 2^S-cell direct-address table in device
+ *                     memory with one atomic OR of tid | ~tid << wt |
+ *                     kind << 2wt (racy <=> write bit and two distinct tids
+ *                     <=> (OR tid) & (OR ~tid) != 0), the table is scanned
+ *                     once, and the witness cell's keys are re-generated and
+ *                     folded (sort-free).  Used for a
+ *                     chunk when its table is small against its accesses
+ *                     (2^S <= 8 x its key bound, or <= 1 MiB) and fits the
+ *                     scratch plan; other chunks take the AUTO choice below.
+ *   MAP_DETECT_AUTO:  DIRECT where it qualifies; otherwise TABLE when the
+ *                     chunk holds >= 2^16 keys and at least 2^(S-1) of them
+ *                     (dense sort-field space), else SORT.
+ * All paths give the same verdict, witness, access count and racy-segment
+ * count. */
 #define MAP_DETECT_AUTO 0u
 #define MAP_DETECT_SORT 0x10u
 #define MAP_DETECT_TABLE 0x20u
-#define MAP_DETECT_MASK 0x30u
+#define MAP_DETECT_DIRECT 0x40u
+#define MAP_DETECT_MASK 0x70u
 
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */

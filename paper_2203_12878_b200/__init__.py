@@ -47,11 +47,13 @@ class _Instance(ctypes.Structure):
                 ("param_names", ctypes.POINTER(ctypes.c_char_p)), ("param_values", ctypes.POINTER(ctypes.c_uint64))]
 
 
-KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other", "onesweep_next")   # MAP_K_* order
+KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other", "onesweep_next",
+                  "direct", "clear")   # MAP_K_* order
+_NK = len(KERNEL_CLASSES)
 
 
 class _Stats(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_float * 7), ("launches", ctypes.c_uint32 * 7), ("bytes", ctypes.c_uint64 * 7)]
+    _fields_ = [("ms", ctypes.c_float * _NK), ("launches", ctypes.c_uint32 * _NK), ("bytes", ctypes.c_uint64 * _NK)]
 
 
 class _Exec(ctypes.Structure):
@@ -61,7 +63,7 @@ class _Exec(ctypes.Structure):
                 ("flags", ctypes.c_uint32)]
 
 GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
-DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20}   # MAP_DETECT_* (include/mapcheck.h)
+DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40}   # MAP_DETECT_* (include/mapcheck.h)
 
 
 class _Result(ctypes.Structure):

@@ -20,6 +20,7 @@ SOURCES = [
     "kernels/exchange.cu",
     "kernels/table.cu",
     "kernels/listing.cu",
+    "kernels/direct.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "kernels/segstate.cuh",
            "capi/jit.h"]

@@ -140,23 +140,54 @@ struct Module {
 std::mutex g_mu;
 std::map<std::string, Module> g_cache;   // source text -> loaded module (process-wide)
 
+// The tail of EMIT_KEY per generate mode (variables in scope: sf_, tidv, KIND,
+// sg, e, t, cnt, stage, keys, me).
+std::string emit_tail(uint32_t mode, uint32_t w_tid, int T) {
+  std::ostringstream s;
+  if (mode == MAPC_MODE_DIRECT) {
+    // cell |= tid | (~tid & M) << wt | kind << 2wt  (direct.cu); fire-and-forget red.or
+    s << "const u64 code_ = (u64)tidv | ((~(u64)tidv & TMASK) << " << w_tid << "u) | ((u64)(KIND) << " << 2 * w_tid
+      << "u); atomicOr(reinterpret_cast<CELL*>(keys) + sf_, (CELL)code_); if (!sg.dense) ++cnt;";
+  } else if (mode == MAPC_MODE_FILTER) {
+    s << "if (sf_ == target) { const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
+         "stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; }";
+  } else {
+    s << "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
+         "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
+         "else { stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; }";
+  }
+  return s.str();
+}
+
 }  // namespace
 
-std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
+std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes) {
   static_assert(sizeof(MapcSeg) == 5 * 8 + 8 * 4 + 9 * 16, "Seg layout mirrored in the JIT prelude");
   std::ostringstream s;
   const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
+  // keys staged per thread per tile for compaction: the guarded segments' emits
+  // (keys mode), every segment's (filter mode), none (direct mode)
+  const uint32_t stage_emits = V * (mode == MAPC_MODE_DIRECT   ? 1u
+                                    : mode == MAPC_MODE_FILTER ? (uint32_t)MAPC_MAX_EMITS
+                                                               : std::max(1u, ch.max_emits));
   s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
-       "u64 cap) {\n"
+       "u64 cap, const u64* target_ptr) {\n"
     << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
+    << "  typedef " << (cell_bytes == 4 ? "u32" : "u64") << " CELL;\n"
     << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
     << "  const u64 IDX_LO = " << ch.lay.idx_lo << "ull;\n"
-    << "  __shared__ u64 stage[" << (ch.max_emits ? ch.max_emits : 1) * V << " * " << T << "];\n"
+    << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
     << "  __shared__ u64 s_base;\n"
     << "  const int me = threadIdx.x;\n"
     << "  u32 err = 0;\n"
+    << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
+    << "  (void)TMASK; (void)target_ptr;\n";
+  if (mode == MAPC_MODE_FILTER)
+    s << "  const u64 target = *target_ptr;\n"
+      << "  if (target == ~0ull) return;\n";
+  s
     << "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n"
     << "    int lo = 0, hi = n_segs - 1;\n"
     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
@@ -169,9 +200,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
       << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
          "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
          "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
-         "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
-         "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
-         "else { stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; } }\n"
+         << emit_tail(mode, ch.lay.w_tid, T) << " }\n"
       << "    switch (sg.prog_begin) {\n";
     for (const JitProgram& pg : ch.programs) {
       s << "    case " << pg.prog_begin << "u: {\n"
@@ -197,8 +226,15 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
     }
     s << "    default: break;\n"
       << "    }\n"
-      << "#undef EMIT_KEY\n"
-      << "    if (!sg.dense) {\n"
+      << "#undef EMIT_KEY\n";
+    if (mode == MAPC_MODE_DIRECT) {
+      s << "    if (!sg.dense) {\n"
+        << "      const u32 wsum_ = __reduce_add_sync(0xffffffffu, cnt);\n"
+        << "      if ((me & 31) == 0 && wsum_) atomicAdd(n_ctr, (u64)wsum_);\n"
+        << "    }\n";
+      return;
+    }
+    s << "    if (" << (mode == MAPC_MODE_FILTER ? "true" : "!sg.dense") << ") {\n"
       << "      u32 total;\n"
       << "      const u32 excl = block_excl_scan<" << T << ">(cnt, scan_tmp, &total);\n"
       << "      if (me == 0) s_base = total ? atomicAdd(n_ctr, (u64)total) : 0ull;\n"
@@ -243,9 +279,9 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32) {
   return s.str();
 }
 
-std::string module_source(const std::vector<JitChunk>& chunks, bool u32) {
+std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, uint32_t cell_bytes) {
   std::string src = kPrelude;
-  for (size_t i = 0; i < chunks.size(); ++i) src += chunk_kernel_source(chunks[i], (int)i, u32);
+  for (size_t i = 0; i < chunks.size(); ++i) src += chunk_kernel_source(chunks[i], (int)i, u32, mode, cell_bytes);
   return src;
 }
 
@@ -275,10 +311,12 @@ int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string*
 }
 
 // One NVRTC program per chunk, compiled in parallel; modules cached by source.
-int build_module(const std::vector<JitChunk>& chunks, bool u32, JitHandle* out, std::string* log) {
+int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
+                 JitHandle* out, std::string* log) {
   const size_t nc = chunks.size();
   std::vector<std::string> srcs(nc);
-  for (size_t i = 0; i < nc; ++i) srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32);
+  for (size_t i = 0; i < nc; ++i)
+    srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
   std::vector<int> need;
   {
     std::lock_guard<std::mutex> g(g_mu);
@@ -332,7 +370,8 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, JitHandle* out, 
 
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
-                         unsigned int* err_flag, unsigned long long cap, int n_sms, cudaStream_t s) {
+                         unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
+                         int n_sms, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
   int occ = 1;
@@ -341,7 +380,7 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
   const unsigned long long capb = (unsigned long long)n_sms * occ;
   const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
-                  (void*)&cap};
+                  (void*)&cap, (void*)&target};
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 

@@ -26,13 +26,18 @@ struct JitHandle {
   std::vector<cudaKernel_t> kernels;   // one per chunk
 };
 
-std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32);
-std::string module_source(const std::vector<JitChunk>& chunks, bool u32);
+// mode: MAPC_MODE_KEYS (keys -> key buffer), MAPC_MODE_DIRECT (red.or into the
+// direct-address table passed as `keys`, cells of cell_bytes), MAPC_MODE_FILTER
+// (only keys with sort field *target, compacted; n_ctr counts them).
+std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes);
+std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, uint32_t cell_bytes);
 int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log);
-// Compile (or fetch from the process-wide cache) one module with a kernel per chunk.
-int build_module(const std::vector<JitChunk>& chunks, bool u32, JitHandle* out, std::string* log);
+// Compile (or fetch from the process-wide cache) one kernel per chunk for one mode.
+int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
+                 JitHandle* out, std::string* log);
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
-                         unsigned int* err_flag, unsigned long long cap, int n_sms, cudaStream_t s);
+                         unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
+                         int n_sms, cudaStream_t s);
 
 }  // namespace mapj

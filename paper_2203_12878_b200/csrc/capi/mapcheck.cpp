@@ -32,7 +32,14 @@ cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cudaStream_t s
 cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long tile_lo,
                                  unsigned long long tile_hi, const MapcLayout* lay, int u32_mode,
                                  unsigned long long* keys, MapcCtrl* ctrl, int n_sms, uint32_t nreg,
-                                 uint32_t max_emits, uint32_t force_compact, cudaStream_t s);
+                                 uint32_t max_emits, uint32_t force_compact, uint32_t mode, void* tab,
+                                 uint32_t cell_bytes, cudaStream_t s);
+cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
+                                    MapcCtrl* ctrl, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
+cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t w_tid,
+                                     unsigned long long cap, cudaStream_t s);
 int mapc_bucket_max_world();
 cudaError_t mapc_launch_bucket_count(const unsigned long long* keys, const MapcCtrl* ctrl, uint32_t pay_bits,
                                      uint32_t world, unsigned long long* counts, int n_sms, cudaStream_t s);
@@ -94,13 +101,19 @@ struct Chunk {
   uint32_t max_emits = 0;                   // largest n_emits of a non-dense segment
   size_t stage_ops = 0, stage_segs = 0;     // offsets in the pinned staging buffer
   mapj::JitChunk jit;                       // straight-line programs for the specialised generate
+  // sort-free direct-address detect (direct.cu): one cell per sort-field value
+  uint64_t cells = 0;                       // 2^S
+  uint32_t cell_bytes = 4;                  // 4 if 2 w_tid + 1 <= 32, else 8
+  bool direct_ok = false;                   // the table is cheap enough and fits the scratch plan
 };
 
 struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
-  bool jit_ready = false;
-  mapj::JitHandle jit;
+  bool jit_ready[3] = {false, false, false};   // per generate mode (MAPC_MODE_*)
+  mapj::JitHandle jit[3];
+  size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
+  size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
   size_t max_segs = 0;
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
@@ -313,11 +326,27 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.stage_segs = stage;
     stage += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg), 64);
   }
+  size_t dtab = 0;
   for (auto& ch : out.chunks) {
     ch.lay.cap = kcap;
     ch.jit.lay = ch.lay;
     ch.jit.max_emits = ch.max_emits;
     if (ch.segs.size() <= 4) ch.jit.segs = ch.segs;
+    // direct-address table: 2^S cells.  Worth it when the scan of the table
+    // (8 B of HBM per u32 cell: clear + read) is small against the keys
+    // pipeline it replaces (>= 56 B per access): 2^S <= 8 * bound, or the
+    // table is tiny.  Its size is bounded by key buffer B (which it overlays)
+    // or 1 GiB.
+    const uint32_t S = ch.lay.sort_bits;
+    ch.cell_bytes = 2 * ch.lay.w_tid + 1 <= 32 ? 4u : 8u;
+    if (S <= 40) {
+      ch.cells = 1ull << S;
+      const uint64_t tb = ch.cells * ch.cell_bytes;
+      const bool cheap = ch.cells <= 8 * std::max<uint64_t>(ch.bound, 1) || tb <= (1ull << 20);
+      const bool fits = tb <= kcap * 8 || tb <= (1ull << 30);
+      ch.direct_ok = cheap && fits;
+      if (ch.direct_ok) dtab = std::max<size_t>(dtab, tb);
+    }
   }
   out.cap = kcap;
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
@@ -339,6 +368,13 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.table_ctas = (uint32_t)std::min<uint64_t>(MAPC_TABLE_MAX_CTAS, (kcap + mapc_table_tile() - 1) / mapc_table_tile());
   out.off_tparts = off; off += align_up((size_t)2 * out.table_ctas * sizeof(MapcTablePart));
   out.off_tstore = off; off += align_up((size_t)2 * out.table_ctas * MAPC_TABLE_WORDS * 4);
+  out.off_gate = off; off += align_up(64);
+  out.dtab_bytes = dtab;
+  if (dtab <= kcap * 8) {
+    out.off_dtab = out.off_b;                 // the direct path never touches key buffer B
+  } else {
+    out.off_dtab = off; off += align_up(dtab);
+  }
   out.total = off;
   out.stage_bytes = stage + align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult), 64);
   *P = std::move(out);
@@ -356,7 +392,7 @@ MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~
   bool table = false;
   if (sel == MAP_DETECT_TABLE) {
     table = true;
-  } else if (sel == MAP_DETECT_AUTO) {
+  } else if (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT) {
     const uint32_t S = L.sort_bits;
     table = nk >= (1ull << 16) && (S <= 1 || nk >= (1ull << (S - 1)));
   }
@@ -366,6 +402,13 @@ MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~
     L.sort_lo = L.pay_bits + L.tb;
   }
   return L;
+}
+
+// Sort-free direct-address detect for this chunk (MAP_DETECT_AUTO or
+// MAP_DETECT_DIRECT, and the chunk's table qualifies; direct.cu).
+bool use_direct(const Chunk& ch, uint32_t flags) {
+  const uint32_t sel = flags & MAP_DETECT_MASK;
+  return (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT) && ch.direct_ok;
 }
 
 // Whether a radix pass also accumulates the next pass's range table (k_rsweep
@@ -561,18 +604,38 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // amortised), the bytecode VM otherwise (map_exec.flags, MAP_GEN_*).
   const uint32_t gsel = ex->flags & 3u;
   const int gen_mode = gsel == MAP_GEN_VM ? 0 : gsel == MAP_GEN_JIT ? 1 : (p->C.max_accesses >= (1ull << 26) ? 1 : 0);
-  if (gen_mode == 1 && !P.jit_ready && !P.chunks.empty()) {
-    std::vector<mapj::JitChunk> jc;
-    for (auto& ch : P.chunks) jc.push_back(ch.jit);
-    std::string log;
-    if (mapj::build_module(jc, p->C.u32_mode, &P.jit, &log) != 0) {
-      p->last_error = "specialised generate: " + log;
-      return MAP_E_CUDA;
+  if (gen_mode == 1 && !P.chunks.empty()) {
+    // the modes this run needs: keys (sort / table detect), direct + filter (direct detect)
+    bool need[3] = {false, false, false};
+    for (auto& ch : P.chunks) {
+      if (use_direct(ch, ex->flags)) need[MAPC_MODE_DIRECT] = need[MAPC_MODE_FILTER] = true;
+      else need[MAPC_MODE_KEYS] = true;
     }
-    P.jit_ready = true;
+    std::vector<mapj::JitChunk> jc;
+    std::vector<uint32_t> cb;
+    for (auto& ch : P.chunks) {
+      jc.push_back(ch.jit);
+      cb.push_back(ch.cell_bytes);
+    }
+    std::vector<std::thread> builders;
+    std::string logs[3];
+    int rcs[3] = {0, 0, 0};
+    for (uint32_t m = 0; m < 3; ++m)
+      if (need[m] && !P.jit_ready[m])
+        builders.emplace_back([&, m]() { rcs[m] = mapj::build_module(jc, p->C.u32_mode, m, cb, &P.jit[m], &logs[m]); });
+    for (auto& t : builders) t.join();
+    for (uint32_t m = 0; m < 3; ++m) {
+      if (rcs[m] != 0) {
+        p->last_error = "specialised generate: " + logs[m];
+        return MAP_E_CUDA;
+      }
+      if (need[m]) P.jit_ready[m] = true;
+    }
   }
   uint32_t passes_total = 0;
   for (auto& ch : P.chunks) passes_total += effective_layout(ch, ex->flags).n_passes;
+  unsigned char* const dtab = base + P.off_dtab;
+  auto* gate = (uint32_t*)(base + P.off_gate);
   if (p->last_lookback != (void*)lookback || p->device != ex->device || p->epoch + passes_total >= 0xFFFF) {
     CK(cudaMemsetAsync(lookback, 0, P.lb_bytes, s));
     p->epoch = 0;
@@ -587,7 +650,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     if (c % world == rank) mine.push_back(c);
   // events: 2 per timed launch group + 2 for the whole run
   const bool prof = ex->stats != nullptr;
-  size_t need_ev = 2 + (prof ? mine.size() * (2 * (6 + MAPC_MAX_PASSES)) : 0);
+  size_t need_ev = 2 + (prof ? mine.size() * (2 * (8 + MAPC_MAX_PASSES)) : 0);
   while (p->events.size() < need_ev) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
@@ -612,6 +675,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   };
   uint64_t h2d = 0;
   CK(cudaEventRecord(p->events[0], s));
+  CK(cudaMemsetAsync(gate, 0xFF, sizeof(uint32_t), s));
   for (size_t c : mine) {
     const Chunk& ch = P.chunks[c];
     const MapcLayout L = effective_layout(ch, ex->flags);
@@ -621,14 +685,53 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     size_t m = begin(MAP_K_OTHER);
     CK(mapc_launch_chunk_init(ctrl, ch.dense_total, s));
     end(m);
+    if (use_direct(ch, ex->flags)) {
+      // sort-free direct-address detect (direct.cu): clear the table, fold every
+      // access into its cell, scan the table, re-emit the witness cell's keys
+      const uint64_t tbytes = ch.cells * ch.cell_bytes;
+      m = begin(MAP_K_CLEAR);
+      CK(mapc_launch_table_clear(dtab, tbytes, n_sms, s));
+      end(m);
+      if (ch.total_tiles) {
+        m = begin(MAP_K_DIRECT);
+        if (gen_mode == 1)
+          CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, segs, (int)ch.segs.size(), ch.total_tiles,
+                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, s));
+        else
+          CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                                  n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
+        end(m);
+      }
+      m = begin(MAP_K_DETECT);
+      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, s));
+      end(m);
+      m = begin(MAP_K_OTHER);
+      launches += 2;
+      st_acc.launches[MAP_K_OTHER] += 2;
+      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s));
+      if (ch.total_tiles) {
+        ++launches;
+        st_acc.launches[MAP_K_OTHER]++;
+        if (gen_mode == 1)
+          CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
+                                &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, s));
+        else
+          CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
+                                  n_sms, ch.nreg, MAPC_MAX_EMITS, 0, MAPC_MODE_FILTER, nullptr, ch.cell_bytes, s));
+      }
+      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s));
+      CK(mapc_launch_chunk_finish(ctrl, 0, res + c, s));
+      end(m);
+      continue;
+    }
     if (ch.total_tiles) {
       m = begin(MAP_K_GENERATE);
       if (gen_mode == 1)
-        CK(mapj::launch_chunk(P.jit, c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n, &ctrl->err,
-                              L.cap, n_sms, s));
+        CK(mapj::launch_chunk(P.jit[MAPC_MODE_KEYS], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n,
+                              &ctrl->err, L.cap, nullptr, n_sms, s));
       else
         CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
-                                n_sms, ch.nreg, ch.max_emits, 0, s));
+                                n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, s));
       end(m);
     }
     if (sort_mode == 1) {
@@ -704,6 +807,15 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     r.n_accesses += cr.n;
     r.racy_segments += cr.racy;
     err |= cr.err;
+    if (use_direct(P.chunks[c], ex->flags)) {
+      // direct path: the fused generate reads and writes every cell of the
+      // table once (the per-access reductions happen in L2), the clear writes
+      // it and the scan reads it
+      const uint64_t tbytes = P.chunks[c].cells * P.chunks[c].cell_bytes;
+      st_acc.bytes[MAP_K_DIRECT] += 2 * tbytes;
+      st_acc.bytes[MAP_K_CLEAR] += tbytes;
+      st_acc.bytes[MAP_K_DETECT] += tbytes;
+    } else {
     st_acc.bytes[MAP_K_GENERATE] += 8 * cr.n;
     // the histogram reads that ran: k_hist_ranges, and k_range_hist per later pass
     // whose table the previous scatter did not accumulate
@@ -718,6 +830,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       }
     }
     st_acc.bytes[MAP_K_DETECT] += 8 * cr.n;
+    }
     if (cr.witness != ~0ull) {
       map_witness w{};
       decode(p->C, P.chunks[c], cr.witness, &w);
@@ -741,7 +854,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     p->last_error = "internal consistency check failed (err bits " + std::to_string(err) + ")";
     return MAP_E_RANGE;
   }
-  r.verdict = have ? 1 : 0;
+  // a racy chunk may skip its witness (k_witness_gate) when an earlier racy
+  // chunk of this run must hold a smaller one
+  r.verdict = (have || r.racy_segments) ? 1 : 0;
   p->have_witness = have;
   p->wit = best;
   *out = r;
@@ -865,7 +980,7 @@ map_status map_generate_bucketed(map_program* p, const map_exec* ex, uint32_t ra
   CK(mapc_launch_chunk_init(d.ctrl, 0, d.s));
   const uint64_t t0 = ch.total_tiles * rank / world, t1 = ch.total_tiles * (rank + 1) / world;
   CK(mapc_launch_generate(d.segs, (int)ch.segs.size(), t0, t1, &L, p->C.u32_mode ? 1 : 0, d.bufA, d.ctrl, d.n_sms,
-                          ch.nreg, MAPC_MAX_EMITS, 1, d.s));
+                          ch.nreg, MAPC_MAX_EMITS, 1, MAPC_MODE_KEYS, nullptr, 4, d.s));
   CK(cudaMemsetAsync(d.xch, 0, 2 * 64 * sizeof(unsigned long long), d.s));
   CK(mapc_launch_bucket_count(d.bufA, d.ctrl, L.pay_bits, world, d.xch, d.n_sms, d.s));
   std::vector<unsigned long long> cnt(world);
@@ -956,7 +1071,7 @@ map_status map_list_races(map_program* p, const map_exec* ex, map_witness* out, 
     CK(mapc_launch_chunk_init(d.ctrl, ch.dense_total, d.s));
     if (ch.total_tiles)
       CK(mapc_launch_generate(d.segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, d.bufA,
-                              d.ctrl, d.n_sms, ch.nreg, ch.max_emits, 0, d.s));
+                              d.ctrl, d.n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, d.s));
     if (L.n_passes) {
       CK(cudaMemsetAsync(d.rhist, 0, P.rh_bytes, d.s));
       CK(mapc_launch_hist_ranges(d.bufA, d.ctrl, d.rhist, L.sort_lo, L.n_passes, d.G, d.s));
@@ -1056,7 +1171,7 @@ size_t map_debug_jit_source(const map_program* cp, uint64_t chunk_max_accesses, 
   if (!p || ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p)) != MAP_OK) return 0;
   if (chunk >= p->plan.chunks.size()) return 0;
   std::vector<mapj::JitChunk> one{p->plan.chunks[chunk].jit};
-  const std::string src = mapj::module_source(one, p->C.u32_mode);
+  const std::string src = mapj::module_source(one, p->C.u32_mode, MAPC_MODE_KEYS, 4);
   put_diag(src, out, cap);
   return src.size();
 }
@@ -1078,7 +1193,11 @@ int map_debug_jit_check(const map_program* cp, uint64_t chunk_max_accesses, char
         std::vector<char> cubin;
         std::string li;
         std::vector<mapj::JitChunk> one{chunks[i].jit};
-        if (mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode), &cubin, &li) != 0) {
+        bool bad = false;
+        for (uint32_t mode = 0; mode < 3 && !bad; ++mode)
+          bad = mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode, mode, chunks[i].cell_bytes), &cubin,
+                                    &li) != 0;
+        if (bad) {
           std::lock_guard<std::mutex> g(mu);
           r = 1;
           l = li;

@@ -28,6 +28,11 @@
 #define MAPC_GEN_V 4                 // tuples per thread per VM pass
 #define MAPC_GEN_TILE (MAPC_GEN_THREADS * MAPC_GEN_V)
 
+// Generate modes (generate.cu, capi/jit.cpp).
+#define MAPC_MODE_KEYS 0u      // write every access as a packed u64 key (sort / table detect)
+#define MAPC_MODE_DIRECT 1u    // fold every access into its cell of the direct-address table (direct.cu)
+#define MAPC_MODE_FILTER 2u    // re-emit only the keys whose sort field is ctrl->racy_sf (witness cell)
+
 enum MapcOpcode : uint8_t {
   VM_ADD = 0, VM_SUB,   /* monus */
   VM_MUL, VM_DIV, VM_MOD, VM_SHL, VM_SHR, VM_MIN, VM_MAX,
@@ -134,6 +139,8 @@ struct MapcCtrl {
   unsigned int rt_done[MAPC_MAX_PASSES];    // pass p's range table accumulated by the previous scatter
   unsigned int rt_bad[MAPC_MAX_PASSES];     // ... but abandoned (digits not warp-uniform): recompute
   MapcFastDiv rng_div;                      // divides a key position by rng_L
+  unsigned long long nf;                    // direct detect: keys of the witness cell re-emitted (filter mode)
+  unsigned long long wit_sf;                // direct detect: cell whose witness is folded (UINT64_MAX = none)
 };
 
 // Per-chunk result copied out by the last kernel of the chunk.

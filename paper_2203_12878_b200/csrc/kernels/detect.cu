@@ -459,6 +459,7 @@ __global__ void k_chunk_init(MapcCtrl* __restrict__ ctrl, unsigned long long n0)
   if (threadIdx.x == 0) {
     ctrl->witness = ~0ull;
     ctrl->racy_sf = ~0ull;
+    ctrl->wit_sf = ~0ull;
     ctrl->n = n0;            // dense keys are placed directly; compaction appends after them
   }
 }

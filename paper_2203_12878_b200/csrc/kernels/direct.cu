@@ -1,0 +1,169 @@
+// direct.cu -- sort-free direct-address detect.
+//
+// The race condition of a cell (phase, array, block, index) is order-
+// independent: racy <=> the cell holds a write and two
+// distinct tids.  Both facts survive a bitwise OR, so every access can be
+// folded into its cell with ONE fire-and-forget global red.or, and no key is
+// ever materialised or sorted:
+//
+//   cell |= tid | (~tid & M) << wt | kind << 2wt        (M = 2^wt - 1)
+//
+// After all accesses, A = OR of the tids and B = OR of their complements.
+// One tid t gives A & B = t & ~t = 0; two distinct tids differ in some bit k,
+// one sets bit k of A and the other bit k of B, so A & B != 0.  Hence
+//   racy(cell) <=> (cell >> 2wt) & 1  and  (cell & (cell >> wt) & M) != 0.
+// The table index of a cell is the chunk's sort field sf,
+// so sf order is cell order.  Generate (generate.cu / the JIT kernels, mode
+// MAPC_MODE_DIRECT) does the red.or; k_direct_scan reads the table once
+// (counts racy cells, atomicMin of the smallest racy sf); the canonical
+// witness of that one cell is folded from its keys, which generate re-emits in
+// mode MAPC_MODE_FILTER (k_witness_flat).  Cells are u32 when 2wt + 1 <= 32,
+// else u64.
+#include "common.cuh"
+#include "segstate.cuh"
+
+namespace mapk {
+
+constexpr int DS_THREADS = 256;
+
+template <typename C>
+__device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
+  const C m = wt >= 8 * sizeof(C) ? ~C(0) : ((C(1) << wt) - 1);
+  return ((c >> (2 * wt)) & 1) && ((c & (c >> wt) & m) != 0);
+}
+
+// Grid-stride over 16-byte vectors of cells; each thread's first racy cell is
+// its smallest (indices increase along the stride).
+template <typename C>
+__global__ void __launch_bounds__(DS_THREADS)
+k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
+  constexpr int PER = 16 / sizeof(C);
+  const unsigned long long nvec = cells / PER;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long best = ~0ull, racy = 0;
+  const uint4* __restrict__ v4 = reinterpret_cast<const uint4*>(tab);
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(v4 + i));
+    C c[PER];
+    memcpy(c, &v, 16);
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (cell_racy(c[j], wt)) {
+        ++racy;
+        if (best == ~0ull) best = i * PER + j;
+      }
+  }
+  // ragged tail (cells not a multiple of PER)
+  for (unsigned long long i = nvec * PER + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
+       i += stride)
+    if (cell_racy(tab[i], wt)) {
+      ++racy;
+      best = min(best, i);
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    racy += __shfl_xor_sync(0xffffffffu, racy, o);
+    best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (racy) atomicAdd(&ctrl->racy, racy);
+    if (best != ~0ull) atomicMin(&ctrl->racy_sf, best);
+  }
+}
+
+// Canonical witness of the smallest racy cell from its keys (all with sf =
+// ctrl->racy_sf, in arrival order, ctrl->nf of them; filter-mode generate).
+constexpr int WF_THREADS = 512;
+__global__ void __launch_bounds__(WF_THREADS)
+k_witness_flat(const unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t pay_bits,
+               uint32_t w_tid, unsigned long long cap) {
+  const unsigned long long target = ctrl->wit_sf;
+  if (target == ~0ull) return;
+  const unsigned long long n = ctrl->nf;
+  if (n > cap) {
+    if (threadIdx.x == 0) atomicOr(&ctrl->err, MAPC_ERR_CAPACITY);
+    return;
+  }
+  const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
+  __shared__ St part[WF_THREADS];
+  St s;
+  st_init(s);
+  for (unsigned long long i = threadIdx.x; i < n; i += WF_THREADS) {
+    const unsigned long long key = keys[i];
+    if ((key >> pay_bits) != target) {          // library bug guard: the filter let a foreign key through
+      atomicOr(&ctrl->err, MAPC_ERR_LAYOUT);
+      continue;
+    }
+    st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = WF_THREADS / 2; h; h >>= 1) {
+    if (threadIdx.x < h) st_merge(part[threadIdx.x], part[threadIdx.x + h]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ctrl->witness = st_witness(part[0], target, w_tid);
+}
+
+// Which racy chunk folds a witness.  The canonical witness is the minimum over
+// chunks, and phase is its most significant field: once a racy chunk whose
+// phases end at ph_hi has been seen (on this stream, in chunk order), a later
+// chunk whose phases all exceed ph_hi cannot hold the minimum, so its filter
+// pass is skipped (its racy count still counts).  *gate = the smallest ph_hi
+// of a racy chunk so far (UINT32_MAX = none; reset once per run).
+__global__ void k_witness_gate(MapcCtrl* __restrict__ ctrl, uint32_t* __restrict__ gate, uint32_t ph_lo,
+                               uint32_t ph_hi) {
+  const unsigned long long sf = ctrl->racy_sf;
+  if (sf == ~0ull) return;
+  if (*gate < ph_lo) return;
+  ctrl->wit_sf = sf;
+  if (ph_hi < *gate) *gate = ph_hi;
+}
+
+// Table reset: 16-byte stores over the cells (the table region is 256-B aligned).
+__global__ void k_table_clear(uint4* __restrict__ tab, unsigned long long n16) {
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    tab[i] = make_uint4(0, 0, 0, 0);
+}
+
+}  // namespace mapk
+
+extern "C" cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, cudaStream_t s) {
+  const unsigned long long n16 = (bytes + 15) / 16;
+  if (n16 == 0) return cudaSuccess;
+  const unsigned long long want = (n16 + 255) / 256;
+  const unsigned long long cap = (unsigned long long)n_sms * 8;
+  mapk::k_table_clear<<<(int)(want < cap ? want : cap), 256, 0, s>>>((uint4*)tab, n16);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi,
+                                                cudaStream_t s) {
+  mapk::k_witness_gate<<<1, 1, 0, s>>>(ctrl, gate, ph_lo, ph_hi);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes,
+                                               uint32_t w_tid, MapcCtrl* ctrl, int n_sms, cudaStream_t s) {
+  if (cells == 0) return cudaSuccess;
+  const unsigned long long vec = (cells * cell_bytes + 15) / 16;
+  const unsigned long long want = (vec + mapk::DS_THREADS - 1) / mapk::DS_THREADS;
+  const unsigned long long cap = (unsigned long long)n_sms * 8;
+  const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  if (cell_bytes == 4)
+    mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
+  else
+    mapk::k_direct_scan<unsigned long long>
+        <<<grid, mapk::DS_THREADS, 0, s>>>((const unsigned long long*)tab, cells, w_tid, ctrl);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits,
+                                                uint32_t w_tid, unsigned long long cap, cudaStream_t s) {
+  mapk::k_witness_flat<<<1, mapk::WF_THREADS, 0, s>>>(keys, ctrl, pay_bits, w_tid, cap);
+  return cudaGetLastError();
+}

@@ -36,7 +36,7 @@ template <typename W>
 __global__ void __launch_bounds__(MAPC_GEN_THREADS)
 k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long tile_lo, unsigned long long tile_hi,
             MapcLayout lay, unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t nreg,
-            uint32_t force_compact) {
+            uint32_t force_compact, uint32_t mode, void* __restrict__ tab, uint32_t cell_bytes) {
   constexpr int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   constexpr uint32_t WB = VmWidth<W>::bits;
   extern __shared__ __align__(16) unsigned char gsm[];
@@ -46,6 +46,13 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
   __shared__ unsigned long long s_base;
   const int me = threadIdx.x;
   uint32_t err = 0;
+  // filter mode: only the keys of the witness cell (none if the chunk is DRF)
+  const unsigned long long target = mode == MAPC_MODE_FILTER ? ctrl->wit_sf : ~0ull;
+  if (mode == MAPC_MODE_FILTER && target == ~0ull) return;
+  unsigned long long* const n_out = mode == MAPC_MODE_FILTER ? &ctrl->nf : &ctrl->n;
+  // direct mode: cell code of (tid, kind) = tid | (~tid & M) << wt | kind << 2wt (direct.cu)
+  const uint32_t wt = lay.w_tid;
+  const unsigned long long tmask = wt >= 64 ? ~0ull : ((1ull << wt) - 1);
 #define RG(r, v) R[((size_t)(r) * V + (v)) * T + me]
 
   for (unsigned long long tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
@@ -55,7 +62,8 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
       if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
     }
     const MapcSeg& sg = segs[lo];
-    const bool dense = sg.dense && !force_compact;    // stage API: every key goes through compaction
+    // stage API and filter mode: every key goes through compaction
+    const bool dense = sg.dense && !force_compact && mode != MAPC_MODE_FILTER;
     const uint32_t tl0 = (uint32_t)(tile - sg.tile_begin) * (uint32_t)(V * T);
     const uint32_t L = sg.n_levels;
     uint32_t tidv[V], lbv[V];
@@ -162,7 +170,16 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
             const unsigned long long idx = (unsigned long long)AV(v) - lay.idx_lo;
             if (lay.w_index < 64 && (idx >> lay.w_index) != 0) err |= MAPC_ERR_LAYOUT;
             const unsigned long long sf = sg.key_hi + arr + ((unsigned long long)lbv[v] << lay.w_index) + idx;
+            if (mode == MAPC_MODE_DIRECT) {
+              const unsigned long long code =
+                  tidv[v] | ((~(unsigned long long)tidv[v] & tmask) << wt) | (kind << (2 * wt));
+              if (cell_bytes == 4) atomicOr(reinterpret_cast<uint32_t*>(tab) + sf, (uint32_t)code);
+              else atomicOr(reinterpret_cast<unsigned long long*>(tab) + sf, code);
+              cnt += dense ? 0u : 1u;
+              continue;
+            }
             const unsigned long long key = (sf << lay.pay_bits) | ((unsigned long long)tidv[v] << 1) | kind;
+            if (mode == MAPC_MODE_FILTER && sf != target) continue;
             if (dense) {
               keys[sg.key_begin + (unsigned long long)e * sg.n_tuples + tl0 + v * T + me] = key;
             } else {
@@ -179,10 +196,15 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
 #undef BV
 #undef VLOOP
     }
-    if (!dense) {                                     // uniform across the CTA
+    if (mode == MAPC_MODE_DIRECT) {                   // only the count: the accesses are in the table
+      if (!dense) {
+        const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);
+        if ((me & 31) == 0 && wsum) atomicAdd(&ctrl->n, (unsigned long long)wsum);
+      }
+    } else if (!dense) {                              // uniform across the CTA
       uint32_t total;
       const uint32_t excl = block_excl_scan<T>(cnt, scan_tmp, &total);
-      if (me == 0) s_base = total ? atomicAdd(&ctrl->n, (unsigned long long)total) : 0ull;
+      if (me == 0) s_base = total ? atomicAdd(n_out, (unsigned long long)total) : 0ull;
       __syncthreads();
       const unsigned long long obase = s_base;
       for (uint32_t j = 0; j < cnt; ++j) {
@@ -208,7 +230,8 @@ extern "C" cudaError_t mapc_upload_ops(const MapcOp* host_ops, size_t n_ops, cud
 extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long long tile_lo,
                                             unsigned long long tile_hi, const MapcLayout* lay, int u32_mode,
                                             unsigned long long* keys, MapcCtrl* ctrl, int n_sms, uint32_t nreg,
-                                            uint32_t max_emits, uint32_t force_compact, cudaStream_t s) {
+                                            uint32_t max_emits, uint32_t force_compact, uint32_t mode, void* tab,
+                                            uint32_t cell_bytes, cudaStream_t s) {
   if (tile_hi <= tile_lo) return cudaSuccess;
   const unsigned long long total_tiles = tile_hi - tile_lo;
   const size_t wb = u32_mode ? 4 : 8;
@@ -216,7 +239,8 @@ extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, uns
                       (size_t)MAPC_GEN_V * max_emits * MAPC_GEN_THREADS * 8;
   const void* fn = u32_mode ? (const void*)mapk::k_generate2<uint32_t> : (const void*)mapk::k_generate2<uint64_t>;
   static size_t attr[2] = {0, 0};
-  if (smem > 48 * 1024 && attr[u32_mode ? 0 : 1] < smem) {
+  // opt in above 32 KiB: the default 48 KiB limit also covers the static shared variables
+  if (smem > 32 * 1024 && attr[u32_mode ? 0 : 1] < smem) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[u32_mode ? 0 : 1] = smem;
@@ -227,6 +251,6 @@ extern "C" cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, uns
   unsigned long long cap = (unsigned long long)n_sms * occ;
   int grid = (int)(total_tiles < cap ? total_tiles : cap);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&tile_lo, (void*)&tile_hi, (void*)lay, (void*)&keys,
-                  (void*)&ctrl, (void*)&nreg, (void*)&force_compact};
+                  (void*)&ctrl, (void*)&nreg, (void*)&force_compact, (void*)&mode, (void*)&tab, (void*)&cell_bytes};
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, smem, s);
 }

@@ -22,7 +22,7 @@ def main(rep, launches, tag):
     prof = os.path.join(ROOT, "profiles")
     hdr, units, rows = raw_rows(rep)
     idx = {h: i for i, h in enumerate(hdr)}
-    lines, traffic = [], None
+    lines, traffic, direct = [], None, None
     for r in rows:
         name = r[idx["Kernel Name"]]
         get = lambda k: float(r[idx[k]]) if k in idx and r[idx[k]] else float("nan")
@@ -34,6 +34,10 @@ def main(rep, launches, tag):
         lines.append(f"{name.split('(')[0]:40s} dur {dur*1e3:8.3f} ms  dram read {rd/1e9:7.3f} GB  write {wr/1e9:7.3f} GB  "
                      f"-> {(rd+wr)/dur/1e9:7.1f} GB/s  issue {get('smsp__issue_active.avg.pct_of_peak_sustained_active'):5.1f}%  "
                      f"occupancy {get('sm__warps_active.avg.pct_of_peak_sustained_active'):5.1f}%  regs {get('launch__registers_per_thread'):.0f}")
+        if name.startswith("gen_") and (direct is None or dur > direct["duration_s"]):
+            # the direct-mode generate (the longest gen_ launch: the filter pass exits at once when DRF)
+            direct = {"kernel": name.split("(")[0] + " (mode direct)", "dram_bytes_per_launch": rd + wr, "dram_read": rd,
+                      "dram_write": wr, "duration_s": dur, "source": os.path.basename(rep)}
         if "k_rsweep" in name and traffic is None:
             traffic = {"kernel": name.split("(")[0], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                        "duration_s": dur, "source": os.path.basename(rep)}
@@ -43,6 +47,9 @@ def main(rep, launches, tag):
     if traffic:
         with open(os.path.join(prof, "ncu_rsweep_traffic.json"), "w") as f:
             json.dump(traffic, f, indent=1)
+    if direct and "direct" in tag:
+        with open(os.path.join(prof, "ncu_direct_traffic.json"), "w") as f:
+            json.dump(direct, f, indent=1)
     # launch list -> shares
     shutil.copy(launches, os.path.join(prof, f"{tag}_launches.csv"))
     txt = open(launches).read()

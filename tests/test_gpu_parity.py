@@ -211,7 +211,7 @@ def test_exchange_mode_many_chunks():
 
 # ---- detect paths: full sort + segmented scan vs partial sort + bucket tables ----
 
-@pytest.mark.parametrize("detect", ["sort", "table"])
+@pytest.mark.parametrize("detect", ["sort", "table", "direct"])
 @pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
 def test_detect_paths_match_oracle(name, sizes, detect):
     inst = config(name, **sizes)
@@ -234,7 +234,7 @@ def test_fuzz_corpus_table_detect():
     assert not bad, bad[:3]
 
 
-@pytest.mark.parametrize("detect", ["sort", "table"])
+@pytest.mark.parametrize("detect", ["sort", "table", "direct"])
 def test_one_bucket_across_all_ranges(detect):
     # few distinct cells, millions of keys: with the table path every range of the
     # detect kernel sees the same bucket, so the partial tables chain end to end
@@ -253,10 +253,12 @@ def test_full_size_detect_paths_agree(name):
     p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
     a = p.check_races(detect="sort")
     b = p.check_races(detect="table")
+    c = p.check_races(detect="direct")
     assert (a.verdict, a.witness, a.n_accesses, a.racy_segments) == (b.verdict, b.witness, b.n_accesses, b.racy_segments)
+    assert (a.verdict, a.witness, a.n_accesses, a.racy_segments) == (c.verdict, c.witness, c.n_accesses, c.racy_segments)
 
 
-@pytest.mark.parametrize("detect", ["sort", "table"])
+@pytest.mark.parametrize("detect", ["sort", "table", "direct"])
 @pytest.mark.parametrize("name,sizes", [("5a", dict(T=3, R=8, C=64)), ("5b", dict(T=2, R=4, C=96)),
                                         ("5b", dict(T=1, R=3, C=40)), ("1a", dict(M=4096))])
 def test_jit_single_segment_chunks(name, sizes, detect):
@@ -317,7 +319,7 @@ def test_race_list_full_size_properties(name):
     assert tuples == sorted(tuples) and len(set(t[:4] for t in tuples)) == len(tuples)
 
 
-@pytest.mark.parametrize("detect", ["table", "sort"])
+@pytest.mark.parametrize("detect", ["table", "sort", "direct"])
 def test_scattered_indices_two_bucket_passes(detect):
     # 2^21 accesses over a 2^22-cell index space, scattered by the index expression:
     # two radix passes on the bucket bits whose next-pass digits are not warp-uniform,
@@ -327,3 +329,72 @@ def test_scattered_indices_two_bucket_passes(detect):
     r = mc.check(src, block=(1024, 1, 1), params=params, detect=detect)
     o = oracle.check(src, block=(1024, 1, 1), params=params)
     same(r, o)
+
+
+# ---- sort-free direct-address detect (direct.cu) -----------------------------
+
+def _got(r):
+    return (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments)
+
+
+def _want(o):
+    return (o.verdict, o.witness, o.n_accesses, o.n_racy_segments)
+
+
+@pytest.mark.parametrize("gen", ["vm", "jit"])
+def test_fuzz_corpus_direct_detect(gen):
+    bad = []
+    seeds = range(1, 400, 2) if gen == "vm" else range(0, 120, 3)
+    for seed in seeds:
+        inst, _ = fuzz.random_instance(seed)
+        o = oracle.check_instance(inst, threads=1)
+        p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+        r = p.check_races(detect="direct", gen=gen)
+        if _got(r) != _want(o):
+            bad.append((seed, inst.src, _got(r), _want(o)))
+        # one (phase, block) unit per chunk: the witness gate skips later racy chunks
+        unit = max(1, p.info.max_unit_accesses)
+        r = p.check_races(detect="direct", gen=gen, chunk_max_accesses=unit)
+        if _got(r) != _want(o):
+            bad.append((seed, "unit chunks", inst.src, _got(r), _want(o)))
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("name,sizes", [("5a", dict(T=4, R=4, C=64)), ("3b", dict(ts=32, rw=8, grid=64)),
+                                        ("4a", dict(n=4096)), ("2b", {})])
+def test_direct_path_runs(name, sizes):
+    # the automatic choice takes the direct path on dense configs: the fused
+    # generate + table launches ran, and no key was generated or sorted
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    r = p.check_races(profile=True)
+    same(r, oracle.check_instance(inst))
+    assert r.kernels["direct"]["launches"] > 0 and r.kernels["clear"]["launches"] > 0
+    assert r.kernels["generate"]["launches"] == 0 and r.kernels["onesweep"]["launches"] == 0
+
+
+def test_direct_u64_cells():
+    # 65536 threads per block: w_tid = 16 > 15, so cells are u64
+    for src in ["wr[tid % 7]", "rd[tid % 5]; if (tid = 40000) { wr[3] } else { skip }", "wr[tid]; rd[tid]"]:
+        o = oracle.check(src, block=(1024, 64, 1))
+        for detect in ("direct", "sort"):
+            same(mc.check(src, block=(1024, 64, 1), detect=detect), o)
+
+
+def test_direct_racy_every_chunk():
+    # every phase racy, one phase per chunk: only the first racy chunk folds a
+    # witness (later phases cannot hold the minimum); the racy counts still add up
+    inst = config("5b", block=64, T=6, R=4, C=16)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    unit = max(1, p.info.max_unit_accesses)
+    for gen in ("vm", "jit"):
+        same(p.check_races(detect="direct", gen=gen, chunk_max_accesses=unit), o)
+
+
+def test_direct_broadcast_witness_cell():
+    # the witness cell holds 2^20 + 1024 accesses: the filter re-emits all of them
+    src = "forU x in 0..1024 { rd[0] }; wr[0]"
+    o = oracle.check(src, block=(1024, 1, 1))
+    for gen in ("vm", "jit"):
+        same(mc.check(src, block=(1024, 1, 1), detect="direct", gen=gen), o)
