@@ -43,8 +43,11 @@ std::string opnd(const MapcOp& op, bool a_side, bool u32) {
 
 // Straight-line body of one group program for one tuple (variables in scope:
 // W r[], bool act, bool valid, u32 tidv, u32 lbv, u32 e-counter, tuple index t).
-std::string program_body(const std::vector<MapcOp>& ops, bool u32) {
+// site_literal: EMIT expands to EMIT_SITE(k, index, array, kind) with the
+// site's ordinal k as a literal (the paired direct mode keeps per-site state).
+std::string program_body(const std::vector<MapcOp>& ops, bool u32, bool site_literal = false) {
   std::ostringstream s;
+  int site = 0;
   const char* WB = u32 ? "32u" : "64u";
   for (const MapcOp& op : ops) {
     const uint32_t c = op.code & MAPC_CODE_MASK;
@@ -87,8 +90,12 @@ std::string program_body(const std::vector<MapcOp>& ops, bool u32) {
       case VM_ACT: s << "act = " << A << " != 0;\n"; break;
       case VM_MOVI: s << D << " = " << lit(op.imm, u32) << ";\n"; break;
       case VM_EMIT:
-        s << "if (act && valid) { EMIT_KEY(" << A << ", " << (op.aux >> 1) << "ull, " << (op.aux & 1u) << "ull); }\n"
-          << "++e;\n";
+        if (site_literal)
+          s << "if (act && valid) { EMIT_SITE(" << site++ << ", " << A << ", " << (op.aux >> 1) << "ull, " << (op.aux & 1u)
+            << "ull); }\n";
+        else
+          s << "if (act && valid) { EMIT_KEY(" << A << ", " << (op.aux >> 1) << "ull, " << (op.aux & 1u) << "ull); }\n"
+            << "++e;\n";
         break;
       default: break;
     }
@@ -192,6 +199,62 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "    int lo = 0, hi = n_segs - 1;\n"
     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
     ;
+  // Direct mode with u32 cells: every thread takes two CONSECUTIVE tuples
+  // (t, t+1) of the tile; an access site whose two cells are adjacent and
+  // 8-byte aligned (sf, sf + 1; sf even -- the unit-stride innermost loops of
+  // row sweeps and stencils) is folded with ONE red.or.b64 of both codes,
+  // otherwise with one red.or.b32 each.  The generate is bound by the rate of
+  // memory instructions (profiles/r1h_red_width_microbench.txt: b32 2.9 TB/s of
+  // payload, b64 4.0 TB/s with a DRAM-resident table), so pairing halves the
+  // instructions on the common path.  Same cells, same codes: same table.
+  const bool paired = mode == MAPC_MODE_DIRECT && cell_bytes == 4;
+  auto paired_case = [&](std::ostringstream& s, const JitProgram& pg) {
+    int ne = 0;
+    for (const MapcOp& op : pg.ops) ne += (op.code & MAPC_CODE_MASK) == VM_EMIT;
+    const int NE = std::max(ne, 1);
+    s << "    case " << pg.prog_begin << "u: {\n"
+      << "#pragma unroll 1\n"
+      << "      for (int v = 0; v < " << V / 2 << "; ++v) {\n"
+      << "        const u32 tp = tl0 + v * " << 2 * T << "u + 2u * me;\n"
+      << "        u64 sfP[2][" << NE << "]; u32 cdP[2][" << NE << "]; bool okP[2][" << NE << "];\n"
+      << "#pragma unroll\n"
+      << "        for (int h = 0; h < 2; ++h) {\n"
+      << "#pragma unroll\n"
+      << "          for (int k = 0; k < " << NE << "; ++k) okP[h][k] = false;\n"
+      << "          const u32 t = tp + h;\n"
+      << "          const bool valid = t < sg.n_tuples;\n"
+      << "          u32 rem = valid ? t : 0u;\n"
+      << "          W r[" << MAPC_NREG << "];\n";
+    for (int l = (int)pg.n_levels - 1; l >= 0; --l)
+      s << "          { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
+        << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
+    s << "          const u32 qb = fdiv(rem, sg.tid_div);\n"
+      << "          const u32 tidv = rem - qb * sg.tid_div.d;\n"
+      << "          const u32 lbv = sg.lb0 + qb;\n"
+      << "          r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
+      << "          bool act = true;\n"
+      << "#define EMIT_SITE(K, IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
+         "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
+         "sfP[h][K] = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
+         "cdP[h][K] = tidv | ((~tidv & (u32)TMASK) << " << ch.lay.w_tid << "u) | ((u32)(KIND) << "
+      << 2 * ch.lay.w_tid << "u); okP[h][K] = true; }\n"
+      << program_body(pg.ops, u32, true)
+      << "#undef EMIT_SITE\n"
+      << "          (void)act;\n"
+      << "        }\n"
+      << "#pragma unroll\n"
+      << "        for (int k = 0; k < " << ne << "; ++k) {\n"
+      << "          if (okP[0][k] && okP[1][k] && sfP[1][k] == sfP[0][k] + 1 && !(sfP[0][k] & 1ull)) {\n"
+      << "            atomicOr(reinterpret_cast<u64*>(keys) + (sfP[0][k] >> 1), (u64)cdP[0][k] | ((u64)cdP[1][k] << 32));\n"
+      << "          } else {\n"
+      << "            if (okP[0][k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[0][k], cdP[0][k]);\n"
+      << "            if (okP[1][k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[1][k], cdP[1][k]);\n"
+      << "          }\n"
+      << "          if (!sg.dense) cnt += (u32)okP[0][k] + (u32)okP[1][k];\n"
+      << "        }\n"
+      << "      }\n"
+      << "      break; }\n";
+  };
   // the per-tile body, emitted once per baked segment (fields as literals) and
   // once generic (fields loaded from segs[])
   auto tile_body = [&](std::ostringstream& s) {
@@ -203,6 +266,10 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
          << emit_tail(mode, ch.lay.w_tid, T) << " }\n"
       << "    switch (sg.prog_begin) {\n";
     for (const JitProgram& pg : ch.programs) {
+      if (paired) {
+        paired_case(s, pg);
+        continue;
+      }
       s << "    case " << pg.prog_begin << "u: {\n"
         << "#pragma unroll 1\n"
         << "      for (int v = 0; v < " << V << "; ++v) {\n"

@@ -32,29 +32,48 @@ __device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
   return ((c >> (2 * wt)) & 1) && ((c & (c >> wt) & m) != 0);
 }
 
-// Grid-stride over 16-byte vectors of cells; each thread's first racy cell is
-// its smallest (indices increase along the stride).
+// Grid-stride over 16-byte vectors of cells, DS_UNROLL vectors in flight per
+// thread; each thread's first racy cell is its smallest (indices increase
+// along the stride).  The common all-clean vector costs a few ALU ops per cell.
+constexpr int DS_UNROLL = 4;
 template <typename C>
 __global__ void __launch_bounds__(DS_THREADS)
 k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
   constexpr int PER = 16 / sizeof(C);
   const unsigned long long nvec = cells / PER;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const C m = wt >= 8 * sizeof(C) ? ~C(0) : ((C(1) << wt) - 1);
   unsigned long long best = ~0ull, racy = 0;
   const uint4* __restrict__ v4 = reinterpret_cast<const uint4*>(tab);
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(v4 + i));
-    C c[PER];
-    memcpy(c, &v, 16);
+  for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < nvec;
+       i0 += stride * DS_UNROLL) {
+    uint4 v[DS_UNROLL];
 #pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (cell_racy(c[j], wt)) {
-        ++racy;
-        if (best == ~0ull) best = i * PER + j;
+    for (int u = 0; u < DS_UNROLL; ++u) {
+      const unsigned long long i = i0 + u * stride;
+      if (i < nvec)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(v4 + i));
+      else
+        v[u] = make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < DS_UNROLL; ++u) {
+      C c[PER];
+      memcpy(c, &v[u], 16);
+      C hit = 0;
+#pragma unroll
+      for (int j = 0; j < PER; ++j) hit |= (c[j] >> (2 * wt)) & (C)((c[j] & (c[j] >> wt) & m) != 0);
+      if (hit) {
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+          if (cell_racy(c[j], wt)) {
+            ++racy;
+            best = min(best, (i0 + u * stride) * PER + j);
+          }
       }
+    }
   }
   // ragged tail (cells not a multiple of PER)
   for (unsigned long long i = nvec * PER + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
@@ -151,7 +170,7 @@ extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long lo
                                                uint32_t w_tid, MapcCtrl* ctrl, int n_sms, cudaStream_t s) {
   if (cells == 0) return cudaSuccess;
   const unsigned long long vec = (cells * cell_bytes + 15) / 16;
-  const unsigned long long want = (vec + mapk::DS_THREADS - 1) / mapk::DS_THREADS;
+  const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
   const unsigned long long cap = (unsigned long long)n_sms * 8;
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   if (cell_bytes == 4)

@@ -1,0 +1,57 @@
+"""The cell code of the direct-address detect (include/mapcheck.h
+MAP_DETECT_DIRECT), checked against the definition it replaces -- no GPU.
+
+A cell is racy iff it holds a write and two DISTINCT tids (
+same-thread pairs never race, R11).  The kernels keep per cell only
+the bitwise OR of code(t, k) = t | (~t & M) << wt | k << 2wt over its
+accesses.  Claim: (OR t) & (OR ~t) & M != 0  <=>  the tids are not all equal.
+Brute force over every nonempty tid set for wt <= 4 (all 2^16 - 1 subsets of
+16 tids), plus random multisets with kinds for larger wt, against the plain
+definition (some pair of accesses with different tids, one of them a write).
+"""
+import itertools
+import random
+
+import pytest
+
+
+def code(t, k, wt):
+    m = (1 << wt) - 1
+    return t | ((~t & m) << wt) | (k << (2 * wt))
+
+
+def racy_from_cell(c, wt):
+    m = (1 << wt) - 1
+    return bool((c >> (2 * wt)) & 1) and (c & (c >> wt) & m) != 0
+
+
+def racy_by_definition(accs):
+    return any(t1 != t2 and (k1 or k2) for (t1, k1), (t2, k2) in itertools.combinations(accs, 2))
+
+
+@pytest.mark.parametrize("wt", [0, 1, 2, 3, 4])
+def test_two_distinct_tids_exhaustive(wt):
+    n = 1 << wt
+    m = (1 << wt) - 1
+    for mask in range(1, 1 << n):
+        tids = [t for t in range(n) if mask >> t & 1]
+        a = b = 0
+        for t in tids:
+            a |= t
+            b |= ~t & m
+        assert ((a & b) != 0) == (len(tids) >= 2)
+
+
+@pytest.mark.parametrize("wt", [1, 5, 10, 15, 16, 31])
+def test_cell_code_matches_race_definition(wt):
+    rng = random.Random(1000 + wt)
+    for _ in range(3000):
+        n = rng.randint(1, 6)
+        pool = [rng.randrange(1 << wt) for _ in range(rng.randint(1, 3))]
+        accs = [(rng.choice(pool), rng.random() < 0.3) for _ in range(n)]
+        c = 0
+        for t, k in accs:
+            c |= code(t, int(k), wt)
+        assert racy_from_cell(c, wt) == racy_by_definition(accs)
+    # the code fits the cell: 2 wt + 1 bits (u32 cells up to wt = 15)
+    assert code((1 << wt) - 1, 1, wt) < (1 << (2 * wt + 1))

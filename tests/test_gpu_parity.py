@@ -398,3 +398,18 @@ def test_direct_broadcast_witness_cell():
     o = oracle.check(src, block=(1024, 1, 1))
     for gen in ("vm", "jit"):
         same(mc.check(src, block=(1024, 1, 1), detect="direct", gen=gen), o)
+
+
+@pytest.mark.parametrize("src,params", [
+    ("params N; forU c in 0..N { wr[c + 1 + tid * N] }", {"N": 64}),                      # odd base: no pairs
+    ("params N; forU c in 0..N { if (c % 3 = 1) { wr[c + tid * N] } else { rd[c + tid * N] } }", {"N": 64}),
+    ("params N; forU c in 0..N { rd[c + tid * (N - 1)]; if (c = 5) { wr[c + tid * (N - 1)] } else { skip } }",
+     {"N": 33}),                                                                            # overlaps, odd rows
+    ("params N; forU c in 0..N { rd[2 * c]; wr[2 * c + 1 + (tid % 2)] }", {"N": 100}),      # stride 2
+])
+def test_direct_paired_cells(src, params):
+    # the paired direct generate (two consecutive tuples per thread, one red.or.b64
+    # for adjacent aligned cells) on aligned, unaligned, guarded and strided sites
+    o = oracle.check(src, block=(64, 1, 1), grid=(3, 1, 1), params=params)
+    for gen in ("jit", "vm"):
+        same(mc.check(src, block=(64, 1, 1), grid=(3, 1, 1), params=params, detect="direct", gen=gen), o)
