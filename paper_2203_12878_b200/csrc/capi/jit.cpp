@@ -13,6 +13,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdint>
 #include <thread>
@@ -109,7 +110,7 @@ typedef unsigned long long u64;
 struct FD { u32 d, m, s, pow2; };
 struct Seg {
   u64 tuple_begin, n_tuples, tile_begin, key_begin, key_hi;
-  u32 prog_begin, prog_end, n_levels, b0, lb0, n_emits, dense, pad;
+  u32 prog_begin, prog_end, n_levels, b0, lb0, n_emits, dense, tid_inner;
   FD trip_div[8];
   FD tid_div;
 };
@@ -147,6 +148,22 @@ struct Module {
 std::mutex g_mu;
 std::map<std::string, Module> g_cache;   // source text -> loaded module (process-wide)
 
+// Mixed-radix decode of the tuple index `rem` (in scope) into r[tid], r[bid],
+// r[k_l], tidv, lbv: (block, tid, k_0..k_{L-1}) with k_{L-1} fastest, or tid
+// fastest when sg.tid_inner (a literal for baked segments, so one branch folds).
+std::string decode_tuple(const JitProgram& pg, const std::string& ind) {
+  std::ostringstream s;
+  s << ind << "u32 tidv = 0;\n"
+    << ind << "if (sg.tid_inner) { const u32 q = fdiv(rem, sg.tid_div); tidv = rem - q * sg.tid_div.d; rem = q; }\n";
+  for (int l = (int)pg.n_levels - 1; l >= 0; --l)
+    s << ind << "{ const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
+      << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
+  s << ind << "if (!sg.tid_inner) { const u32 q = fdiv(rem, sg.tid_div); tidv = rem - q * sg.tid_div.d; rem = q; }\n"
+    << ind << "const u32 lbv = sg.lb0 + rem;\n"
+    << ind << "r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + rem);\n";
+  return s.str();
+}
+
 // The tail of EMIT_KEY per generate mode (variables in scope: sf_, tidv, KIND,
 // sg, e, t, cnt, stage, keys, me).
 std::string emit_tail(uint32_t mode, uint32_t w_tid, int T) {
@@ -174,12 +191,19 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   // keys staged per thread per tile for compaction: the guarded segments' emits
   // (keys mode), every segment's (filter mode), none (direct mode)
+  const bool paired = mode == MAPC_MODE_DIRECT && cell_bytes == 4;
   const uint32_t stage_emits = V * (mode == MAPC_MODE_DIRECT   ? 1u
                                     : mode == MAPC_MODE_FILTER ? (uint32_t)MAPC_MAX_EMITS
                                                                : std::max(1u, ch.max_emits));
-  s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index
+  // direct mode: minimum resident CTAs per SM (caps registers at 40): 12 measured
+  // best on 5a/5b (profiles/r1j_probe_minb.jsonl, r1j_probe_dyn_minb.jsonl); MAPC_JIT_MINB overrides (0 = none)
+  static const int minb_env = [] { const char* e = getenv("MAPC_JIT_MINB"); return e ? atoi(e) : 12; }();
+  const int minb = mode == MAPC_MODE_DIRECT ? minb_env : 0;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << T;
+  if (minb > 0) s << ", " << minb;
+  s << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
-       "u64 cap, const u64* target_ptr) {\n"
+       "u64 cap, const u64* target_ptr, u64* tile_ctr) {\n"
     << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
     << "  typedef " << (cell_bytes == 4 ? "u32" : "u64") << " CELL;\n"
     << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
@@ -187,10 +211,13 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
     << "  __shared__ u64 s_base;\n"
+    << "  (void)tile_ctr;\n"
     << "  const int me = threadIdx.x;\n"
     << "  u32 err = 0;\n"
     << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
     << "  (void)TMASK; (void)target_ptr;\n";
+  if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
+    s << "  u64 sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS << "]; bool okP[" << MAPC_MAX_EMITS << "];\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
@@ -207,51 +234,47 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // memory instructions (profiles/r1h_red_width_microbench.txt: b32 2.9 TB/s of
   // payload, b64 4.0 TB/s with a DRAM-resident table), so pairing halves the
   // instructions on the common path.  Same cells, same codes: same table.
-  const bool paired = mode == MAPC_MODE_DIRECT && cell_bytes == 4;
   auto paired_case = [&](std::ostringstream& s, const JitProgram& pg) {
     int ne = 0;
     for (const MapcOp& op : pg.ops) ne += (op.code & MAPC_CODE_MASK) == VM_EMIT;
     const int NE = std::max(ne, 1);
+    const std::string cell =
+        "const u64 idx_ = (u64)(IX) - IDX_LO; if (WI < 64 && (idx_ >> WI) != 0) err |= " +
+        std::to_string(MAPC_ERR_LAYOUT) + "u; "
+        "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
+        "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) + "u) | ((u32)(KIND) << " +
+        std::to_string(2 * ch.lay.w_tid) + "u); if (!sg.dense) ++cnt; ";
     s << "    case " << pg.prog_begin << "u: {\n"
       << "#pragma unroll 1\n"
       << "      for (int v = 0; v < " << V / 2 << "; ++v) {\n"
       << "        const u32 tp = tl0 + v * " << 2 * T << "u + 2u * me;\n"
-      << "        u64 sfP[2][" << NE << "]; u32 cdP[2][" << NE << "]; bool okP[2][" << NE << "];\n"
       << "#pragma unroll\n"
-      << "        for (int h = 0; h < 2; ++h) {\n"
-      << "#pragma unroll\n"
-      << "          for (int k = 0; k < " << NE << "; ++k) okP[h][k] = false;\n"
-      << "          const u32 t = tp + h;\n"
-      << "          const bool valid = t < sg.n_tuples;\n"
-      << "          u32 rem = valid ? t : 0u;\n"
-      << "          W r[" << MAPC_NREG << "];\n";
-    for (int l = (int)pg.n_levels - 1; l >= 0; --l)
-      s << "          { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
-        << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
-    s << "          const u32 qb = fdiv(rem, sg.tid_div);\n"
-      << "          const u32 tidv = rem - qb * sg.tid_div.d;\n"
-      << "          const u32 lbv = sg.lb0 + qb;\n"
-      << "          r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
-      << "          bool act = true;\n"
-      << "#define EMIT_SITE(K, IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
-         "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
-         "sfP[h][K] = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
-         "cdP[h][K] = tidv | ((~tidv & (u32)TMASK) << " << ch.lay.w_tid << "u) | ((u32)(KIND) << "
-      << 2 * ch.lay.w_tid << "u); okP[h][K] = true; }\n"
-      << program_body(pg.ops, u32, true)
-      << "#undef EMIT_SITE\n"
-      << "          (void)act;\n"
-      << "        }\n"
-      << "#pragma unroll\n"
-      << "        for (int k = 0; k < " << ne << "; ++k) {\n"
-      << "          if (okP[0][k] && okP[1][k] && sfP[1][k] == sfP[0][k] + 1 && !(sfP[0][k] & 1ull)) {\n"
-      << "            atomicOr(reinterpret_cast<u64*>(keys) + (sfP[0][k] >> 1), (u64)cdP[0][k] | ((u64)cdP[1][k] << 32));\n"
-      << "          } else {\n"
-      << "            if (okP[0][k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[0][k], cdP[0][k]);\n"
-      << "            if (okP[1][k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[1][k], cdP[1][k]);\n"
-      << "          }\n"
-      << "          if (!sg.dense) cnt += (u32)okP[0][k] + (u32)okP[1][k];\n"
-      << "        }\n"
+      << "        for (int k = 0; k < " << NE << "; ++k) okP[k] = false;\n";
+    // tuple t: remember each site's cell; tuple t + 1: one red.or.b64 when the
+    // two cells are adjacent and aligned, else one red.or.b32 each
+    for (int h = 0; h < 2; ++h) {
+      s << "        {\n"
+        << "          const u32 t = tp + " << h << "u;\n"
+        << "          const bool valid = t < sg.n_tuples;\n"
+        << "          u32 rem = valid ? t : 0u;\n"
+        << "          W r[" << MAPC_NREG << "];\n"
+        << decode_tuple(pg, "          ")
+        << "          bool act = true;\n";
+      if (h == 0)
+        s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; cdP[K] = cd_; okP[K] = true; }\n";
+      else
+        s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell
+          << "if (okP[K] && sf_ == sfP[K] + 1 && !(sfP[K] & 1ull)) { "
+             "atomicOr(reinterpret_cast<u64*>(keys) + (sf_ >> 1), (u64)cdP[K] | ((u64)cd_ << 32)); okP[K] = false; } "
+             "else atomicOr(reinterpret_cast<u32*>(keys) + sf_, cd_); }\n";
+      s << program_body(pg.ops, u32, true)
+        << "#undef EMIT_SITE\n"
+        << "          (void)act;\n"
+        << "        }\n";
+    }
+    s << "#pragma unroll\n"
+      << "        for (int k = 0; k < " << ne << "; ++k)\n"
+      << "          if (okP[k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[k], cdP[k]);\n"
       << "      }\n"
       << "      break; }\n";
   };
@@ -277,13 +300,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         << "        const bool valid = t < sg.n_tuples;\n"
         << "        u32 rem = valid ? t : 0u;\n"
         << "        W r[" << MAPC_NREG << "];\n";
-      for (int l = (int)pg.n_levels - 1; l >= 0; --l)
-        s << "        { const u32 q = fdiv(rem, sg.trip_div[" << l << "]); r[" << MAPC_REG_K0 + l
-          << "] = (W)(rem - q * sg.trip_div[" << l << "].d); rem = q; }\n";
-      s << "        const u32 qb = fdiv(rem, sg.tid_div);\n"
-        << "        const u32 tidv = rem - qb * sg.tid_div.d;\n"
-        << "        const u32 lbv = sg.lb0 + qb;\n"
-        << "        r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = (W)(sg.b0 + qb);\n"
+      s << decode_tuple(pg, "        ")
         << "        bool act = true;\n"
         << "        u32 e = 0;\n"
         << program_body(pg.ops, u32)
@@ -324,7 +341,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "    case " << i << ": {\n"
         << "    const Seg sg = {" << g.tuple_begin << "ull, " << g.n_tuples << "ull, " << g.tile_begin << "ull, "
         << g.key_begin << "ull, " << g.key_hi << "ull, " << g.prog_begin << "u, " << g.prog_end << "u, " << g.n_levels
-        << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, 0u, {";
+        << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, " << g.tid_inner << "u, {";
       for (int l = 0; l < 8; ++l) s << (l ? ", " : "") << fd(g.trip_div[l]);
       s << "}, " << fd(g.tid_div) << "};\n";
       tile_body(s);
@@ -438,7 +455,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         int n_sms, cudaStream_t s) {
+                         unsigned long long* tile_ctr, int n_sms, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
   int occ = 1;
@@ -447,7 +464,7 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
   const unsigned long long capb = (unsigned long long)n_sms * occ;
   const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
-                  (void*)&cap, (void*)&target};
+                  (void*)&cap, (void*)&target, (void*)&tile_ctr};
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 

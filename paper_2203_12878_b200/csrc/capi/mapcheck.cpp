@@ -239,6 +239,7 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
           s.lb0 = (uint32_t)(b - b_lo);
           s.n_emits = g.n_emits;
           s.dense = g.dense ? 1 : 0;
+          s.tid_inner = g.tid_inner ? 1 : 0;
           for (uint32_t l = 0; l < g.n_levels; ++l) s.trip_div[l] = mapc::make_fastdiv((uint32_t)g.trips[l]);
           s.tid_div = mapc::make_fastdiv((uint32_t)B);
           ch.total_tuples += s.n_tuples;
@@ -696,7 +697,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         m = begin(MAP_K_DIRECT);
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, segs, (int)ch.segs.size(), ch.total_tiles,
-                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, s));
+                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms,
+                                s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
@@ -714,7 +716,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         st_acc.launches[MAP_K_OTHER]++;
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
-                                &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, s));
+                                &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, MAPC_MAX_EMITS, 0, MAPC_MODE_FILTER, nullptr, ch.cell_bytes, s));
@@ -728,7 +730,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       m = begin(MAP_K_GENERATE);
       if (gen_mode == 1)
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_KEYS], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n,
-                              &ctrl->err, L.cap, nullptr, n_sms, s));
+                              &ctrl->err, L.cap, nullptr, &ctrl->tile_ctr, n_sms, s));
       else
         CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                 n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, s));
@@ -1143,7 +1145,7 @@ size_t map_debug_dump(const map_program* p, char* buf, size_t cap) {
       out += "instance " + std::to_string(i) + " phase " + std::to_string(in.phase) + " group " + std::to_string(g) +
              " levels " + std::to_string(G.n_levels) + " trips";
       for (uint32_t l = 0; l < G.n_levels; ++l) out += " " + std::to_string(G.trips[l]);
-      out += std::string(G.dense ? " dense" : "") + " emits " + std::to_string(G.n_emits) + "\n";
+      out += std::string(G.dense ? " dense" : "") + (G.tid_inner ? " tid_inner" : "") + " emits " + std::to_string(G.n_emits) + "\n";
       for (const MapcOp& op : G.ops) {
         const uint32_t c = op.code & MAPC_CODE_MASK;
         out += "  r" + std::to_string(op.dst) + " = " + (c <= VM_NOP ? names[c] : "?") + " ";
@@ -1171,7 +1173,9 @@ size_t map_debug_jit_source(const map_program* cp, uint64_t chunk_max_accesses, 
   if (!p || ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap(p)) != MAP_OK) return 0;
   if (chunk >= p->plan.chunks.size()) return 0;
   std::vector<mapj::JitChunk> one{p->plan.chunks[chunk].jit};
-  const std::string src = mapj::module_source(one, p->C.u32_mode, MAPC_MODE_KEYS, 4);
+  const char* mode_env = getenv("MAPC_DEBUG_JIT_MODE");          // 0 keys, 1 direct, 2 filter
+  const uint32_t mode = mode_env ? (uint32_t)atoi(mode_env) : MAPC_MODE_KEYS;
+  const std::string src = mapj::module_source(one, p->C.u32_mode, mode, p->plan.chunks[chunk].cell_bytes);
   put_diag(src, out, cap);
   return src.size();
 }

@@ -36,6 +36,8 @@ uint32_t fastdiv_apply(uint32_t n, const MapcFastDiv& f) {
 
 namespace {
 
+void choose_tuple_order(GroupProg* g, uint64_t n_threads);   // defined below (coalescing heuristic)
+
 using u128 = unsigned __int128;
 constexpr uint64_t kU64 = ~0ull;
 
@@ -752,6 +754,7 @@ struct Builder {
         if (!Lw.run(tmpl, &g)) continue;
         if (!g.has_emit && !Lw.has_fault_) continue;
         if (Lw.max_value() >= (1ull << 32)) C.u32_mode = false;
+        choose_tuple_order(&g, C.n_threads);
         info.bound_per_block = checked((u128)info.bound_per_block + (u128)g.tuples_per_block * std::max<uint32_t>(g.n_emits, 0),
                                        "access bound");
         C.total_ops += (uint32_t)g.ops.size();
@@ -762,6 +765,87 @@ struct Builder {
     if (!info.groups.empty()) C.inst.push_back(std::move(info));
   }
 };
+
+// ---- tuple order (coalescing) ------------------------------------------------
+// Concrete evaluation of a group program for one tuple on the host (64-bit
+// naturals; the interval analysis already proved the device's width exact).
+// Records the index of every EMIT whose guard holds, in site order (-1 = no emit).
+void eval_sites(const GroupProg& g, uint64_t tid, uint64_t bid, const uint64_t* k, std::vector<int64_t>* out) {
+  uint64_t r[MAPC_NREG] = {};
+  r[MAPC_REG_TID] = tid;
+  r[MAPC_REG_BID] = bid;
+  for (uint32_t l = 0; l < g.n_levels; ++l) r[MAPC_REG_K0 + l] = k[l];
+  bool act = true;
+  out->clear();
+  for (const MapcOp& op : g.ops) {
+    const uint32_t c = op.code & MAPC_CODE_MASK;
+    const uint64_t A = (op.code & MAPC_A_IMM) ? op.imm : r[op.a];
+    const uint64_t B = (op.code & MAPC_B_IMM) ? op.imm : r[op.b];
+    uint64_t v = 0;
+    switch (c) {
+      case VM_ADD: v = A + B; break;
+      case VM_SUB: v = A > B ? A - B : 0; break;
+      case VM_MUL: v = A * B; break;
+      case VM_DIV: v = B ? A / B : 0; break;
+      case VM_MOD: v = B ? A % B : 0; break;
+      case VM_SHL: v = B >= 64 ? 0 : A << B; break;
+      case VM_SHR: v = B >= 64 ? 0 : A >> B; break;
+      case VM_MIN: v = std::min(A, B); break;
+      case VM_MAX: v = std::max(A, B); break;
+      case VM_BAND: v = A & op.imm; break;
+      case VM_EQ: v = A == B; break;
+      case VM_NE: v = A != B; break;
+      case VM_LT: v = A < B; break;
+      case VM_LE: v = A <= B; break;
+      case VM_GT: v = A > B; break;
+      case VM_GE: v = A >= B; break;
+      case VM_LAND: v = (A != 0) && (B != 0); break;
+      case VM_LOR: v = (A != 0) || (B != 0); break;
+      case VM_LNOT: v = A == 0; break;
+      case VM_TRIP: {
+        const uint64_t st = (op.aux & MAPC_AUX_CONST) ? (op.aux & ~MAPC_AUX_CONST) : r[op.aux];
+        const uint64_t sp = B > A ? B - A : 0;
+        v = sp == 0 ? 0 : (st <= 1 ? sp : (sp - 1) / st + 1);
+        break;
+      }
+      case VM_MADK: v = A + r[op.aux] * B; break;
+      case VM_MOVI: v = op.imm; break;
+      case VM_ACT: act = A != 0; continue;
+      case VM_EMIT: out->push_back(act ? (int64_t)A : -1); continue;
+      default: continue;
+    }
+    r[op.dst] = v;
+  }
+}
+
+// Sectors (32 B of u32 cells) touched by one warp of 32 consecutive tuples at a
+// few positions of block 0's tuple space, per site, summed.
+uint64_t warp_sectors(const GroupProg& g, uint64_t n_threads, bool tid_inner) {
+  const uint64_t n = g.tuples_per_block;
+  uint64_t total = 0;
+  std::vector<int64_t> idx;
+  for (int pos = 1; pos <= 3; ++pos) {
+    const uint64_t t0 = (n * pos / 4) / 32 * 32;
+    std::vector<std::set<int64_t>> sec(g.n_emits);
+    for (uint64_t t = t0; t < std::min(n, t0 + 32); ++t) {
+      uint64_t rem = t, tid, k[MAPC_MAX_LEVELS] = {};
+      if (tid_inner) { tid = rem % n_threads; rem /= n_threads; }
+      for (int l = (int)g.n_levels - 1; l >= 0; --l) { k[l] = rem % g.trips[l]; rem /= g.trips[l]; }
+      if (!tid_inner) tid = rem % n_threads;
+      eval_sites(g, tid, 0, k, &idx);
+      for (size_t e = 0; e < idx.size() && e < sec.size(); ++e)
+        if (idx[e] >= 0) sec[e].insert(idx[e] >> 3);
+    }
+    for (auto& s : sec) total += s.size();
+  }
+  return total;
+}
+
+void choose_tuple_order(GroupProg* g, uint64_t n_threads) {
+  g->tid_inner = false;
+  if (g->n_levels == 0 || n_threads == 1 || !g->has_emit) return;
+  g->tid_inner = warp_sectors(*g, n_threads, true) < warp_sectors(*g, n_threads, false);
+}
 
 }  // namespace
 

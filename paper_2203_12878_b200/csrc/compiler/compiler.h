@@ -36,6 +36,11 @@ struct GroupProg {
   bool has_emit = false;
   Interval index;                         // hull of emitted index values
   uint64_t tuples_per_block = 0;          // blockDim * prod(trips)
+  // Tuple order within a block: false = innermost loop fastest (tid above the
+  // loops), true = tid fastest (loops above tid).  Chosen so that 32
+  // consecutive tuples (a warp) touch the fewest 32-byte sectors of cells
+  // (choose_tuple_order); any order enumerates the same accesses.
+  bool tid_inner = false;
 };
 
 struct InstanceInfo {

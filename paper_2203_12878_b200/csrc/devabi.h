@@ -90,7 +90,7 @@ struct MapcSeg {
   uint32_t lb0;                       // local block index of b0 in the chunk layout
   uint32_t n_emits;                   // EMIT ops in the program (max keys per tuple)
   uint32_t dense;                     // 1: every tuple emits exactly n_emits keys
-  uint32_t pad;
+  uint32_t tid_inner;                 // tuple order: 1 = tid fastest, 0 = innermost loop fastest
   MapcFastDiv trip_div[MAPC_MAX_LEVELS];  // innermost level last
   MapcFastDiv tid_div;                // blockDim
 };
@@ -141,6 +141,7 @@ struct MapcCtrl {
   MapcFastDiv rng_div;                      // divides a key position by rng_L
   unsigned long long nf;                    // direct detect: keys of the witness cell re-emitted (filter mode)
   unsigned long long wit_sf;                // direct detect: cell whose witness is folded (UINT64_MAX = none)
+  unsigned long long tile_ctr;              // direct generate: dynamic tile counter (tiles past the first wave)
 };
 
 // Per-chunk result copied out by the last kernel of the chunk.

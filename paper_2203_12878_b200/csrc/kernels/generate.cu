@@ -73,16 +73,26 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
       const uint32_t t = tl0 + v * T + me;
       valid[v] = t < sg.n_tuples;
       uint32_t rem = valid[v] ? t : 0u;
+      // mixed radix: (block, tid, k_0..k_{L-1}) with k_{L-1} fastest, or
+      // (block, k_0..k_{L-1}, tid) with tid fastest (sg.tid_inner)
+      if (sg.tid_inner) {
+        const uint32_t q = fastdiv(rem, sg.tid_div);
+        tidv[v] = rem - q * sg.tid_div.d;
+        rem = q;
+      }
       for (int l = (int)L - 1; l >= 0; --l) {
         const uint32_t q = fastdiv(rem, sg.trip_div[l]);
         RG(MAPC_REG_K0 + l, v) = (W)(rem - q * sg.trip_div[l].d);
         rem = q;
       }
-      const uint32_t q = fastdiv(rem, sg.tid_div);
-      tidv[v] = rem - q * sg.tid_div.d;
+      if (!sg.tid_inner) {
+        const uint32_t q = fastdiv(rem, sg.tid_div);
+        tidv[v] = rem - q * sg.tid_div.d;
+        rem = q;
+      }
       RG(MAPC_REG_TID, v) = (W)tidv[v];
-      RG(MAPC_REG_BID, v) = (W)(sg.b0 + q);
-      lbv[v] = sg.lb0 + q;
+      RG(MAPC_REG_BID, v) = (W)(sg.b0 + rem);
+      lbv[v] = sg.lb0 + rem;
       act[v] = true;
     }
     uint32_t cnt = 0, e = 0;
