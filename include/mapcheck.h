@@ -29,6 +29,10 @@
  *    at least map_scratch_bytes() bytes (PyTorch allocates it) and a CUDA
  *    stream; the library never cudaMallocs on the hot path.  All work is
  *    enqueued on that stream; map_check_races synchronizes it once at the end.
+ *    The overlapped direct-address pipeline additionally runs the table scans
+ *    on one library-owned side stream per program (created at first use,
+ *    destroyed by map_program_free), ordered by events and joined back into
+ *    the caller's stream before the run ends.
  *  - There is no CPU fallback: without a usable CUDA device the run entry
  *    points return MAP_E_CUDA.
  */

@@ -455,12 +455,13 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         unsigned long long* tile_ctr, int n_sms, cudaStream_t s) {
+                         unsigned long long* tile_ctr, int n_sms, int max_ctas_per_sm, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
   if (occ < 1) occ = 1;
+  if (max_ctas_per_sm > 0 && occ > max_ctas_per_sm) occ = max_ctas_per_sm;
   const unsigned long long capb = (unsigned long long)n_sms * occ;
   const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,

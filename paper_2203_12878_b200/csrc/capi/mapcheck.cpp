@@ -34,9 +34,9 @@ cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long 
                                  unsigned long long* keys, MapcCtrl* ctrl, int n_sms, uint32_t nreg,
                                  uint32_t max_emits, uint32_t force_compact, uint32_t mode, void* tab,
                                  uint32_t cell_bytes, cudaStream_t s);
-cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, cudaStream_t s);
+cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm, cudaStream_t s);
 cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
-                                    MapcCtrl* ctrl, int n_sms, cudaStream_t s);
+                                    MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s);
 cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
 cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t w_tid,
                                      unsigned long long cap, cudaStream_t s);
@@ -105,6 +105,7 @@ struct Chunk {
   uint64_t cells = 0;                       // 2^S
   uint32_t cell_bytes = 4;                  // 4 if 2 w_tid + 1 <= 32, else 8
   bool direct_ok = false;                   // the table is cheap enough and fits the scratch plan
+  size_t dev_segs = 0;                      // offset of this chunk's segment table in the all-chunks region
 };
 
 struct Plan {
@@ -114,6 +115,8 @@ struct Plan {
   mapj::JitHandle jit[3];
   size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
   size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
+  size_t off_ctrl2 = 0;                     // second control block (overlapped direct pipeline)
+  size_t off_allsegs = 0;                   // every chunk's segment table (overlapped direct pipeline)
   size_t max_segs = 0;
   // scratch offsets
   size_t off_a = 0, off_b = 0, off_lb = 0, off_ff = 0, off_lf = 0, off_segs = 0, off_ctrl = 0, off_res = 0, off_rh = 0;
@@ -140,8 +143,16 @@ struct map_program {
   int device = -1;
   std::string last_error;
   std::vector<cudaEvent_t> events;   // pool for per-kernel timing
+  // overlapped direct pipeline: a library-owned side stream (scan, clear and
+  // witness of chunk k run there while chunk k+1's generate runs on the caller's
+  // stream) and its ordering events
+  cudaStream_t side = nullptr;
+  int side_dev = -1;
+  std::vector<cudaEvent_t> sync_events;
   ~map_program() {
     for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (cudaEvent_t e : sync_events) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -370,6 +381,12 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_tparts = off; off += align_up((size_t)2 * out.table_ctas * sizeof(MapcTablePart));
   out.off_tstore = off; off += align_up((size_t)2 * out.table_ctas * MAPC_TABLE_WORDS * 4);
   out.off_gate = off; off += align_up(64);
+  out.off_ctrl2 = off; off += align_up(sizeof(MapcCtrl));
+  out.off_allsegs = off;
+  for (auto& ch : out.chunks) {
+    ch.dev_segs = off - out.off_allsegs;
+    off += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg));
+  }
   out.dtab_bytes = dtab;
   if (dtab <= kcap * 8) {
     out.off_dtab = out.off_b;                 // the direct path never touches key buffer B
@@ -674,10 +691,116 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   auto end = [&](size_t e1) {
     if (prof) cudaEventRecord(p->events[e1], s);
   };
+  auto begin_on = [&](int kind, cudaStream_t st) -> size_t {   // same, on another stream
+    ++launches;
+    st_acc.launches[kind]++;
+    if (!prof) return 0;
+    cudaEventRecord(p->events[ev], st);
+    marks.push_back({kind, ev, ev + 1});
+    ev += 2;
+    return ev - 1;
+  };
+  auto end_on = [&](size_t e1, cudaStream_t st) {
+    if (prof) cudaEventRecord(p->events[e1], st);
+  };
   uint64_t h2d = 0;
   CK(cudaEventRecord(p->events[0], s));
   CK(cudaMemsetAsync(gate, 0xFF, sizeof(uint32_t), s));
+  // Overlapped direct pipeline: the direct generate is bound
+  // by L2 atomics, not HBM, so chunk k's table scan + clear and witness run on a
+  // library-owned side stream while chunk k+1's generate runs on the caller's
+  // stream (two tables inside key buffer B, two control blocks, every chunk's
+  // segment table resident).  The generate leaves room on every SM for the
+  // side kernels' CTAs.  MAPC_OVERLAP=0 restores the sequential pipeline.
+  static const int ovl_env = [] { const char* e = getenv("MAPC_OVERLAP"); return e ? atoi(e) : 1; }();
+  static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 11; }();
+  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 2; }();
+  const size_t tab_stride = align_up(P.dtab_bytes);
+  bool ovl = ovl_env != 0 && gen_mode == 1 && mine.size() >= 2 && P.off_dtab == P.off_b &&
+             2 * tab_stride <= P.cap * 8;
+  for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags);
+  if (ovl) {
+    if (!p->side || p->side_dev != ex->device) {
+      if (p->side) cudaStreamDestroy(p->side);
+      p->side = nullptr;
+      CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+      p->side_dev = ex->device;
+    }
+    while (p->sync_events.size() < 5) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p->sync_events.push_back(e);
+    }
+    cudaStream_t s2 = p->side;
+    cudaEvent_t ev_gen[2] = {p->sync_events[0], p->sync_events[1]};
+    cudaEvent_t ev_done[2] = {p->sync_events[2], p->sync_events[3]};
+    cudaEvent_t ev_join = p->sync_events[4];
+    auto* ctrl2 = (MapcCtrl*)(base + P.off_ctrl2);
+    for (size_t c : mine) {
+      const Chunk& ch = P.chunks[c];
+      CK(cudaMemcpyAsync(base + P.off_allsegs + ch.dev_segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg),
+                         cudaMemcpyHostToDevice, s));
+      h2d += ch.segs.size() * sizeof(MapcSeg);
+    }
+    CK(cudaEventRecord(ev_join, s));                  // the side stream starts after the gate reset and uploads
+    CK(cudaStreamWaitEvent(s2, ev_join, 0));
+    for (size_t i = 0; i < mine.size(); ++i) {
+      const size_t c = mine[i];
+      const Chunk& ch = P.chunks[c];
+      const MapcLayout L = effective_layout(ch, ex->flags);
+      const int b = (int)(i & 1);
+      MapcCtrl* cb = b ? ctrl2 : ctrl;
+      unsigned char* tb = dtab + b * tab_stride;
+      auto* sg = (MapcSeg*)(base + P.off_allsegs + ch.dev_segs);
+      const uint64_t tbytes = ch.cells * ch.cell_bytes;
+      if (i >= 2) CK(cudaStreamWaitEvent(s, ev_done[b], 0));   // chunk i-2 released table b and ctrl b
+      size_t m = begin(MAP_K_OTHER);
+      CK(mapc_launch_chunk_init(cb, ch.dense_total, s));
+      end(m);
+      if (i < 2) {                                     // first use of table b in this run
+        m = begin(MAP_K_CLEAR);
+        CK(mapc_launch_table_clear(tb, tbytes, n_sms, 0, s));
+        end(m);
+      }
+      if (ch.total_tiles) {
+        m = begin(MAP_K_DIRECT);
+        CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, sg, (int)ch.segs.size(), ch.total_tiles,
+                              (unsigned long long*)tb, &cb->n, &cb->err, L.cap, &cb->wit_sf, &cb->tile_ctr, n_sms,
+                              ovl_gen_ctas, s));
+        end(m);
+      }
+      CK(cudaEventRecord(ev_gen[b], s));
+      CK(cudaStreamWaitEvent(s2, ev_gen[b], 0));
+      // scan, then clear table b when chunk i+2 uses it again (a scan that also
+      // zeroes the cells it read was measured 2.5x slower: profiles/r1k_*)
+      m = begin_on(MAP_K_DETECT, s2);
+      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, ovl_side_ctas, s2));
+      end_on(m, s2);
+      if (i + 2 < mine.size()) {
+        m = begin_on(MAP_K_CLEAR, s2);
+        CK(mapc_launch_table_clear(tb, tbytes, n_sms, ovl_side_ctas, s2));
+        end_on(m, s2);
+      }
+      m = begin_on(MAP_K_OTHER, s2);
+      launches += 2;
+      st_acc.launches[MAP_K_OTHER] += 2;
+      CK(mapc_launch_witness_gate(cb, gate, ch.phase_lo, ch.phase_hi, s2));
+      if (ch.total_tiles) {
+        ++launches;
+        st_acc.launches[MAP_K_OTHER]++;
+        CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, sg, (int)ch.segs.size(), ch.total_tiles, bufA, &cb->nf,
+                              &cb->err, L.cap, &cb->wit_sf, &cb->tile_ctr, n_sms, 0, s2));
+      }
+      CK(mapc_launch_witness_flat(bufA, cb, L.pay_bits, L.w_tid, L.cap, s2));
+      CK(mapc_launch_chunk_finish(cb, 0, res + c, s2));
+      end_on(m, s2);
+      CK(cudaEventRecord(ev_done[b], s2));
+    }
+    CK(cudaEventRecord(ev_join, s2));                 // join the side stream back into the caller's
+    CK(cudaStreamWaitEvent(s, ev_join, 0));
+  }
   for (size_t c : mine) {
+    if (ovl) break;
     const Chunk& ch = P.chunks[c];
     const MapcLayout L = effective_layout(ch, ex->flags);
     CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
@@ -691,21 +814,20 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       // access into its cell, scan the table, re-emit the witness cell's keys
       const uint64_t tbytes = ch.cells * ch.cell_bytes;
       m = begin(MAP_K_CLEAR);
-      CK(mapc_launch_table_clear(dtab, tbytes, n_sms, s));
+      CK(mapc_launch_table_clear(dtab, tbytes, n_sms, 0, s));
       end(m);
       if (ch.total_tiles) {
         m = begin(MAP_K_DIRECT);
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, segs, (int)ch.segs.size(), ch.total_tiles,
-                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms,
-                                s));
+                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, 0, s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
         end(m);
       }
       m = begin(MAP_K_DETECT);
-      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, s));
+      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s));
       end(m);
       m = begin(MAP_K_OTHER);
       launches += 2;
@@ -716,7 +838,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         st_acc.launches[MAP_K_OTHER]++;
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
-                                &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, s));
+                                &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, 0, s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, MAPC_MAX_EMITS, 0, MAPC_MODE_FILTER, nullptr, ch.cell_bytes, s));
@@ -730,7 +852,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       m = begin(MAP_K_GENERATE);
       if (gen_mode == 1)
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_KEYS], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n,
-                              &ctrl->err, L.cap, nullptr, &ctrl->tile_ctr, n_sms, s));
+                              &ctrl->err, L.cap, nullptr, &ctrl->tile_ctr, n_sms, 0, s));
       else
         CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                 n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, s));

@@ -24,7 +24,7 @@
 
 namespace mapk {
 
-constexpr int DS_THREADS = 256;
+constexpr int DS_THREADS = 128;
 
 template <typename C>
 __device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
@@ -35,7 +35,7 @@ __device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
 // Grid-stride over 16-byte vectors of cells, DS_UNROLL vectors in flight per
 // thread; each thread's first racy cell is its smallest (indices increase
 // along the stride).  The common all-clean vector costs a few ALU ops per cell.
-constexpr int DS_UNROLL = 4;
+constexpr int DS_UNROLL = 8;
 template <typename C>
 __global__ void __launch_bounds__(DS_THREADS)
 k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
@@ -58,6 +58,7 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
       else
         v[u] = make_uint4(0, 0, 0, 0);
     }
+
 #pragma unroll
     for (int u = 0; u < DS_UNROLL; ++u) {
       C c[PER];
@@ -151,11 +152,14 @@ __global__ void k_table_clear(uint4* __restrict__ tab, unsigned long long n16) {
 
 }  // namespace mapk
 
-extern "C" cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, cudaStream_t s) {
+// ctas_per_sm: 0 = fill the GPU; k > 0 = k CTAs per SM (the overlapped pipeline
+// runs these next to a generate that leaves room for them).
+extern "C" cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm,
+                                               cudaStream_t s) {
   const unsigned long long n16 = (bytes + 15) / 16;
   if (n16 == 0) return cudaSuccess;
   const unsigned long long want = (n16 + 255) / 256;
-  const unsigned long long cap = (unsigned long long)n_sms * 8;
+  const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 8);
   mapk::k_table_clear<<<(int)(want < cap ? want : cap), 256, 0, s>>>((uint4*)tab, n16);
   return cudaGetLastError();
 }
@@ -167,11 +171,12 @@ extern "C" cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, 
 }
 
 extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes,
-                                               uint32_t w_tid, MapcCtrl* ctrl, int n_sms, cudaStream_t s) {
+                                               uint32_t w_tid, MapcCtrl* ctrl, int n_sms, int ctas_per_sm,
+                                               cudaStream_t s) {
   if (cells == 0) return cudaSuccess;
   const unsigned long long vec = (cells * cell_bytes + 15) / 16;
   const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
-  const unsigned long long cap = (unsigned long long)n_sms * 8;
+  const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 16);
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   if (cell_bytes == 4)
     mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
