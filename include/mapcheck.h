@@ -135,9 +135,10 @@ typedef struct {
  *                     <=> (OR tid) & (OR ~tid) != 0), the table is scanned
  *                     once, and the witness cell's keys are re-generated and
  *                     folded (sort-free).  Used for a
- *                     chunk when its table is small against its accesses
- *                     (2^S <= 8 x its key bound, or <= 1 MiB) and fits the
- *                     scratch plan; other chunks take the AUTO choice below.
+ *                     chunk when its estimated time (fixed cost + clear and
+ *                     scan of the table + per-access generate) beats the keys
+ *                     pipelines' estimate and the table fits the scratch plan
+ *                     (DESIGN.md §5.6); other chunks take the AUTO choice below.
  *   MAP_DETECT_AUTO:  DIRECT where it qualifies; otherwise TABLE when the
  *                     chunk holds >= 2^16 keys and at least 2^(S-1) of them
  *                     (dense sort-field space), else SORT.

@@ -344,17 +344,19 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.jit.lay = ch.lay;
     ch.jit.max_emits = ch.max_emits;
     if (ch.segs.size() <= 4) ch.jit.segs = ch.segs;
-    // direct-address table: 2^S cells.  Worth it when the scan of the table
-    // (8 B of HBM per u32 cell: clear + read) is small against the keys
-    // pipeline it replaces (>= 56 B per access): 2^S <= 8 * bound, or the
-    // table is tiny.  Its size is bounded by key buffer B (which it overlays)
-    // or 1 GiB.
+    // direct-address table: 2^S cells.  Worth it when its estimated time --
+    // a fixed ~25 us, the table written (clear) and read (scan) at ~6 TB/s, the
+    // generate at ~1.5 ps per access -- beats the keys pipelines' (~40 us fixed,
+    // >= ~50 ps per access at these sizes incl. their passes and launches;
+    // DESIGN.md §6, profiles/r1j_configs.jsonl).  Its size is bounded by key
+    // buffer B (which it overlays) or 1 GiB.
     const uint32_t S = ch.lay.sort_bits;
     ch.cell_bytes = 2 * ch.lay.w_tid + 1 <= 32 ? 4u : 8u;
     if (S <= 40) {
       ch.cells = 1ull << S;
       const uint64_t tb = ch.cells * ch.cell_bytes;
-      const bool cheap = ch.cells <= 8 * std::max<uint64_t>(ch.bound, 1) || tb <= (1ull << 20);
+      const double n = (double)std::max<uint64_t>(ch.bound, 1);
+      const bool cheap = 25e-6 + 2.0 * (double)tb / 6e12 + 1.5e-12 * n <= 40e-6 + 50e-12 * n;
       const bool fits = tb <= kcap * 8 || tb <= (1ull << 30);
       ch.direct_ok = cheap && fits;
       if (ch.direct_ok) dtab = std::max<size_t>(dtab, tb);

@@ -163,6 +163,7 @@ class Lowerer {
   std::map<std::tuple<uint8_t, int, int, int, uint64_t>, int> cse_;
   std::vector<int> k_;
   std::vector<int> xval_;
+  std::map<int, std::pair<int, int>> relv_;   // cond id -> (lhs, rhs) value ids of its last evaluation
   int tid_ = -1, bid_ = -1, act_ = -1, vm_act_ = -1;
   bool empty_ = false;
   uint64_t trips_[MAPC_MAX_LEVELS] = {};
@@ -358,9 +359,92 @@ class Lowerer {
       case Cond::False: return konst(0);
       case Cond::And: { int l = cond(x.lhs); int r = cond(x.rhs); return land(l, r); }
       case Cond::Or: { int l = cond(x.lhs); int r = cond(x.rhs); return lor(l, r); }
-      case Cond::Rel: { int a = expr(x.lhs); int b = expr(x.rhs); return rel(x.rel, a, b); }
+      case Cond::Rel: {
+        int a = expr(x.lhs);
+        int b = expr(x.rhs);
+        relv_[c] = {a, b};
+        return rel(x.rel, a, b);
+      }
     }
     return konst(0);
+  }
+
+  // ---- guard refinement ------------------------------------------------------
+  // Inside `if (c)` every ACTIVE tuple satisfies c (inside the else branch, not
+  // c), so the intervals of the values c compares can be narrowed there: the
+  // index hull, the layout and the loop boxes of guarded code get tight (e.g.
+  // the scans' `if (k*1024 + tid < (N >> (l+1)))`).  Values computed in the
+  // branch are only used under the branch's act (EMIT and fault checks are
+  // masked, nested guards are AND-ed into act), so a value an inactive tuple
+  // computes outside its narrowed interval is never observed.  The narrowed
+  // intervals and the CSE entries created in the branch are undone on exit.
+  struct Scope {
+    std::vector<std::pair<int, Interval>> undo;
+    std::map<std::tuple<uint8_t, int, int, int, uint64_t>, int> cse;
+    bool empty = false;
+  };
+  void narrow(Scope& sc, int v, uint64_t lo, uint64_t hi) {
+    const Interval o = vals_[v].iv;
+    const uint64_t nl = std::max(o.lo, lo), nh = std::min(o.hi, hi);
+    if (nl > nh) { sc.empty = true; return; }
+    if (nl == o.lo && nh == o.hi) return;
+    if (isc(v)) return;                              // a constant inside its bounds
+    sc.undo.push_back({v, o});
+    vals_[v].iv = {nl, nh};
+  }
+  void refine(Scope& sc, int c, bool pos) {
+    const Cond& x = P_.conds[c];
+    switch (x.kind) {
+      case Cond::True: case Cond::False: return;
+      case Cond::And: if (pos) { refine(sc, x.lhs, true); refine(sc, x.rhs, true); } return;
+      case Cond::Or: if (!pos) { refine(sc, x.lhs, false); refine(sc, x.rhs, false); } return;
+      case Cond::Rel: {
+        auto it = relv_.find(c);
+        if (it == relv_.end()) return;
+        int a = it->second.first, b = it->second.second;
+        RelOp r = x.rel;
+        if (!pos) {
+          switch (r) {
+            case RelOp::Lt: r = RelOp::Ge; break;
+            case RelOp::Le: r = RelOp::Gt; break;
+            case RelOp::Gt: r = RelOp::Le; break;
+            case RelOp::Ge: r = RelOp::Lt; break;
+            case RelOp::Eq: r = RelOp::Ne; break;
+            case RelOp::Ne: r = RelOp::Eq; break;
+          }
+        }
+        if (r == RelOp::Gt) { std::swap(a, b); r = RelOp::Lt; }
+        if (r == RelOp::Ge) { std::swap(a, b); r = RelOp::Le; }
+        const Interval A = iv(a), B = iv(b);
+        switch (r) {
+          case RelOp::Lt:                              // a < b
+            if (B.hi == 0) { sc.empty = true; return; }
+            narrow(sc, a, 0, B.hi - 1);
+            if (A.lo == kU64) { sc.empty = true; return; }
+            narrow(sc, b, A.lo + 1, kU64);
+            return;
+          case RelOp::Le:                              // a <= b
+            narrow(sc, a, 0, B.hi);
+            narrow(sc, b, A.lo, kU64);
+            return;
+          case RelOp::Eq:
+            narrow(sc, a, B.lo, B.hi);
+            narrow(sc, b, A.lo, A.hi);
+            return;
+          default: return;
+        }
+      }
+    }
+  }
+  Scope open_scope(int c, bool pos) {
+    Scope sc;
+    sc.cse = cse_;
+    refine(sc, c, pos);
+    return sc;
+  }
+  void close_scope(Scope& sc) {
+    for (auto it = sc.undo.rbegin(); it != sc.undo.rend(); ++it) vals_[it->first].iv = it->second;
+    cse_ = std::move(sc.cse);
   }
 
   // ------------------------------------------------------------- fault scan
@@ -439,9 +523,17 @@ class Lowerer {
         if (!rel) return;
         int saved = act_;
         act_ = land(saved, c);
-        walk(st.then_s, d);
+        {
+          Scope sc = open_scope(st.cond, true);
+          if (!sc.empty) walk(st.then_s, d);
+          close_scope(sc);
+        }
         act_ = land(saved, lnot(c));
-        walk(st.else_s, d);
+        {
+          Scope sc = open_scope(st.cond, false);
+          if (!sc.empty) walk(st.else_s, d);
+          close_scope(sc);
+        }
         act_ = saved;
         return;
       }

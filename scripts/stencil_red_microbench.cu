@@ -68,6 +68,62 @@ k_stencil_packed(unsigned long long* tab, uint32_t R, uint32_t C, uint32_t H, ui
   }
 }
 
+// Same as k_stencil (no hints) but every CTA walks a CONTIGUOUS block of the
+// pair space (blocked instead of grid-stride tile order).
+__global__ void __launch_bounds__(128, 12)
+k_stencil_blocked(unsigned long long* tab, uint32_t R, uint32_t C, uint32_t H, uint64_t half, uint64_t n_pairs) {
+  const uint32_t C2 = C / 2;
+  const uint64_t per_cta = (n_pairs + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = blockIdx.x * per_cta, hi = min(n_pairs, lo + per_cta);
+  for (uint64_t t = lo + threadIdx.x; t < hi; t += blockDim.x) {
+    const uint32_t c2 = (uint32_t)(t % C2);
+    const uint32_t r = (uint32_t)((t / C2) % R);
+    const uint32_t tid = (uint32_t)(t / ((uint64_t)C2 * R));
+    const uint32_t row = tid * R + r;
+    const uint64_t code = tid | ((~tid & 1023u) << 10);
+    const unsigned long long v = code | (code << 32);
+    const unsigned long long w = v | (1ull << 20) | (1ull << 52);
+    atomicOr(tab + (((uint64_t)((row + H - 1) % H) * C) >> 1) + c2, v);
+    atomicOr(tab + (((uint64_t)row * C) >> 1) + c2, v);
+    atomicOr(tab + (((uint64_t)((row + 1) % H) * C) >> 1) + c2, v);
+    atomicOr(tab + ((half + (uint64_t)row * C) >> 1) + c2, w);
+  }
+}
+
+// k_stencil + L2 prefetch of the cells DIST grid-strides ahead
+template <int DIST>
+__global__ void __launch_bounds__(128, 12)
+k_stencil_pf(unsigned long long* tab, uint32_t R, uint32_t C, uint32_t H, uint64_t half, uint64_t n_pairs) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t C2 = C / 2;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_pairs; t += stride) {
+    {
+      const uint64_t tp = t + DIST * stride;
+      if (tp < n_pairs) {
+        const uint32_t c2 = (uint32_t)(tp % C2);
+        const uint32_t r = (uint32_t)((tp / C2) % R);
+        const uint32_t tid = (uint32_t)(tp / ((uint64_t)C2 * R));
+        const uint32_t row = tid * R + r;
+        if ((c2 & 15) == 0) {   // one prefetch per 128-B line
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(tab + (((uint64_t)((row + 1) % H) * C) >> 1) + c2));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(tab + ((half + (uint64_t)row * C) >> 1) + c2));
+        }
+      }
+    }
+    const uint32_t c2 = (uint32_t)(t % C2);
+    const uint32_t r = (uint32_t)((t / C2) % R);
+    const uint32_t tid = (uint32_t)(t / ((uint64_t)C2 * R));
+    const uint32_t row = tid * R + r;
+    const uint64_t code = tid | ((~tid & 1023u) << 10);
+    const unsigned long long v = code | (code << 32);
+    const unsigned long long w = v | (1ull << 20) | (1ull << 52);
+    atomicOr(tab + (((uint64_t)((row + H - 1) % H) * C) >> 1) + c2, v);
+    atomicOr(tab + (((uint64_t)row * C) >> 1) + c2, v);
+    atomicOr(tab + (((uint64_t)((row + 1) % H) * C) >> 1) + c2, v);
+    atomicOr(tab + ((half + (uint64_t)row * C) >> 1) + c2, w);
+  }
+}
+
 int main() {
   const uint32_t R = 256, C = 1024, H = 1024 * R;
   const uint64_t cells_max = (2ull << 28) + 8192;
@@ -111,6 +167,36 @@ int main() {
       if (rep && ms < best) best = ms;
     }
     printf("%-26s %.3f ms per 2^30 accesses (%.1f G acc/s)\n", "packed 3 x 21 bits", best, 1073741824.0 / best / 1e6);
+  }
+  {
+    float best = 1e9;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaMemset(tab, 0, cells_max * 4);
+      cudaEventRecord(e0);
+      k_stencil_blocked<<<148 * 12, 128>>>(tab, R, C, H, 1ull << 28, n_pairs);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep && ms < best) best = ms;
+    }
+    printf("%-26s %.3f ms per 2^30 accesses (%.1f G acc/s)\n", "blocked CTA ranges", best, 1073741824.0 / best / 1e6);
+  }
+  for (int dist : {1, 2, 4}) {
+    float best = 1e9;
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaMemset(tab, 0, cells_max * 4);
+      cudaEventRecord(e0);
+      if (dist == 1) k_stencil_pf<1><<<148 * 12, 128>>>(tab, R, C, H, 1ull << 28, n_pairs);
+      if (dist == 2) k_stencil_pf<2><<<148 * 12, 128>>>(tab, R, C, H, 1ull << 28, n_pairs);
+      if (dist == 4) k_stencil_pf<4><<<148 * 12, 128>>>(tab, R, C, H, 1ull << 28, n_pairs);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep && ms < best) best = ms;
+    }
+    printf("prefetch L2 %d strides ahead  %.3f ms per 2^30 accesses (%.1f G acc/s)\n", dist, best, 1073741824.0 / best / 1e6);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
