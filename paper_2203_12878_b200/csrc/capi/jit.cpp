@@ -146,7 +146,30 @@ struct Module {
 };
 
 std::mutex g_mu;
-std::map<std::string, Module> g_cache;   // source text -> loaded module (process-wide)
+std::map<std::string, Module> g_cache;   // chunk_key -> loaded module (process-wide)
+
+// Everything the generated source depends on, as raw bytes (cheaper than
+// generating the source text to look a module up: e2e runs recompile per step).
+template <typename T>
+void put(std::string& k, const T& v) { k.append(reinterpret_cast<const char*>(&v), sizeof(T)); }
+std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell_bytes) {
+  std::string k;
+  put(k, u32);
+  put(k, mode);
+  put(k, cell_bytes);
+  put(k, ch.lay);
+  put(k, ch.max_emits);
+  put(k, ch.programs.size());
+  for (const JitProgram& pg : ch.programs) {
+    put(k, pg.prog_begin);
+    put(k, pg.n_levels);
+    put(k, pg.ops.size());
+    k.append(reinterpret_cast<const char*>(pg.ops.data()), pg.ops.size() * sizeof(MapcOp));
+  }
+  put(k, ch.segs.size());
+  k.append(reinterpret_cast<const char*>(ch.segs.data()), ch.segs.size() * sizeof(MapcSeg));
+  return k;
+}
 
 // Mixed-radix decode of the tuple index `rem` (in scope) into r[tid], r[bid],
 // r[k_l], tidv, lbv: (block, tid, k_0..k_{L-1}) with k_{L-1} fastest, or tid
@@ -394,19 +417,19 @@ int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string*
   return 0;
 }
 
-// One NVRTC program per chunk, compiled in parallel; modules cached by source.
+// One NVRTC program per chunk, compiled in parallel; modules cached by chunk_key.
 int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
                  JitHandle* out, std::string* log) {
   const size_t nc = chunks.size();
-  std::vector<std::string> srcs(nc);
-  for (size_t i = 0; i < nc; ++i)
-    srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
+  std::vector<std::string> keys(nc), srcs(nc);
+  for (size_t i = 0; i < nc; ++i) keys[i] = chunk_key(chunks[i], u32, mode, cell_bytes[i]);
   std::vector<int> need;
   {
     std::lock_guard<std::mutex> g(g_mu);
     for (size_t i = 0; i < nc; ++i)
-      if (!g_cache.count(srcs[i])) need.push_back((int)i);
+      if (!g_cache.count(keys[i])) need.push_back((int)i);
   }
+  for (int i : need) srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
   std::vector<std::vector<char>> cubins(nc);
   std::vector<std::string> logs(nc);
   std::vector<int> rc(nc, 0);
@@ -426,7 +449,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
   std::lock_guard<std::mutex> g(g_mu);
   out->kernels.assign(nc, nullptr);
   for (size_t i = 0; i < nc; ++i) {
-    auto it = g_cache.find(srcs[i]);
+    auto it = g_cache.find(keys[i]);
     if (it == g_cache.end()) {
       if (rc[i] != 0) {
         *log = logs[i];
@@ -445,7 +468,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
         return 1;
       }
       m.kernels.push_back(k);
-      it = g_cache.emplace(srcs[i], std::move(m)).first;
+      it = g_cache.emplace(keys[i], std::move(m)).first;
     }
     out->kernels[i] = it->second.kernels[0];
   }

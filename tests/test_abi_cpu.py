@@ -114,3 +114,23 @@ def test_no_cpu_fallback():
     with pytest.raises(mc.MapError) as e:
         p.check_races()
     assert e.value.status == 6
+
+
+def test_guard_refinement_tightens_layouts():
+    # Inside `if (k*1024 + tid < (N >> (l+1)))` the compiler narrows k*1024 + tid, so the
+    # Blelloch scan's indices (1 << l)*(2*(k*1024+tid)+1) - 1 stay below N = 2^20: the sort
+    # field is phase + 20 index bits, not the bounding box's 2^30-wide hull.
+    inst = config("4c")
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    info = p.chunk_info(0)
+    assert info["sort_bits"] <= 6 + 20
+    # the unguarded stencil keeps its exact 29-bit index field
+    inst = config("5a")
+    assert mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).chunk_info(0)["sort_bits"] == 29
+
+
+def test_guard_refinement_unreachable_branch():
+    # a guard that no tuple satisfies (tid < 64 and tid >= 64) leaves no access behind it
+    p = mc.MapProgram("if (tid < 64) { if (tid >= 64) { wr[tid] } else { skip } } else { skip }; rd[0]",
+                      (1, 1, 1), (128, 1, 1), {})
+    assert p.info.max_accesses == 128
