@@ -775,8 +775,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       CK(cudaStreamWaitEvent(s2, ev_gen[b], 0));
       // scan, then clear table b when chunk i+2 uses it again (a scan that also
       // zeroes the cells it read was measured 2.5x slower: profiles/r1k_*)
+      // the last chunk's scan has no generate to share the GPU with: full grid
+      const bool last = i + 1 == mine.size();
       m = begin_on(MAP_K_DETECT, s2);
-      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, ovl_side_ctas, s2));
+      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
       end_on(m, s2);
       if (i + 2 < mine.size()) {
         m = begin_on(MAP_K_CLEAR, s2);
