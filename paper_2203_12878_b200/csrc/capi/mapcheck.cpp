@@ -298,6 +298,11 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       const uint64_t nlo = std::min(ilo, ph[j].ilo), nhi = std::max(ihi, ph[j].ihi);
       if (!layout_fits(C, ph[j].phase - ph[i].phase, G, nlo, nhi, &L)) break;
       if (ops + ph[j].ops > MAPC_MAX_OPS) break;
+      // Keep the direct-address table of a chunk L2-sized (<= 64 MiB of u32
+      // cells) once the chunk is big enough to amortise its fixed cost (>= 2^23
+      // accesses): the table's atomics then mostly hit L2 (4a: 92 -> 121 G acc/s,
+      // profiles/r1n_chunking.jsonl).
+      if (j > i && acc >= (1ull << 23) && L.sort_bits >= 24) break;
       acc += (uint64_t)nb;
       ilo = nlo; ihi = nhi; ops += ph[j].ops;
       Lok = L;
@@ -623,7 +628,12 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // generate path: NVRTC-specialised kernels for large plans (compile cost
   // amortised), the bytecode VM otherwise (map_exec.flags, MAP_GEN_*).
   const uint32_t gsel = ex->flags & 3u;
-  const int gen_mode = gsel == MAP_GEN_VM ? 0 : gsel == MAP_GEN_JIT ? 1 : (p->C.max_accesses >= (1ull << 26) ? 1 : 0);
+  // (AUTO: the NVRTC compile is amortised only over large chunks -- plans of
+  // >= 2^26 accesses in at most 64 chunks; a plan cut into thousands of small
+  // chunks would compile thousands of kernels)
+  const int gen_mode = gsel == MAP_GEN_VM    ? 0
+                       : gsel == MAP_GEN_JIT ? 1
+                                             : (p->C.max_accesses >= (1ull << 26) && P.chunks.size() <= 64 ? 1 : 0);
   if (gen_mode == 1 && !P.chunks.empty()) {
     // the modes this run needs: keys (sort / table detect), direct + filter (direct detect)
     bool need[3] = {false, false, false};

@@ -72,7 +72,21 @@ def test_full_size_plans():
     assert p.info.max_accesses == 2**34
     assert p.info.u32_mode
     assert p.n_chunks() == 16
-    assert p.n_chunks(2**31) == 8
+    # a larger capacity does not merge phases: two phases would double the
+    # direct-address table of a chunk (4 GiB) for no saving per access
+    assert p.n_chunks(2**31) == 16
+
+
+def test_plans_keep_direct_tables_l2_sized():
+    # Hillis-Steele scan (20 phases x ~3M accesses): once a chunk holds >= 2^23 accesses
+    # it is closed before its table would reach 2^24 cells (64 MiB of u32 cells)
+    inst = config("4a")
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    infos = [p.chunk_info(c) for c in range(p.n_chunks())]
+    assert len(infos) > 1
+    assert all(i["sort_bits"] < 24 for i in infos)
+    assert sum(i["phase_hi"] - i["phase_lo"] + 1 for i in infos) == p.info.n_phases - 1 or \
+        sum(i["phase_hi"] - i["phase_lo"] + 1 for i in infos) == p.info.n_phases
 
 
 @pytest.mark.parametrize("src,status", [
