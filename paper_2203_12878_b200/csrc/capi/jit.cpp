@@ -215,6 +215,13 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // keys staged per thread per tile for compaction: the guarded segments' emits
   // (keys mode), every segment's (filter mode), none (direct mode)
   const bool paired = mode == MAPC_MODE_DIRECT && cell_bytes == 4;
+  // Direct mode: every CTA walks a contiguous block of tiles (instead of a grid
+  // stride), so the cells a CTA re-touches (stencil rows r-1, r, r+1) stay in L2
+  // between its tiles: the table's DRAM traffic drops to the algorithmic read +
+  // write of every cell (profiles/r1k_stencil_red_microbench.txt), which leaves
+  // HBM bandwidth to the overlapped scans.  MAPC_BLOCKED_TILES=0 restores the stride.
+  static const bool blocked_env = [] { const char* e = getenv("MAPC_BLOCKED_TILES"); return !(e && e[0] == '0'); }();
+  const bool blocked = mode == MAPC_MODE_DIRECT && blocked_env;
   const uint32_t stage_emits = V * (mode == MAPC_MODE_DIRECT   ? 1u
                                     : mode == MAPC_MODE_FILTER ? (uint32_t)MAPC_MAX_EMITS
                                                                : std::max(1u, ch.max_emits));
@@ -245,7 +252,10 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
   s
-    << "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n"
+    << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
+                  "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
+                  "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
+                : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n")
     << "    int lo = 0, hi = n_segs - 1;\n"
     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
     ;
