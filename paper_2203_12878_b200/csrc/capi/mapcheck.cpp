@@ -756,6 +756,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     }
     CK(cudaEventRecord(ev_join, s));                  // the side stream starts after the gate reset and uploads
     CK(cudaStreamWaitEvent(s2, ev_join, 0));
+    // the second table's first clear runs on the side stream under chunk 0's generate
+    {
+      const Chunk& c1 = P.chunks[mine[1]];
+      size_t m = begin_on(MAP_K_CLEAR, s2);
+      CK(mapc_launch_table_clear(dtab + tab_stride, c1.cells * c1.cell_bytes, n_sms, ovl_side_ctas, s2));
+      end_on(m, s2);
+      CK(cudaEventRecord(ev_done[1], s2));
+    }
     for (size_t i = 0; i < mine.size(); ++i) {
       const size_t c = mine[i];
       const Chunk& ch = P.chunks[c];
@@ -769,11 +777,12 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       size_t m = begin(MAP_K_OTHER);
       CK(mapc_launch_chunk_init(cb, ch.dense_total, s));
       end(m);
-      if (i < 2) {                                     // first use of table b in this run
+      if (i == 0) {                                    // first use of table 0 in this run
         m = begin(MAP_K_CLEAR);
         CK(mapc_launch_table_clear(tb, tbytes, n_sms, 0, s));
         end(m);
       }
+      if (i == 1) CK(cudaStreamWaitEvent(s, ev_done[1], 0));   // table 1 cleared on the side stream
       if (ch.total_tiles) {
         m = begin(MAP_K_DIRECT);
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, sg, (int)ch.segs.size(), ch.total_tiles,
