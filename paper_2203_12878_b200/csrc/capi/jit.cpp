@@ -163,6 +163,8 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   for (const JitProgram& pg : ch.programs) {
     put(k, pg.prog_begin);
     put(k, pg.n_levels);
+    put(k, pg.pair_nocarry);
+    put(k, pg.tid_inner);
     put(k, pg.ops.size());
     k.append(reinterpret_cast<const char*>(pg.ops.data()), pg.ops.size() * sizeof(MapcOp));
   }
@@ -285,14 +287,38 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       << "        for (int k = 0; k < " << NE << "; ++k) okP[k] = false;\n";
     // tuple t: remember each site's cell; tuple t + 1: one red.or.b64 when the
     // two cells are adjacent and aligned, else one red.or.b32 each
+    // With an even innermost range, tuple t + 1 is tuple t with the innermost
+    // coordinate + 1 (tp is even): its coordinates are copied, not decoded, so
+    // NVRTC shares every value of the program that does not depend on that
+    // coordinate between the two tuples.
+    const bool nocarry = pg.pair_nocarry;
+    const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
+    if (nocarry)
+      s << "        bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n";
     for (int h = 0; h < 2; ++h) {
       s << "        {\n"
-        << "          const u32 t = tp + " << h << "u;\n"
-        << "          const bool valid = t < sg.n_tuples;\n"
-        << "          u32 rem = valid ? t : 0u;\n"
-        << "          W r[" << MAPC_NREG << "];\n"
-        << decode_tuple(pg, "          ")
-        << "          bool act = true;\n";
+        << "          const u32 t = tp + " << h << "u;\n";
+      if (h == 1 && nocarry) {
+        s << "          const bool valid = valid0_;\n"
+          << "          W r[" << MAPC_NREG << "];\n"
+          << "          const u32 tidv = tidv0_" << (tid_is_inner ? " + 1u" : "") << ";\n"
+          << "          const u32 lbv = lbv0_;\n"
+          << "          r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = bid0_;\n";
+        for (uint32_t l = 0; l < pg.n_levels; ++l)
+          s << "          r[" << MAPC_REG_K0 + l << "] = c0_[" << l << "]"
+            << (!tid_is_inner && l + 1 == pg.n_levels ? " + (W)1" : "") << ";\n";
+        s << "          (void)t;\n";
+      } else {
+        s << "          const bool valid = t < sg.n_tuples;\n"
+          << "          u32 rem = valid ? t : 0u;\n"
+          << "          W r[" << MAPC_NREG << "];\n"
+          << decode_tuple(pg, "          ");
+        if (h == 0 && nocarry) {
+          s << "          valid0_ = valid; tidv0_ = tidv; lbv0_ = lbv; bid0_ = r[" << MAPC_REG_BID << "];\n";
+          for (uint32_t l = 0; l < pg.n_levels; ++l) s << "          c0_[" << l << "] = r[" << MAPC_REG_K0 + l << "];\n";
+        }
+      }
+      s << "          bool act = true;\n";
       if (h == 0)
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; cdP[K] = cd_; okP[K] = true; }\n";
       else

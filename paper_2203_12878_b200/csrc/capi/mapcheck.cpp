@@ -214,7 +214,13 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
       const mapc::InstanceInfo& in = C.inst[ii];
       for (const mapc::GroupProg& g : in.groups) {
         const uint32_t pb = (uint32_t)ch.ops.size();
-        ch.jit.programs.push_back(mapj::JitProgram{pb, g.n_levels, g.ops});
+        {
+          mapj::JitProgram jp{pb, g.n_levels, g.ops};
+          const uint64_t inner = (g.tid_inner || g.n_levels == 0) ? B : g.trips[g.n_levels - 1];
+          jp.pair_nocarry = inner % 2 == 0;
+          jp.tid_inner = g.tid_inner;
+          ch.jit.programs.push_back(std::move(jp));
+        }
         for (const MapcOp& op : g.ops) {
           ch.ops.push_back(lower_op_for_mode(op, C.u32_mode));
           const uint32_t code = op.code & MAPC_CODE_MASK;
@@ -726,7 +732,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // side kernels' CTAs.  MAPC_OVERLAP=0 restores the sequential pipeline.
   static const int ovl_env = [] { const char* e = getenv("MAPC_OVERLAP"); return e ? atoi(e) : 1; }();
   static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 12; }();
-  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 2; }();
+  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 3; }();
   const size_t tab_stride = align_up(P.dtab_bytes);
   bool ovl = ovl_env != 0 && gen_mode == 1 && mine.size() >= 2 && P.off_dtab == P.off_b &&
              2 * tab_stride <= P.cap * 8;
