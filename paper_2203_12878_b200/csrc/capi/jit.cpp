@@ -235,7 +235,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (minb > 0) s << ", " << minb;
   s << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
-       "u64 cap, const u64* target_ptr, u64* tile_ctr) {\n"
+       "u64 cap, const u64* target_ptr) {\n"
     << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
     << "  typedef " << (cell_bytes == 4 ? "u32" : "u64") << " CELL;\n"
     << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
@@ -243,7 +243,6 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
     << "  __shared__ u64 s_base;\n"
-    << "  (void)tile_ctr;\n"
     << "  const int me = threadIdx.x;\n"
     << "  u32 err = 0;\n"
     << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
@@ -514,7 +513,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         unsigned long long* tile_ctr, int n_sms, int max_ctas_per_sm, cudaStream_t s) {
+                         int n_sms, int max_ctas_per_sm, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
   int occ = 1;
@@ -524,7 +523,7 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
   const unsigned long long capb = (unsigned long long)n_sms * occ;
   const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
-                  (void*)&cap, (void*)&target, (void*)&tile_ctr};
+                  (void*)&cap, (void*)&target};
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 

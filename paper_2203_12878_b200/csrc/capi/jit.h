@@ -43,6 +43,6 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         unsigned long long* tile_ctr, int n_sms, int max_ctas_per_sm, cudaStream_t s);
+                         int n_sms, int max_ctas_per_sm, cudaStream_t s);
 
 }  // namespace mapj

@@ -792,7 +792,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       if (ch.total_tiles) {
         m = begin(MAP_K_DIRECT);
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, sg, (int)ch.segs.size(), ch.total_tiles,
-                              (unsigned long long*)tb, &cb->n, &cb->err, L.cap, &cb->wit_sf, &cb->tile_ctr, n_sms,
+                              (unsigned long long*)tb, &cb->n, &cb->err, L.cap, &cb->wit_sf, n_sms,
                               ovl_gen_ctas, s));
         end(m);
       }
@@ -818,7 +818,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         ++launches;
         st_acc.launches[MAP_K_OTHER]++;
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, sg, (int)ch.segs.size(), ch.total_tiles, bufA, &cb->nf,
-                              &cb->err, L.cap, &cb->wit_sf, &cb->tile_ctr, n_sms, 0, s2));
+                              &cb->err, L.cap, &cb->wit_sf, n_sms, 0, s2));
       }
       CK(mapc_launch_witness_flat(bufA, cb, L.pay_bits, L.w_tid, L.cap, s2));
       CK(mapc_launch_chunk_finish(cb, 0, res + c, s2));
@@ -849,7 +849,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         m = begin(MAP_K_DIRECT);
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, segs, (int)ch.segs.size(), ch.total_tiles,
-                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, 0, s));
+                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
@@ -867,7 +867,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         st_acc.launches[MAP_K_OTHER]++;
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
-                                &ctrl->err, L.cap, &ctrl->wit_sf, &ctrl->tile_ctr, n_sms, 0, s));
+                                &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, MAPC_MAX_EMITS, 0, MAPC_MODE_FILTER, nullptr, ch.cell_bytes, s));
@@ -881,7 +881,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       m = begin(MAP_K_GENERATE);
       if (gen_mode == 1)
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_KEYS], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->n,
-                              &ctrl->err, L.cap, nullptr, &ctrl->tile_ctr, n_sms, 0, s));
+                              &ctrl->err, L.cap, nullptr, n_sms, 0, s));
       else
         CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                 n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, s));

@@ -141,7 +141,6 @@ struct MapcCtrl {
   MapcFastDiv rng_div;                      // divides a key position by rng_L
   unsigned long long nf;                    // direct detect: keys of the witness cell re-emitted (filter mode)
   unsigned long long wit_sf;                // direct detect: cell whose witness is folded (UINT64_MAX = none)
-  unsigned long long tile_ctr;              // direct generate: dynamic tile counter (tiles past the first wave)
 };
 
 // Per-chunk result copied out by the last kernel of the chunk.
