@@ -454,15 +454,16 @@ int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string*
 
 // One NVRTC program per chunk, compiled in parallel; modules cached by chunk_key.
 int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
-                 JitHandle* out, std::string* log) {
+                 const std::vector<char>& want, JitHandle* out, std::string* log) {
   const size_t nc = chunks.size();
   std::vector<std::string> keys(nc), srcs(nc);
-  for (size_t i = 0; i < nc; ++i) keys[i] = chunk_key(chunks[i], u32, mode, cell_bytes[i]);
+  for (size_t i = 0; i < nc; ++i)
+    if (want[i]) keys[i] = chunk_key(chunks[i], u32, mode, cell_bytes[i]);
   std::vector<int> need;
   {
     std::lock_guard<std::mutex> g(g_mu);
     for (size_t i = 0; i < nc; ++i)
-      if (!g_cache.count(keys[i])) need.push_back((int)i);
+      if (want[i] && !g_cache.count(keys[i])) need.push_back((int)i);
   }
   for (int i : need) srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
   std::vector<std::vector<char>> cubins(nc);
@@ -482,8 +483,9 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
     for (auto& t : pool) t.join();
   }
   std::lock_guard<std::mutex> g(g_mu);
-  out->kernels.assign(nc, nullptr);
+  if (out->kernels.size() != nc) out->kernels.assign(nc, nullptr);
   for (size_t i = 0; i < nc; ++i) {
+    if (!want[i]) continue;
     auto it = g_cache.find(keys[i]);
     if (it == g_cache.end()) {
       if (rc[i] != 0) {

@@ -37,9 +37,10 @@ struct JitHandle {
 std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes);
 std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, uint32_t cell_bytes);
 int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log);
-// Compile (or fetch from the process-wide cache) one kernel per chunk for one mode.
+// Compile (or fetch from the process-wide cache) the kernels of the chunks with
+// want[i] != 0 for one mode; out->kernels has one entry per chunk (null = not built).
 int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
-                 JitHandle* out, std::string* log);
+                 const std::vector<char>& want, JitHandle* out, std::string* log);
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,

@@ -111,8 +111,7 @@ struct Chunk {
 struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
-  bool jit_ready[3] = {false, false, false};   // per generate mode (MAPC_MODE_*)
-  mapj::JitHandle jit[3];
+  mapj::JitHandle jit[3];                    // per generate mode (MAPC_MODE_*); null = not built yet
   size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
   size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
   size_t off_ctrl2 = 0;                     // second control block (overlapped direct pipeline)
@@ -640,12 +639,25 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   const int gen_mode = gsel == MAP_GEN_VM    ? 0
                        : gsel == MAP_GEN_JIT ? 1
                                              : (p->C.max_accesses >= (1ull << 26) && P.chunks.size() <= 64 ? 1 : 0);
-  if (gen_mode == 1 && !P.chunks.empty()) {
-    // the modes this run needs: keys (sort / table detect), direct + filter (direct detect)
-    bool need[3] = {false, false, false};
-    for (auto& ch : P.chunks) {
-      if (use_direct(ch, ex->flags)) need[MAPC_MODE_DIRECT] = need[MAPC_MODE_FILTER] = true;
-      else need[MAPC_MODE_KEYS] = true;
+  const uint32_t world = ex->world ? ex->world : 1;
+  const uint32_t rank = ex->rank;
+  if (rank >= world) return MAP_E_ARG;
+  std::vector<size_t> mine;          // this rank's chunks (multi-GPU: c % world == rank)
+  for (size_t c = 0; c < P.chunks.size(); ++c)
+    if (c % world == rank) mine.push_back(c);
+  if (gen_mode == 1 && !mine.empty()) {
+    // the kernels this run needs, per mode: keys (sort / table detect), direct +
+    // filter (direct detect), for this rank's chunks only
+    std::vector<char> want[3];
+    bool any[3] = {false, false, false};
+    for (uint32_t m = 0; m < 3; ++m) want[m].assign(P.chunks.size(), 0);
+    for (size_t c : mine) {
+      const bool d = use_direct(P.chunks[c], ex->flags);
+      for (uint32_t m = 0; m < 3; ++m) {
+        const bool w = d ? m != MAPC_MODE_KEYS : m == MAPC_MODE_KEYS;
+        const bool have = P.jit[m].kernels.size() == P.chunks.size() && P.jit[m].kernels[c] != nullptr;
+        if (w && !have) { want[m][c] = 1; any[m] = true; }
+      }
     }
     std::vector<mapj::JitChunk> jc;
     std::vector<uint32_t> cb;
@@ -657,16 +669,15 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     std::string logs[3];
     int rcs[3] = {0, 0, 0};
     for (uint32_t m = 0; m < 3; ++m)
-      if (need[m] && !P.jit_ready[m])
-        builders.emplace_back([&, m]() { rcs[m] = mapj::build_module(jc, p->C.u32_mode, m, cb, &P.jit[m], &logs[m]); });
+      if (any[m])
+        builders.emplace_back(
+            [&, m]() { rcs[m] = mapj::build_module(jc, p->C.u32_mode, m, cb, want[m], &P.jit[m], &logs[m]); });
     for (auto& t : builders) t.join();
-    for (uint32_t m = 0; m < 3; ++m) {
+    for (uint32_t m = 0; m < 3; ++m)
       if (rcs[m] != 0) {
         p->last_error = "specialised generate: " + logs[m];
         return MAP_E_CUDA;
       }
-      if (need[m]) P.jit_ready[m] = true;
-    }
   }
   uint32_t passes_total = 0;
   for (auto& ch : P.chunks) passes_total += effective_layout(ch, ex->flags).n_passes;
@@ -678,12 +689,6 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     p->last_lookback = lookback;
     p->device = ex->device;
   }
-  const uint32_t world = ex->world ? ex->world : 1;
-  const uint32_t rank = ex->rank;
-  if (rank >= world) return MAP_E_ARG;
-  std::vector<size_t> mine;
-  for (size_t c = 0; c < P.chunks.size(); ++c)
-    if (c % world == rank) mine.push_back(c);
   // events: 2 per timed launch group + 2 for the whole run
   const bool prof = ex->stats != nullptr;
   size_t need_ev = 2 + (prof ? mine.size() * (2 * (8 + MAPC_MAX_PASSES)) : 0);
