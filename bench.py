@@ -316,6 +316,15 @@ def main():
     roofline = kernel_roofline(kern, dominant, peak, peak_kind)
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
     pipe_bytes = sum(v["bytes"] for v in kern.values())
+    # the dominant kernel alone: the direct path's chunks run one after another
+    # (MAP_EXEC_SEQUENTIAL), so its CUDA-event time is not shared with the
+    # overlapped scans (reported next to the live, overlapped figure)
+    if dominant == "direct" and kern.get("direct", {}).get("launches"):
+        solo = [prog.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank,
+                                 world=world, profile=True, detect=args.detect, overlap=False) for _ in range(2)]
+        r_solo = kernel_roofline(kernel_table(solo[1:]), "direct", peak, peak_kind)
+        roofline["solo"] = {"achieved": r_solo["achieved"], "frac": r_solo["frac"],
+                            "note": "same kernel, chunks run sequentially (no concurrent scans)"}
     kernels_out = {k: {"ms_per_step": v["ms"] / len(results), "share": v["ms"] / kern_total,
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,
                        "launches_per_step": v["launches"] / len(results)} for k, v in kern.items()}

@@ -150,6 +150,11 @@ typedef struct {
 #define MAP_DETECT_DIRECT 0x40u
 #define MAP_DETECT_MASK 0x70u
 
+/* MAP_EXEC_SEQUENTIAL (map_exec.flags): run the direct path's chunks one after
+ * another on the caller's stream only (no side stream: each chunk's clear,
+ * generate and scan in turn) -- for measuring the kernels alone; same results. */
+#define MAP_EXEC_SEQUENTIAL 0x100u
+
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */
   int32_t n_chunks;           /* chunks this call processed                          */

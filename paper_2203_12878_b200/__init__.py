@@ -64,6 +64,7 @@ class _Exec(ctypes.Structure):
 
 GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
 DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40}   # MAP_DETECT_* (include/mapcheck.h)
+EXEC_SEQUENTIAL = 0x100                                                       # MAP_EXEC_SEQUENTIAL
 
 
 class _Result(ctypes.Structure):
@@ -324,14 +325,16 @@ class MapProgram:
 
     def check_races(self, scratch=None, stream=None, chunk_max_accesses: int = 0, device: Optional[int] = None,
                     rank: int = 0, world: int = 1, profile: bool = False, gen: str = "auto",
-                    detect: str = "auto") -> Result:
+                    detect: str = "auto", overlap: bool = True) -> Result:
         """Run generate -> sort -> detect on one GPU (blocking).
 
         scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
         stream: a torch.cuda.Stream (default: the current stream);
         rank/world: process only chunks c with c % world == rank (multi-GPU sharding);
         profile: record CUDA events around every launch and return per-kernel-class timings;
-        gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised)."""
+        gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised);
+        detect: "auto" | "direct" | "table" | "sort" (include/mapcheck.h MAP_DETECT_*);
+        overlap: False = MAP_EXEC_SEQUENTIAL (the direct path's chunks one after another)."""
         import torch
         if not torch.cuda.is_available():
             raise MapError(6, "no CUDA device (there is no CPU fallback)")
@@ -344,7 +347,8 @@ class MapProgram:
         stats = _Stats() if profile else None
         ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
                    scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
-                   ctypes.pointer(stats) if stats is not None else None, GEN_PATHS[gen] | DETECT_PATHS[detect])
+                   ctypes.pointer(stats) if stats is not None else None,
+                   GEN_PATHS[gen] | DETECT_PATHS[detect] | (0 if overlap else EXEC_SEQUENTIAL))
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:

@@ -739,7 +739,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 12; }();
   static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 3; }();
   const size_t tab_stride = align_up(P.dtab_bytes);
-  bool ovl = ovl_env != 0 && gen_mode == 1 && mine.size() >= 2 && P.off_dtab == P.off_b &&
+  bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
+             P.off_dtab == P.off_b &&
              2 * tab_stride <= P.cap * 8;
   for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags);
   if (ovl) {
