@@ -413,3 +413,22 @@ def test_direct_paired_cells(src, params):
     o = oracle.check(src, block=(64, 1, 1), grid=(3, 1, 1), params=params)
     for gen in ("jit", "vm"):
         same(mc.check(src, block=(64, 1, 1), grid=(3, 1, 1), params=params, detect="direct", gen=gen), o)
+
+
+@pytest.mark.parametrize("name,sizes", [("5a", dict(T=6, R=4, C=64)), ("5b", dict(T=5, R=4, C=64)),
+                                        ("4b", dict(n=1 << 14, bs=256))])
+def test_overlapped_and_sequential_direct_pipelines_agree(name, sizes):
+    # the overlapped direct pipeline (side stream, two tables, two control blocks)
+    # and MAP_EXEC_SEQUENTIAL give the oracle's result, also with every rank share
+    inst = config(name, **sizes)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    o = oracle.check_instance(inst)
+    unit = max(1, p.info.max_unit_accesses)
+    for overlap in (True, False):
+        same(p.check_races(gen="jit", detect="direct", chunk_max_accesses=unit, overlap=overlap), o)
+    # a 3-way shard: the ranks' counts add up and their witnesses' minimum is the oracle's
+    parts = [p.check_races(gen="jit", detect="direct", chunk_max_accesses=unit, rank=r, world=3) for r in range(3)]
+    assert sum(x.n_accesses for x in parts) == o.n_accesses
+    assert sum(x.racy_segments for x in parts) == o.n_racy_segments
+    wits = [x.witness.as_tuple() for x in parts if x.witness]
+    assert (min(wits) if wits else None) == o.witness
