@@ -247,8 +247,11 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  u32 err = 0;\n"
     << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
     << "  (void)TMASK; (void)target_ptr;\n";
+  // sort fields below 2^31 (5a: 29 bits): 32-bit cell arithmetic in the paired case
+  const bool sf32 = ch.lay.sort_bits <= 31;
   if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
-    s << "  u64 sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS << "]; bool okP[" << MAPC_MAX_EMITS << "];\n";
+    s << "  " << (sf32 ? "u32" : "u64") << " sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS
+      << "]; bool okP[" << MAPC_MAX_EMITS << "];\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
@@ -274,8 +277,9 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     const int NE = std::max(ne, 1);
     const std::string cell =
         "const u64 idx_ = (u64)(IX) - IDX_LO; if (WI < 64 && (idx_ >> WI) != 0) err |= " +
-        std::to_string(MAPC_ERR_LAYOUT) + "u; "
-        "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
+        std::to_string(MAPC_ERR_LAYOUT) + "u; " +
+        (sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
+              : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
         "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) + "u) | ((u32)(KIND) << " +
         std::to_string(2 * ch.lay.w_tid) + "u); if (!sg.dense) ++cnt; ";
     s << "    case " << pg.prog_begin << "u: {\n"
@@ -322,7 +326,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; cdP[K] = cd_; okP[K] = true; }\n";
       else
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell
-          << "if (okP[K] && sf_ == sfP[K] + 1 && !(sfP[K] & 1ull)) { "
+          << "if (okP[K] && sf_ == sfP[K] + 1 && !(sfP[K] & 1u)) { "
              "atomicOr(reinterpret_cast<u64*>(keys) + (sf_ >> 1), (u64)cdP[K] | ((u64)cd_ << 32)); okP[K] = false; } "
              "else atomicOr(reinterpret_cast<u32*>(keys) + sf_, cd_); }\n";
       s << program_body(pg.ops, u32, true)
