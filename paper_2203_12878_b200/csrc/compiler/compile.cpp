@@ -125,10 +125,18 @@ struct SIns {
 
 class Lowerer {
  public:
+  // unroll_depth >= 0: the forU at that depth of the nest is not a tuple
+  // coordinate; its variable is the constant of iteration unroll_iter (the
+  // loop's bounds and step must be uniform constants, else unroll_failed()).
   Lowerer(const Compiled& C, const std::vector<uint64_t>& syncenv, const std::vector<bool>& sync_set,
-          const std::vector<int>& path, const std::set<int>& sites, bool fault_owner, const std::vector<int>& parent)
+          const std::vector<int>& path, const std::set<int>& sites, bool fault_owner, const std::vector<int>& parent,
+          int unroll_depth = -1, uint64_t unroll_iter = 0)
       : C_(C), P_(C.ast), syncenv_(syncenv), sync_set_(sync_set), path_(path), sites_(sites),
-        fault_owner_(fault_owner), parent_(parent) {}
+        fault_owner_(fault_owner), parent_(parent), unroll_depth_(unroll_depth), unroll_iter_(unroll_iter) {}
+
+  bool unroll_failed() const { return unroll_failed_; }
+  // constant trip count of the forU at `depth` (0 if its bounds are not uniform constants)
+  uint64_t const_trip(int depth) const { return depth < (int)const_trip_.size() ? const_trip_[depth] : 0; }
 
   // Returns false if the group has an empty tuple space.
   bool run(int tmpl, GroupProg* out) {
@@ -167,6 +175,10 @@ class Lowerer {
   int tid_ = -1, bid_ = -1, act_ = -1, vm_act_ = -1;
   bool empty_ = false;
   uint64_t trips_[MAPC_MAX_LEVELS] = {};
+  int unroll_depth_ = -1;
+  uint64_t unroll_iter_ = 0;
+  bool unroll_failed_ = false;
+  std::vector<uint64_t> const_trip_;    // per depth: trip count when lo, hi, step are constants
   uint64_t max_value_ = 0;
   Interval index_hull_{kU64, 0};
   uint32_t n_emits_ = 0;
@@ -553,6 +565,18 @@ class Lowerer {
     int lo = expr(st.lo), hi = expr(st.hi), sp = expr(st.step);
     const Interval L = iv(lo), H = iv(hi), S = iv(sp);
     if (S.lo == 0) range_error("a loop step may be zero");
+    if (const_trip_.size() <= d) const_trip_.resize(d + 1, 0);
+    if (isc(lo) && isc(hi) && isc(sp)) const_trip_[d] = trip_count(cv(lo), cv(hi), cv(sp));
+    if ((int)d == unroll_depth_) {                   // one iteration, as a constant
+      if (!(isc(lo) && isc(hi) && isc(sp))) { unroll_failed_ = true; empty_ = true; return; }
+      if (unroll_iter_ >= const_trip_[d]) { empty_ = true; return; }
+      const uint64_t xv = checked((u128)cv(lo) + (u128)unroll_iter_ * cv(sp), "loop value");
+      trips_[d] = 1;
+      xval_[st.var] = konst(xv);
+      walk(st.body, d + 1);
+      xval_[st.var] = -1;
+      return;
+    }
     // bounding-box trip count: trip is decreasing in lo and step, increasing in hi
     uint64_t tmax = trip_count(L.lo, H.hi, S.lo);
     uint64_t tmin = trip_count(L.hi, H.lo, S.hi);
@@ -650,9 +674,11 @@ class Lowerer {
     std::vector<int> reg(vals_.size(), -1);
     reg[tid_] = MAPC_REG_TID;
     reg[bid_] = MAPC_REG_BID;
-    for (int l = 0; l < L; ++l) reg[k_[l]] = MAPC_REG_K0 + l;
+    int nl = 0;                                      // tuple coordinates (the unrolled level is none)
+    for (int l = 0; l < L; ++l)
+      if (l != unroll_depth_) reg[k_[l]] = MAPC_REG_K0 + nl++;
     std::vector<int> freelist;
-    for (int r = MAPC_NREG - 1; r >= MAPC_REG_K0 + L; --r) freelist.push_back(r);
+    for (int r = MAPC_NREG - 1; r >= MAPC_REG_K0 + nl; --r) freelist.push_back(r);
     auto pinned = [&](int v) { return v == tid_ || v == bid_ || std::find(k_.begin(), k_.end(), v) != k_.end(); };
 
     std::vector<MapcOp> ops;
@@ -713,10 +739,11 @@ class Lowerer {
       ops.push_back(op);
     }
     out->ops = std::move(ops);
-    out->n_levels = (uint32_t)L;
+    out->n_levels = (uint32_t)nl;
     uint64_t tpb = C_.n_threads;
-    for (int l = 0; l < L; ++l) {
-      out->trips[l] = trips_[l];
+    for (int l = 0, j = 0; l < L; ++l) {
+      if (l == unroll_depth_) continue;
+      out->trips[j++] = trips_[l];
       tpb = checked((u128)tpb * trips_[l], "tuple count");
     }
     out->tuples_per_block = tpb;
@@ -845,13 +872,55 @@ struct Builder {
         GroupProg g;
         if (!Lw.run(tmpl, &g)) continue;
         if (!g.has_emit && !Lw.has_fault_) continue;
-        if (Lw.max_value() >= (1ull << 32)) C.u32_mode = false;
-        choose_tuple_order(&g, C.n_threads);
-        info.bound_per_block = checked((u128)info.bound_per_block + (u128)g.tuples_per_block * std::max<uint32_t>(g.n_emits, 0),
-                                       "access bound");
-        C.total_ops += (uint32_t)g.ops.size();
-        ++C.n_groups;
-        info.groups.push_back(std::move(g));
+        std::vector<GroupProg> parts;
+        std::vector<uint64_t> part_max;
+        // A sparse group -- its index hull far wider than its accesses, e.g. a
+        // loop variable in both factors of a product, which intervals cannot
+        // correlate (Blelloch down-sweep with forU levels) -- is split into one
+        // group per iteration of its outermost constant-bounds loop of <= 64
+        // iterations: each part's hull is exact for that value.
+        const unsigned __int128 acc = (unsigned __int128)g.tuples_per_block * std::max<uint32_t>(g.n_emits, 1);
+        const uint64_t span = g.has_emit && g.index.hi >= g.index.lo ? g.index.hi - g.index.lo : 0;
+        if (g.has_emit && (unsigned __int128)span > 64 * acc) {
+          for (size_t d = 0; d < p.size(); ++d) {
+            const uint64_t T = Lw.const_trip(d);
+            if (T == 0 || T > 64) continue;
+            std::vector<GroupProg> ps;
+            std::vector<uint64_t> pm;
+            uint64_t lo = ~0ull, hi = 0;
+            bool ok = true;
+            for (uint64_t u = 0; u < T && ok; ++u) {
+              Lowerer Lu(C, syncenv, sync_set, p, filt, k == 0, parent, (int)d, u);
+              GroupProg gu;
+              const bool nonempty = Lu.run(tmpl, &gu);
+              if (Lu.unroll_failed()) { ok = false; break; }
+              if (!nonempty || (!gu.has_emit && !Lu.has_fault_)) continue;
+              if (gu.has_emit) { lo = std::min(lo, gu.index.lo); hi = std::max(hi, gu.index.hi); }
+              pm.push_back(Lu.max_value());
+              ps.push_back(std::move(gu));
+            }
+            if (ok && !ps.empty() && hi >= lo && (hi - lo) < span / 4) {
+              parts = std::move(ps);
+              part_max = std::move(pm);
+            }
+            break;
+          }
+        }
+        if (parts.empty()) {
+          parts.push_back(std::move(g));
+          part_max.push_back(Lw.max_value());
+        }
+        for (size_t q = 0; q < parts.size(); ++q) {
+          GroupProg& gq = parts[q];
+          if (part_max[q] >= (1ull << 32)) C.u32_mode = false;
+          choose_tuple_order(&gq, C.n_threads);
+          info.bound_per_block = checked((u128)info.bound_per_block +
+                                             (u128)gq.tuples_per_block * std::max<uint32_t>(gq.n_emits, 0),
+                                         "access bound");
+          C.total_ops += (uint32_t)gq.ops.size();
+          ++C.n_groups;
+          info.groups.push_back(std::move(gq));
+        }
       }
     }
     if (!info.groups.empty()) C.inst.push_back(std::move(info));

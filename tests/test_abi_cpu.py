@@ -148,3 +148,14 @@ def test_guard_refinement_unreachable_branch():
     p = mc.MapProgram("if (tid < 64) { if (tid >= 64) { wr[tid] } else { skip } } else { skip }; rd[0]",
                       (1, 1, 1), (128, 1, 1), {})
     assert p.info.max_accesses == 128
+
+
+def test_sparse_group_split_by_constant_loop():
+    # Blelloch down-sweep with forU levels (4d): (N >> (l+1))*(2*(k*1024+tid)+1) - 1 couples l
+    # in two factors; the group is split per value of l, so every part's hull is exact and the
+    # whole MAP gets one dense chunk (sort field: 5 phase bits + 20 index bits)
+    inst = config("4d")
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    assert p.n_chunks() == 1
+    assert p.chunk_info(0)["sort_bits"] <= 5 + 21
+    assert p.info.max_accesses >= 9 * 2**20 - 7
