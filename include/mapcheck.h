@@ -115,7 +115,7 @@ typedef struct {
 
 /* Generate path (map_exec.flags): the bytecode VM, or kernels specialised from
  * the same bytecode with NVRTC at first use (cached per process).  AUTO picks
- * the specialised kernels for plans of >= 2^26 accesses. */
+ * the specialised kernels for plans of >= 2^23 accesses in <= 64 chunks. */
 #define MAP_GEN_AUTO 0u
 #define MAP_GEN_VM 1u
 #define MAP_GEN_JIT 2u

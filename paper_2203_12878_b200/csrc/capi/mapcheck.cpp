@@ -633,12 +633,13 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // generate path: NVRTC-specialised kernels for large plans (compile cost
   // amortised), the bytecode VM otherwise (map_exec.flags, MAP_GEN_*).
   const uint32_t gsel = ex->flags & 3u;
-  // (AUTO: the NVRTC compile is amortised only over large chunks -- plans of
-  // >= 2^26 accesses in at most 64 chunks; a plan cut into thousands of small
-  // chunks would compile thousands of kernels)
+  // (AUTO: the NVRTC compile, once per process, is amortised over plans of
+  // >= 2^23 accesses in at most 64 chunks -- 4a/4b/4d run 1.3-1.4x faster than
+  // on the VM, profiles/r1q_gen_vm_jit.jsonl; a plan cut into thousands of
+  // small chunks would compile thousands of kernels)
   const int gen_mode = gsel == MAP_GEN_VM    ? 0
                        : gsel == MAP_GEN_JIT ? 1
-                                             : (p->C.max_accesses >= (1ull << 26) && P.chunks.size() <= 64 ? 1 : 0);
+                                             : (p->C.max_accesses >= (1ull << 23) && P.chunks.size() <= 64 ? 1 : 0);
   const uint32_t world = ex->world ? ex->world : 1;
   const uint32_t rank = ex->rank;
   if (rank >= world) return MAP_E_ARG;
