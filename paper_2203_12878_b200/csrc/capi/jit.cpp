@@ -119,6 +119,12 @@ __device__ __forceinline__ u32 fdiv(u32 n, const FD& f) {
   u32 hi = __umulhi(f.m, n);
   return (hi + ((n - hi) >> 1)) >> f.s;
 }
+// Block offset (within the segment) of tuple t: t / (blockDim * prod(trips)).
+__device__ __forceinline__ u32 block_of(u32 t, const Seg& sg) {
+  u32 rem = fdiv(t, sg.tid_div);
+  for (u32 l = 0; l < sg.n_levels; ++l) rem = fdiv(rem, sg.trip_div[l]);
+  return rem;
+}
 template <int T>
 __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* tmp, u32* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -239,6 +245,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
     << "  typedef " << (cell_bytes == 4 ? "u32" : "u64") << " CELL;\n"
     << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
+    << "  const u32 WA_ = " << ch.lay.w_array << "u; (void)WA_;\n"
     << "  const u64 IDX_LO = " << ch.lay.idx_lo << "ull;\n"
     << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
@@ -343,8 +350,22 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // the per-tile body, emitted once per baked segment (fields as literals) and
   // once generic (fields loaded from segs[])
   auto tile_body = [&](std::ostringstream& s) {
-    s << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n"
-      << "    u32 cnt = 0;\n"
+    s << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n";
+    if (mode == MAPC_MODE_FILTER) {
+      // the witness cell lies in one phase and one block: tiles of other phases
+      // or whose blocks cannot contain it are skipped (uniform per CTA)
+      const uint32_t hb = ch.lay.w_array + ch.lay.w_block + ch.lay.w_index;
+      s << "    bool skip_ = false;\n";
+      if (hb < 64) s << "    skip_ = (sg.key_hi >> " << hb << "u) != (target >> " << hb << "u);\n";
+      if (ch.lay.w_block > 0)
+        s << "    if (!skip_) {\n"
+          << "      const u32 tlb_ = (u32)((target >> WI) & ((1ull << WB_) - 1ull));\n"
+          << "      const u32 tl1_ = min(tl0 + " << V * T - 1 << "u, (u32)sg.n_tuples - 1u);\n"
+          << "      skip_ = tlb_ < sg.lb0 + block_of(tl0, sg) || tlb_ > sg.lb0 + block_of(tl1_, sg);\n"
+          << "    }\n";
+      s << "    if (!skip_) {\n";
+    }
+    s << "    u32 cnt = 0;\n"
       << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
          "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
          "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
@@ -390,6 +411,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
          "if (pos < cap) keys[pos] = stage[(size_t)j * " << T << " + me]; else err |= " << MAPC_ERR_CAPACITY << "u; }\n"
       << "      __syncthreads();\n"
       << "    }\n";
+    if (mode == MAPC_MODE_FILTER) s << "    }\n";   // !skip_
   };
   auto fd = [](const MapcFastDiv& f) {
     std::ostringstream o;
