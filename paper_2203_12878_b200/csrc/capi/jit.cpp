@@ -204,8 +204,13 @@ std::string emit_tail(uint32_t mode, uint32_t w_tid, int T) {
     s << "const u64 code_ = (u64)tidv | ((~(u64)tidv & TMASK) << " << w_tid << "u) | ((u64)(KIND) << " << 2 * w_tid
       << "u); atomicOr(reinterpret_cast<CELL*>(keys) + sf_, (CELL)code_); if (!sg.dense) ++cnt;";
   } else if (mode == MAPC_MODE_FILTER) {
-    s << "if (sf_ == target) { const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
-         "stage[(size_t)cnt * " << T << " + me] = key_; ++cnt; }";
+    // matches are rare: warp-aggregated slot reservation, no staging, no CTA scan
+    s << "{ const bool hit_ = sf_ == target; const u32 hm_ = __ballot_sync(__activemask(), hit_); "
+         "if (hit_) { const u32 ln_ = me & 31u, ld_ = __ffs(hm_) - 1u; u64 b_ = 0; "
+         "if (ln_ == ld_) b_ = atomicAdd(n_ctr, (u64)__popc(hm_)); b_ = __shfl_sync(hm_, b_, ld_); "
+         "const u64 pos_ = b_ + __popc(hm_ & ((1u << ln_) - 1u)); "
+         "if (pos_ < cap) keys[pos_] = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); else err |= " << MAPC_ERR_CAPACITY
+      << "u; } }";
   } else {
     s << "const u64 key_ = (sf_ << PAY) | ((u64)tidv << 1) | (KIND); "
          "if (sg.dense) keys[sg.key_begin + (u64)e * sg.n_tuples + t] = key_; "
@@ -231,7 +236,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   static const bool blocked_env = [] { const char* e = getenv("MAPC_BLOCKED_TILES"); return !(e && e[0] == '0'); }();
   const bool blocked = mode == MAPC_MODE_DIRECT && blocked_env;
   const uint32_t stage_emits = V * (mode == MAPC_MODE_DIRECT   ? 1u
-                                    : mode == MAPC_MODE_FILTER ? (uint32_t)MAPC_MAX_EMITS
+                                    : mode == MAPC_MODE_FILTER ? 1u
                                                                : std::max(1u, ch.max_emits));
   // direct mode: minimum resident CTAs per SM (caps registers at 40): 12 measured
   // best on 5a/5b (profiles/r1j_probe_minb.jsonl, r1j_probe_dyn_minb.jsonl); MAPC_JIT_MINB overrides (0 = none)
@@ -401,7 +406,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         << "    }\n";
       return;
     }
-    s << "    if (" << (mode == MAPC_MODE_FILTER ? "true" : "!sg.dense") << ") {\n"
+    if (mode != MAPC_MODE_FILTER)   // keys mode: guarded segments compact through shared memory
+      s << "    if (!sg.dense) {\n"
       << "      u32 total;\n"
       << "      const u32 excl = block_excl_scan<" << T << ">(cnt, scan_tmp, &total);\n"
       << "      if (me == 0) s_base = total ? atomicAdd(n_ctr, (u64)total) : 0ull;\n"
