@@ -238,9 +238,10 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   const uint32_t stage_emits = V * (mode == MAPC_MODE_DIRECT   ? 1u
                                     : mode == MAPC_MODE_FILTER ? 1u
                                                                : std::max(1u, ch.max_emits));
-  // direct mode: minimum resident CTAs per SM (caps registers at 40): 12 measured
-  // best on 5a/5b (profiles/r1j_probe_minb.jsonl, r1j_probe_dyn_minb.jsonl); MAPC_JIT_MINB overrides (0 = none)
-  static const int minb_env = [] { const char* e = getenv("MAPC_JIT_MINB"); return e ? atoi(e) : 12; }();
+  // direct mode: minimum resident CTAs per SM (register cap 48): 10 measured best
+  // on 5a with the blocked, carry-free paired generate (profiles/r1q_probe_minb.txt);
+  // MAPC_JIT_MINB overrides (0 = none)
+  static const int minb_env = [] { const char* e = getenv("MAPC_JIT_MINB"); return e ? atoi(e) : 10; }();
   const int minb = mode == MAPC_MODE_DIRECT ? minb_env : 0;
   s << "extern \"C\" __global__ void __launch_bounds__(" << T;
   if (minb > 0) s << ", " << minb;
