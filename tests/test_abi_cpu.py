@@ -159,3 +159,20 @@ def test_sparse_group_split_by_constant_loop():
     assert p.n_chunks() == 1
     assert p.chunk_info(0)["sort_bits"] <= 5 + 21
     assert p.info.max_accesses >= 9 * 2**20 - 7
+
+
+def _dump(p):
+    import ctypes
+    n = mc._lib.map_debug_dump(p._h, None, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    mc._lib.map_debug_dump(p._h, buf, n + 1)
+    return [line for line in buf.value.decode().splitlines() if line.startswith("instance")]
+
+
+def test_tuple_order_choice():
+    # the compiler puts the coordinate with the unit-stride index innermost:
+    # the stencil's column loop c for 5a, tid for the scans' `k*1024 + tid`
+    for name, want in (("5a", False), ("4a", True)):
+        inst = config(name)
+        groups = _dump(mc.MapProgram(inst.src, inst.grid, inst.block, inst.params))
+        assert groups and all(("tid_inner" in g) == want for g in groups), (name, groups[:2])
