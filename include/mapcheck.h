@@ -32,7 +32,11 @@
  *    The overlapped direct-address pipeline additionally runs the table scans
  *    on one library-owned side stream per program (created at first use,
  *    destroyed by map_program_free), ordered by events and joined back into
- *    the caller's stream before the run ends.
+ *    the caller's stream before the run ends.  Without per-kernel timing
+ *    (map_exec.stats == NULL), the second identical call on a program (same
+ *    plan, flags, scratch, stream, shard) captures the run into a CUDA graph
+ *    on a library-owned capture stream and later identical calls replay it
+ *    on the caller's stream; results are the same either way.
  *  - There is no CPU fallback: without a usable CUDA device the run entry
  *    points return MAP_E_CUDA.
  */
