@@ -119,6 +119,12 @@ __device__ __forceinline__ u32 fdiv(u32 n, const FD& f) {
   u32 hi = __umulhi(f.m, n);
   return (hi + ((n - hi) >> 1)) >> f.s;
 }
+// 16-bit cell code (devabi.h code16): constant-weight 3-of-7 codewords per 5-bit tid digit
+__device__ __forceinline__ u32 cw7(u32 d) {
+  const u64 w = d < 8 ? MAPC_CW7_W0_ : d < 16 ? MAPC_CW7_W1_ : d < 24 ? MAPC_CW7_W2_ : MAPC_CW7_W3_;
+  return (u32)(w >> (7u * (d & 7u))) & 0x7Fu;
+}
+__device__ __forceinline__ u32 code16(u32 t, u32 kind) { return cw7(t & 31u) | (cw7((t >> 5) & 31u) << 7) | (kind << 14); }
 // Block offset (within the segment) of tuple t: t / (blockDim * prod(trips)).
 __device__ __forceinline__ u32 block_of(u32 t, const Seg& sg) {
   u32 rem = fdiv(t, sg.tid_div);
@@ -146,6 +152,15 @@ __device__ __forceinline__ u32 block_excl_scan(u32 v, u32* tmp, u32* total) {
 }
 )";
 
+// The prelude with the 16-bit cell code's codeword constants (devabi.h).
+std::string prelude() {
+  std::ostringstream o;
+  o << "#define MAPC_CW7_W0_ " << MAPC_CW7_W0 << "ull\n#define MAPC_CW7_W1_ " << MAPC_CW7_W1
+    << "ull\n#define MAPC_CW7_W2_ " << MAPC_CW7_W2 << "ull\n#define MAPC_CW7_W3_ " << MAPC_CW7_W3 << "ull\n"
+    << kPrelude;
+  return o.str();
+}
+
 struct Module {
   cudaLibrary_t lib = nullptr;
   std::vector<cudaKernel_t> kernels;
@@ -169,7 +184,7 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   for (const JitProgram& pg : ch.programs) {
     put(k, pg.prog_begin);
     put(k, pg.n_levels);
-    put(k, pg.pair_nocarry);
+    put(k, pg.inner_range);
     put(k, pg.tid_inner);
     put(k, pg.ops.size());
     k.append(reinterpret_cast<const char*>(pg.ops.data()), pg.ops.size() * sizeof(MapcOp));
@@ -227,7 +242,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   // keys staged per thread per tile for compaction: the guarded segments' emits
   // (keys mode), every segment's (filter mode), none (direct mode)
-  const bool paired = mode == MAPC_MODE_DIRECT && cell_bytes == 4;
+  const bool paired = mode == MAPC_MODE_DIRECT && (cell_bytes == 4 || cell_bytes == 2);
   // Direct mode: every CTA walks a contiguous block of tiles (instead of a grid
   // stride), so the cells a CTA re-touches (stencil rows r-1, r, r+1) stay in L2
   // between its tiles: the table's DRAM traffic drops to the algorithmic read +
@@ -264,7 +279,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   const bool sf32 = ch.lay.sort_bits <= 31;
   if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
     s << "  " << (sf32 ? "u32" : "u64") << " sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS
-      << "]; bool okP[" << MAPC_MAX_EMITS << "];\n";
+      << "]; bool okP[" << MAPC_MAX_EMITS << "]; u64 accP[" << MAPC_MAX_EMITS << "]; (void)cdP; (void)accP;\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
@@ -293,12 +308,27 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         std::to_string(MAPC_ERR_LAYOUT) + "u; " +
         (sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
               : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
-        "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) + "u) | ((u32)(KIND) << " +
-        std::to_string(2 * ch.lay.w_tid) + "u); if (!sg.dense) ++cnt; ";
+        (cell_bytes == 2 ? std::string("const u32 cd_ = code16(tidv, (u32)(KIND)); ")
+                         : "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) +
+                               "u) | ((u32)(KIND) << " + std::to_string(2 * ch.lay.w_tid) + "u); ") +
+        "if (!sg.dense) ++cnt; ";
+    // one cell's reduction: u32 cells are words; 16-bit cells are halves of a word
+    auto red1 = [&](const std::string& sf, const std::string& cd) {
+      return cell_bytes == 2 ? "atomicOr(reinterpret_cast<u32*>(keys) + (" + sf + " >> 1), " + cd + " << (16u * (u32)(" +
+                                   sf + " & 1u)));"
+                             : "atomicOr(reinterpret_cast<u32*>(keys) + " + sf + ", " + cd + ");";
+    };
+    // an aligned pair of adjacent cells: one 64-bit word of u32 cells, one 32-bit word of 16-bit cells
+    const std::string red2 =
+        cell_bytes == 2 ? "atomicOr(reinterpret_cast<u32*>(keys) + (sf_ >> 1), cdP[K] | (cd_ << 16));"
+                        : "atomicOr(reinterpret_cast<u64*>(keys) + (sf_ >> 1), (u64)cdP[K] | ((u64)cd_ << 32));";
+    // G consecutive tuples per thread: pairs of u32 cells (one red.or.b64), or
+    // quads of 16-bit cells (one red.or.b64 over four cells)
+    const int G = cell_bytes == 2 ? 4 : 2;
     s << "    case " << pg.prog_begin << "u: {\n"
       << "#pragma unroll 1\n"
-      << "      for (int v = 0; v < " << V / 2 << "; ++v) {\n"
-      << "        const u32 tp = tl0 + v * " << 2 * T << "u + 2u * me;\n"
+      << "      for (int v = 0; v < " << V / G << "; ++v) {\n"
+      << "        const u32 tp = tl0 + v * " << G * T << "u + " << G << "u * me;\n"
       << "#pragma unroll\n"
       << "        for (int k = 0; k < " << NE << "; ++k) okP[k] = false;\n";
     // tuple t: remember each site's cell; tuple t + 1: one red.or.b64 when the
@@ -307,22 +337,22 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     // coordinate + 1 (tp is even): its coordinates are copied, not decoded, so
     // NVRTC shares every value of the program that does not depend on that
     // coordinate between the two tuples.
-    const bool nocarry = pg.pair_nocarry;
+    const bool nocarry = pg.inner_range % (uint64_t)G == 0;
     const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
     if (nocarry)
       s << "        bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n";
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < G; ++h) {
       s << "        {\n"
         << "          const u32 t = tp + " << h << "u;\n";
-      if (h == 1 && nocarry) {
+      if (h >= 1 && nocarry) {
         s << "          const bool valid = valid0_;\n"
           << "          W r[" << MAPC_NREG << "];\n"
-          << "          const u32 tidv = tidv0_" << (tid_is_inner ? " + 1u" : "") << ";\n"
+          << "          const u32 tidv = tidv0_" << (tid_is_inner ? " + " + std::to_string(h) + "u" : "") << ";\n"
           << "          const u32 lbv = lbv0_;\n"
           << "          r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = bid0_;\n";
         for (uint32_t l = 0; l < pg.n_levels; ++l)
           s << "          r[" << MAPC_REG_K0 + l << "] = c0_[" << l << "]"
-            << (!tid_is_inner && l + 1 == pg.n_levels ? " + (W)1" : "") << ";\n";
+            << (!tid_is_inner && l + 1 == pg.n_levels ? " + (W)" + std::to_string(h) : "") << ";\n";
         s << "          (void)t;\n";
       } else {
         s << "          const bool valid = t < sg.n_tuples;\n"
@@ -335,22 +365,41 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         }
       }
       s << "          bool act = true;\n";
-      if (h == 0)
+      if (G == 4) {      // quads of 16-bit cells: accumulate the run starting at tuple 0's cell
+        if (h == 0)
+          s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; accP[K] = (u64)cd_; okP[K] = true; }\n";
+        else
+          s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "if (okP[K] && sf_ == sfP[K] + " << h
+            << "u) accP[K] |= (u64)cd_ << " << 16 * h << "; else " << red1("sf_", "cd_") << " }\n";
+      } else if (h == 0) {
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; cdP[K] = cd_; okP[K] = true; }\n";
-      else
+      } else {
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell
           << "if (okP[K] && sf_ == sfP[K] + 1 && !(sfP[K] & 1u)) { "
-             "atomicOr(reinterpret_cast<u64*>(keys) + (sf_ >> 1), (u64)cdP[K] | ((u64)cd_ << 32)); okP[K] = false; } "
-             "else atomicOr(reinterpret_cast<u32*>(keys) + sf_, cd_); }\n";
+          << red2 << " okP[K] = false; } "
+             "else " << red1("sf_", "cd_") << " }\n";
+      }
       s << program_body(pg.ops, u32, true)
         << "#undef EMIT_SITE\n"
         << "          (void)act;\n"
         << "        }\n";
     }
-    s << "#pragma unroll\n"
-      << "        for (int k = 0; k < " << ne << "; ++k)\n"
-      << "          if (okP[k]) atomicOr(reinterpret_cast<u32*>(keys) + sfP[k], cdP[k]);\n"
-      << "      }\n"
+    if (G == 4)          // one red.or.b64 over an aligned quad, else the run's cells one by one
+      s << "#pragma unroll\n"
+        << "        for (int k = 0; k < " << ne << "; ++k) {\n"
+        << "          if (!okP[k]) continue;\n"
+        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); continue; }\n"
+        << "#pragma unroll\n"
+        << "          for (int j = 0; j < 4; ++j) {\n"
+        << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"
+        << "            if (c_) { const auto sj_ = sfP[k] + j; " << red1("sj_", "c_") << " }\n"
+        << "          }\n"
+        << "        }\n";
+    else
+      s << "#pragma unroll\n"
+        << "        for (int k = 0; k < " << ne << "; ++k)\n"
+        << "          if (okP[k]) " << red1("sfP[k]", "cdP[k]") << "\n";
+    s << "      }\n"
       << "      break; }\n";
   };
   // the per-tile body, emitted once per baked segment (fields as literals) and
@@ -455,7 +504,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
 }
 
 std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, uint32_t cell_bytes) {
-  std::string src = kPrelude;
+  std::string src = prelude();
   for (size_t i = 0; i < chunks.size(); ++i) src += chunk_kernel_source(chunks[i], (int)i, u32, mode, cell_bytes);
   return src;
 }
@@ -498,7 +547,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
     for (size_t i = 0; i < nc; ++i)
       if (want[i] && !g_cache.count(keys[i])) need.push_back((int)i);
   }
-  for (int i : need) srcs[i] = std::string(kPrelude) + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
+  for (int i : need) srcs[i] = prelude() + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
   std::vector<std::vector<char>> cubins(nc);
   std::vector<std::string> logs(nc);
   std::vector<int> rc(nc, 0);

@@ -13,10 +13,10 @@ struct JitProgram {
   uint32_t prog_begin;            // case label: the program's offset in the chunk's bytecode
   uint32_t n_levels;
   std::vector<MapcOp> ops;        // mode-independent ops (divisions by constants left to NVRTC)
-  // the innermost tuple coordinate (tid when tid_inner or without loops, else the
-  // innermost loop counter) has an even range: an even tuple index and its
-  // successor differ only in that coordinate (+1), no carry
-  bool pair_nocarry = false;
+  // range of the innermost tuple coordinate (tid when tid_inner or without loops,
+  // else the innermost loop counter): when a multiple of G, the G tuples from a
+  // multiple of G differ only in that coordinate (+0..G-1), no carry
+  uint64_t inner_range = 0;
   bool tid_inner = false;
 };
 

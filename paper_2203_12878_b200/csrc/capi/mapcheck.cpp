@@ -103,7 +103,7 @@ struct Chunk {
   mapj::JitChunk jit;                       // straight-line programs for the specialised generate
   // sort-free direct-address detect (direct.cu): one cell per sort-field value
   uint64_t cells = 0;                       // 2^S
-  uint32_t cell_bytes = 4;                  // 4 if 2 w_tid + 1 <= 32, else 8
+  uint32_t cell_bytes = 4;                  // 2 if w_tid <= 10 (devabi.h code16), 4 if 2 w_tid + 1 <= 32, else 8
   bool direct_ok = false;                   // the table is cheap enough and fits the scratch plan
   size_t dev_segs = 0;                      // offset of this chunk's segment table in the all-chunks region
 };
@@ -227,7 +227,7 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
         {
           mapj::JitProgram jp{pb, g.n_levels, g.ops};
           const uint64_t inner = (g.tid_inner || g.n_levels == 0) ? B : g.trips[g.n_levels - 1];
-          jp.pair_nocarry = inner % 2 == 0;
+          jp.inner_range = inner;
           jp.tid_inner = g.tid_inner;
           ch.jit.programs.push_back(std::move(jp));
         }
@@ -372,7 +372,8 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     // DESIGN.md §6, profiles/r1j_configs.jsonl).  Its size is bounded by key
     // buffer B (which it overlays) or 1 GiB.
     const uint32_t S = ch.lay.sort_bits;
-    ch.cell_bytes = 2 * ch.lay.w_tid + 1 <= 32 ? 4u : 8u;
+    static const bool cell16 = [] { const char* e = getenv("MAPC_CELL16"); return !(e && e[0] == '0'); }();
+    ch.cell_bytes = cell16 && ch.lay.w_tid <= MAPC_CW16_MAX_WT ? 2u : 2 * ch.lay.w_tid + 1 <= 32 ? 4u : 8u;
     if (S <= 40) {
       ch.cells = 1ull << S;
       const uint64_t tb = ch.cells * ch.cell_bytes;

@@ -28,6 +28,19 @@
 #define MAPC_GEN_V 4                 // tuples per thread per VM pass
 #define MAPC_GEN_TILE (MAPC_GEN_THREADS * MAPC_GEN_V)
 
+// Direct-address detect cell codes (direct.cu).  16-bit cells (blockDim <=
+// 1024): tid = (hi, lo) 5-bit digits, each encoded as one of the 32 smallest
+// 7-bit words with exactly three ones (a constant-weight code: the OR of two
+// DISTINCT codewords has more than three ones), kind at bit 14:
+//   code16(t, k) = CW7[t & 31] | CW7[(t >> 5) & 31] << 7 | k << 14
+// racy16(c) <=> bit 14 and (popc(c & 0x7F) > 3 or popc((c >> 7) & 0x7F) > 3).
+// The 32 codewords, 8 per 56-bit word, 7 bits each (low codeword first):
+#define MAPC_CW7_W0 0x3258a931c34587ull
+#define MAPC_CW7_W1 0x58a94a64a8ce1aull
+#define MAPC_CW7_W2 0x931a2c370d1931ull
+#define MAPC_CW7_W3 0xc586c54a54664aull
+#define MAPC_CW16_MAX_WT 10
+
 // Generate modes (generate.cu, capi/jit.cpp).
 #define MAPC_MODE_KEYS 0u      // write every access as a packed u64 key (sort / table detect)
 #define MAPC_MODE_DIRECT 1u    // fold every access into its cell of the direct-address table (direct.cu)

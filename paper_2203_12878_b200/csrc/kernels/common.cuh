@@ -13,6 +13,15 @@ __device__ __forceinline__ uint32_t fastdiv(uint32_t n, const MapcFastDiv& f) {
   return (hi + ((n - hi) >> 1)) >> f.s;
 }
 
+// d-th codeword of the 16-bit cell code (devabi.h), from register constants
+__device__ __forceinline__ uint32_t cw7(uint32_t d) {
+  const unsigned long long w = d < 8 ? MAPC_CW7_W0 : d < 16 ? MAPC_CW7_W1 : d < 24 ? MAPC_CW7_W2 : MAPC_CW7_W3;
+  return (uint32_t)(w >> (7 * (d & 7))) & 0x7Fu;
+}
+__device__ __forceinline__ uint32_t code16(uint32_t t, uint32_t kind) {
+  return cw7(t & 31u) | (cw7((t >> 5) & 31u) << 7) | (kind << 14);
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -18,7 +18,12 @@
 // (counts racy cells, atomicMin of the smallest racy sf); the canonical
 // witness of that one cell is folded from its keys, which generate re-emits in
 // mode MAPC_MODE_FILTER (k_witness_flat).  Cells are u32 when 2wt + 1 <= 32,
-// else u64.
+// else u64 -- except for blockDim <= 1024 (wt <= 10), where a shorter exact code
+// fits 16 bits: each 5-bit digit of the tid becomes one of 32 seven-bit words
+// with exactly three ones (the OR of two distinct such words has four or more),
+// so "two distinct tids" <=> some digit's 7-bit field has popcount > 3
+// (devabi.h code16; tests/test_direct_lemma.py).  Half the table bytes of the
+// u32 code, two cells per 32-bit atomic word.
 #include "common.cuh"
 #include "segstate.cuh"
 
@@ -28,8 +33,13 @@ constexpr int DS_THREADS = 128;
 
 template <typename C>
 __device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
-  const C m = wt >= 8 * sizeof(C) ? ~C(0) : ((C(1) << wt) - 1);
-  return ((c >> (2 * wt)) & 1) && ((c & (c >> wt) & m) != 0);
+  if constexpr (sizeof(C) == 2) {     // constant-weight 16-bit code (devabi.h)
+    const uint32_t x = c;
+    return ((x >> 14) & 1u) && (__popc(x & 0x7Fu) > 3 || __popc((x >> 7) & 0x7Fu) > 3);
+  } else {
+    const C m = wt >= 8 * sizeof(C) ? ~C(0) : ((C(1) << wt) - 1);
+    return ((c >> (2 * wt)) & 1) && ((c & (c >> wt) & m) != 0);
+  }
 }
 
 // Grid-stride over 16-byte vectors of cells, DS_UNROLL vectors in flight per
@@ -42,7 +52,6 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
   constexpr int PER = 16 / sizeof(C);
   const unsigned long long nvec = cells / PER;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  const C m = wt >= 8 * sizeof(C) ? ~C(0) : ((C(1) << wt) - 1);
   unsigned long long best = ~0ull, racy = 0;
   const uint4* __restrict__ v4 = reinterpret_cast<const uint4*>(tab);
   for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < nvec;
@@ -63,9 +72,9 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
     for (int u = 0; u < DS_UNROLL; ++u) {
       C c[PER];
       memcpy(c, &v[u], 16);
-      C hit = 0;
+      bool hit = false;
 #pragma unroll
-      for (int j = 0; j < PER; ++j) hit |= (c[j] >> (2 * wt)) & (C)((c[j] & (c[j] >> wt) & m) != 0);
+      for (int j = 0; j < PER; ++j) hit |= cell_racy(c[j], wt);
       if (hit) {
 #pragma unroll
         for (int j = 0; j < PER; ++j)
@@ -178,7 +187,9 @@ extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long lo
   const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
   const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 16);
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  if (cell_bytes == 4)
+  if (cell_bytes == 2)
+    mapk::k_direct_scan<uint16_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
+  else if (cell_bytes == 4)
     mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
   else
     mapk::k_direct_scan<unsigned long long>

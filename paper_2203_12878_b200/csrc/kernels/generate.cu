@@ -183,7 +183,9 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
             if (mode == MAPC_MODE_DIRECT) {
               const unsigned long long code =
                   tidv[v] | ((~(unsigned long long)tidv[v] & tmask) << wt) | (kind << (2 * wt));
-              if (cell_bytes == 4) atomicOr(reinterpret_cast<uint32_t*>(tab) + sf, (uint32_t)code);
+              if (cell_bytes == 2)   // two 16-bit cells per 32-bit word
+                atomicOr(reinterpret_cast<uint32_t*>(tab) + (sf >> 1), code16(tidv[v], (uint32_t)kind) << (16 * (sf & 1)));
+              else if (cell_bytes == 4) atomicOr(reinterpret_cast<uint32_t*>(tab) + sf, (uint32_t)code);
               else atomicOr(reinterpret_cast<unsigned long long*>(tab) + sf, code);
               cnt += dense ? 0u : 1u;
               continue;

@@ -55,3 +55,44 @@ def test_cell_code_matches_race_definition(wt):
         assert racy_from_cell(c, wt) == racy_by_definition(accs)
     # the code fits the cell: 2 wt + 1 bits (u32 cells up to wt = 15)
     assert code((1 << wt) - 1, 1, wt) < (1 << (2 * wt + 1))
+
+
+# ---- the 16-bit cell code (blockDim <= 1024; devabi.h code16) ---------------
+# Written from its definition, independently of the kernels: each 5-bit digit of the
+# tid maps to one of the 32 smallest 7-bit words with exactly three ones.
+CW7 = [x for x in range(128) if bin(x).count("1") == 3][:32]
+
+
+def code16(t, k):
+    return CW7[t & 31] | (CW7[(t >> 5) & 31] << 7) | (k << 14)
+
+
+def racy16(c):
+    return bool((c >> 14) & 1) and (bin(c & 0x7F).count("1") > 3 or bin((c >> 7) & 0x7F).count("1") > 3)
+
+
+def test_code16_distinct_pairs_exhaustive():
+    # any two distinct tids < 1024 -> the OR has a digit field with popcount > 3;
+    # one tid alone (any number of times) -> every field has popcount exactly 3
+    import numpy as np
+    t = np.arange(1024)
+    lo = np.array([CW7[x & 31] for x in t])
+    hi = np.array([CW7[(x >> 5) & 31] for x in t])
+    pc = np.vectorize(lambda v: bin(int(v)).count("1"))
+    orlo = lo[:, None] | lo[None, :]
+    orhi = hi[:, None] | hi[None, :]
+    multi = (pc(orlo) > 3) | (pc(orhi) > 3)
+    assert (multi == ~np.eye(1024, dtype=bool)).all()
+    assert all(bin(code16(x, 0)).count("1") == 6 for x in range(1024))
+    assert code16(1023, 1) < (1 << 16)
+
+
+def test_code16_matches_race_definition():
+    rng = random.Random(16)
+    for _ in range(5000):
+        pool = [rng.randrange(1024) for _ in range(rng.randint(1, 3))]
+        accs = [(rng.choice(pool), rng.random() < 0.3) for _ in range(rng.randint(1, 6))]
+        c = 0
+        for t, k in accs:
+            c |= code16(t, int(k))
+        assert racy16(c) == racy_by_definition(accs)
