@@ -210,6 +210,39 @@ ROOFLINE_MODELS = {
 }
 
 
+# Issue peak of a B200 (B200_PROFILING.md / B300_MICROARCH.md unit counts): 148 SMs x
+# 4 schedulers x 1 warp-instruction per cycle x 1965 MHz = 1163 G warp-instructions/s.
+ISSUE_PEAK_G = 148 * 4 * 1.965
+
+
+def ncu_direct():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_direct_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def issue_roofline(kern, hbm):
+    """The direct generate with 16-bit cells is bound by instruction issue (ncu: issue
+    ~73% alone): achieved = warp instructions per launch (the committed ncu capture of
+    the bench command) / the live CUDA-event duration, against the issue peak.  The
+    HBM view (algorithmic table bytes) is kept under "hbm"."""
+    info = ncu_direct()
+    inst = info.get("warp_inst_per_launch")
+    k = kern.get("direct", {})
+    if not inst or not k.get("launches") or k.get("ms", 0) <= 0:
+        return hbm
+    per_launch_s = k["ms"] / 1e3 / k["launches"]
+    achieved = inst / per_launch_s / 1e9
+    return {"bound": "alu", "kernel": hbm["kernel"], "achieved": achieved, "peak": ISSUE_PEAK_G,
+            "peak_kind": "derived: 148 SMs x 4 schedulers x 1.965 GHz (one warp-instruction per scheduler-cycle)",
+            "unit": "G warp-inst/s", "frac": achieved / ISSUE_PEAK_G, "traffic": hbm["traffic"],
+            "work_model": f"{inst:.4g} warp instructions per launch (ncu smsp__inst_executed of the bench command, "
+                          f"issue active {info.get('issue_active_pct', float('nan')):.0f}% when alone)",
+            "launches": k["launches"], "hbm": {f: hbm[f] for f in ("achieved", "peak", "unit", "frac", "bytes_model")}}
+
+
 def kernel_roofline(kern, cls, peak, peak_kind):
     """achieved = the class's algorithmic bytes / its CUDA-event time; for the radix
     pass both launch forms (plain, and building the next pass's range table) together."""
@@ -314,6 +347,8 @@ def main():
     ms_of = lambda c: kern.get(c, {}).get("ms", 0) + (kern.get("onesweep_next", {}).get("ms", 0) if c == "onesweep" else 0)
     dominant = max(ROOFLINE_MODELS, key=ms_of)
     roofline = kernel_roofline(kern, dominant, peak, peak_kind)
+    if dominant == "direct":
+        roofline = issue_roofline(kern, roofline)
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
     pipe_bytes = sum(v["bytes"] for v in kern.values())
     # the dominant kernel alone: the direct path's chunks run one after another
@@ -322,8 +357,9 @@ def main():
     if dominant == "direct" and kern.get("direct", {}).get("launches"):
         solo = [prog.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank,
                                  world=world, profile=True, detect=args.detect, overlap=False) for _ in range(2)]
-        r_solo = kernel_roofline(kernel_table(solo[1:]), "direct", peak, peak_kind)
-        roofline["solo"] = {"achieved": r_solo["achieved"], "frac": r_solo["frac"],
+        k_solo = kernel_table(solo[1:])
+        r_solo = issue_roofline(k_solo, kernel_roofline(k_solo, "direct", peak, peak_kind))
+        roofline["solo"] = {"achieved": r_solo["achieved"], "frac": r_solo["frac"], "unit": r_solo["unit"],
                             "note": "same kernel, chunks run sequentially (no concurrent scans)"}
     kernels_out = {k: {"ms_per_step": v["ms"] / len(results), "share": v["ms"] / kern_total,
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,

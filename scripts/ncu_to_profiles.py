@@ -37,7 +37,9 @@ def main(rep, launches, tag):
         if name.startswith("gen_") and (direct is None or dur > direct["duration_s"]):
             # the direct-mode generate (the longest gen_ launch: the filter pass exits at once when DRF)
             direct = {"kernel": name.split("(")[0] + " (mode direct)", "dram_bytes_per_launch": rd + wr, "dram_read": rd,
-                      "dram_write": wr, "duration_s": dur, "source": os.path.basename(rep)}
+                      "dram_write": wr, "duration_s": dur, "source": os.path.basename(rep),
+                      "warp_inst_per_launch": get("smsp__inst_executed.sum"),
+                      "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active")}
         if "k_rsweep" in name and traffic is None:
             traffic = {"kernel": name.split("(")[0], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                        "duration_s": dur, "source": os.path.basename(rep)}
