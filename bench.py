@@ -203,9 +203,9 @@ def ncu_traffic(which):
 ROOFLINE_MODELS = {
     "direct": ("generate fused with the direct-address table reductions (gen_0, mode direct)", "direct",
                "2 x table bytes per launch: every cell of the 2^S-cell table read and written once "
-               "(the per-access red.or are served by L2); bound in practice by L2 atomic updates of lines "
-               "that miss: the same access pattern in isolation takes 1.36 ms per 2^30 accesses with "
-               "red.or.b64 and 1.23 ms with TMA bulk OR reductions (profiles/r1k_*_microbench.txt)"),
+               "(the per-access red.or are served by L2); with 16-bit cells the kernel is issue-bound "
+               "(see the alu roofline); with u32 cells it was bound by L2 atomic updates of lines that miss "
+               "(profiles/r1k_*_microbench.txt)"),
     "onesweep": ("k_rsweep (static-range LSD radix pass)", "rsweep", "16 B per key per active pass (8 read + 8 write)"),
 }
 
