@@ -131,6 +131,8 @@ _lib.map_debug_dump.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
 _lib.map_debug_dump.restype = ctypes.c_size_t
 _lib.map_debug_jit_check.argtypes = [_P, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_size_t]
 _lib.map_debug_jit_check.restype = ctypes.c_int
+_lib.map_debug_jit_source.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_debug_jit_source.restype = ctypes.c_size_t
 _lib.mapc_test_fastdiv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
 _lib.mapc_test_fastdiv.restype = ctypes.c_uint32
 
@@ -302,6 +304,21 @@ class MapProgram:
         buf = ctypes.create_string_buffer(4096)
         r = _lib.map_debug_jit_check(self._h, int(chunk_max_accesses), buf, 4096)
         return "" if r == 0 else (buf.value.decode(errors="replace") or f"status {r}")
+
+    def jit_source(self, chunk: int = 0, mode: int = 1, chunk_max_accesses: int = 0) -> str:
+        """The specialised generate source of one chunk (mode 0 keys, 1 direct, 2 filter; debugging)."""
+        old = os.environ.get("MAPC_DEBUG_JIT_MODE")
+        os.environ["MAPC_DEBUG_JIT_MODE"] = str(int(mode))
+        try:
+            n = _lib.map_debug_jit_source(self._h, int(chunk_max_accesses), int(chunk), None, 0)
+            buf = ctypes.create_string_buffer(n + 1)
+            _lib.map_debug_jit_source(self._h, int(chunk_max_accesses), int(chunk), buf, n + 1)
+        finally:
+            if old is None:
+                del os.environ["MAPC_DEBUG_JIT_MODE"]
+            else:
+                os.environ["MAPC_DEBUG_JIT_MODE"] = old
+        return buf.value.decode()
 
     @property
     def info(self) -> Info:

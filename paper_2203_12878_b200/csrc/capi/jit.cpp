@@ -104,6 +104,43 @@ std::string program_body(const std::vector<MapcOp>& ops, bool u32, bool site_lit
   return s.str();
 }
 
+// Per EMIT site of a program: is its index "X + k" with X independent of the
+// innermost loop coordinate k (register `inner`) and k entering once, additively?
+// Then the cells of tuples t and t + h (k -> k + h, nothing else changed) are
+// sf and sf + h (mod 2^32) and the paired generate needs no run-time test.
+// Conservative taint walk over the straight-line program: 0 = independent of k,
+// 1 = X + k, 2 = anything else.
+std::vector<bool> unit_stride_sites(const std::vector<MapcOp>& ops, uint32_t inner) {
+  uint8_t st[MAPC_NREG] = {};
+  st[inner] = 1;
+  std::vector<bool> out;
+  for (const MapcOp& op : ops) {
+    const uint32_t c = op.code & MAPC_CODE_MASK;
+    const uint8_t a = (op.code & MAPC_A_IMM) ? 0 : st[op.a % MAPC_NREG];
+    const uint8_t b = (op.code & MAPC_B_IMM) ? 0 : st[op.b % MAPC_NREG];
+    uint8_t d;
+    switch (c) {
+      case VM_EMIT: out.push_back(a == 1); continue;
+      case VM_ACT: continue;
+      case VM_MOVI: d = 0; break;
+      case VM_ADD: d = (a == 0 && b == 0) ? 0 : ((a == 1 && b == 0) || (a == 0 && b == 1)) ? 1 : 2; break;
+      case VM_MADK: {
+        const uint8_t x = st[op.aux % MAPC_NREG];
+        d = (x == 0 && b == 0) ? a : 2;
+        break;
+      }
+      case VM_TRIP: {
+        const uint8_t x = (op.aux & MAPC_AUX_CONST) ? 0 : st[op.aux % MAPC_NREG];
+        d = (a == 0 && b == 0 && x == 0) ? 0 : 2;
+        break;
+      }
+      default: d = (a == 0 && b == 0) ? 0 : 2; break;
+    }
+    st[op.dst % MAPC_NREG] = d;
+  }
+  return out;
+}
+
 const char* kPrelude = R"(
 typedef unsigned int u32;
 typedef unsigned long long u64;
@@ -280,6 +317,12 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
     s << "  " << (sf32 ? "u32" : "u64") << " sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS
       << "]; bool okP[" << MAPC_MAX_EMITS << "]; u64 accP[" << MAPC_MAX_EMITS << "]; (void)cdP; (void)accP;\n";
+  // 16-bit cells: the tid part of every code from a 2 KB shared table (one
+  // LDS instead of ~35 select/shift instructions per tuple group)
+  if (paired && cell_bytes == 2)
+    s << "  __shared__ unsigned short s_code16_[1024];\n"
+      << "  for (int i = me; i < 1024; i += " << T << ") s_code16_[i] = (unsigned short)code16((u32)i, 0u);\n"
+      << "  __syncthreads();\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
@@ -308,7 +351,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         std::to_string(MAPC_ERR_LAYOUT) + "u; " +
         (sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
               : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
-        (cell_bytes == 2 ? std::string("const u32 cd_ = code16(tidv, (u32)(KIND)); ")
+        (cell_bytes == 2 ? std::string("const u32 cd_ = tcd_ | ((u32)(KIND) << 14); ")
                          : "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) +
                                "u) | ((u32)(KIND) << " + std::to_string(2 * ch.lay.w_tid) + "u); ") +
         "if (!sg.dense) ++cnt; ";
@@ -341,6 +384,14 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
     if (nocarry)
       s << "        bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n";
+    // sites whose cell advances by exactly h from tuple 0 to tuple h (32-bit sort fields)
+    std::vector<bool> us;
+    if (G == 4 && nocarry && !tid_is_inner && sf32 && pg.n_levels > 0)
+      us = unit_stride_sites(pg.ops, MAPC_REG_K0 + pg.n_levels - 1);
+    us.resize(NE, false);
+    s << "        constexpr bool US_[" << NE << "] = {";
+    for (int k = 0; k < NE; ++k) s << (k ? ", " : "") << (us[k] ? "true" : "false");
+    s << "}; (void)US_;\n";
     for (int h = 0; h < G; ++h) {
       s << "        {\n"
         << "          const u32 t = tp + " << h << "u;\n";
@@ -364,13 +415,17 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
           for (uint32_t l = 0; l < pg.n_levels; ++l) s << "          c0_[" << l << "] = r[" << MAPC_REG_K0 + l << "];\n";
         }
       }
+      // the tid part of the 16-bit code once per tuple, outside the sites' guards
+      // (inside them NVRTC re-derived it at every site: ~30 instructions each);
+      // code16 reads only the low 10 bits of the tid
+      if (cell_bytes == 2) s << "          const u32 tcd_ = s_code16_[tidv & 1023u];\n";
       s << "          bool act = true;\n";
       if (G == 4) {      // quads of 16-bit cells: accumulate the run starting at tuple 0's cell
         if (h == 0)
           s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; accP[K] = (u64)cd_; okP[K] = true; }\n";
         else
-          s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "if (okP[K] && sf_ == sfP[K] + " << h
-            << "u) accP[K] |= (u64)cd_ << " << 16 * h << "; else " << red1("sf_", "cd_") << " }\n";
+          s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "if (okP[K] && (US_[K] || sf_ == sfP[K] + " << h
+            << "u)) accP[K] |= (u64)cd_ << " << 16 * h << "; else " << red1("sf_", "cd_") << " }\n";
       } else if (h == 0) {
         s << "#define EMIT_SITE(K, IX, ARR, KIND) { " << cell << "sfP[K] = sf_; cdP[K] = cd_; okP[K] = true; }\n";
       } else {

@@ -176,3 +176,33 @@ def test_tuple_order_choice():
         inst = config(name)
         groups = _dump(mc.MapProgram(inst.src, inst.grid, inst.block, inst.params))
         assert groups and all(("tid_inner" in g) == want for g in groups), (name, groups[:2])
+
+
+def _us_flags(src, params, block=(64, 1, 1)):
+    p = mc.MapProgram(src, (1, 1, 1), block, params)
+    m = re.search(r"constexpr bool US_\[\d+\] = \{([^}]*)\}", p.jit_source(0, mode=1))
+    assert m, "direct-mode source without unit-stride flags"
+    return [x.strip() == "true" for x in m.group(1).split(",")]
+
+
+def test_unit_stride_sites():
+    # the paired 16-bit generate skips the run-time adjacency test only for sites
+    # whose index is X + c (c the innermost coordinate, X independent of c);
+    # anything else keeps the test
+    inst = config("5a")
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    m = re.search(r"constexpr bool US_\[\d+\] = \{([^}]*)\}", p.jit_source(0, mode=1))
+    assert m and [x.strip() for x in m.group(1).split(",")] == ["true"] * 4
+    head = "params C; shared A;\nforU r in 0..4 {\n  forU c in 0..C {\n    "
+    tail = "\n  }\n}"
+    cases = [
+        ("rd A[tid * 4 * C + r * C + c + 5]", [True]),
+        ("rd A[tid * 4 * C + r * C + 2 * c]", [False]),
+        ("rd A[tid * 4 * C + r * C + (c + 1) % C]", [False]),
+        ("rd A[tid * 4 * C + r * C + c * 1 + c]", [False]),
+        ("rd A[tid * 4 * C + r * C + c - 1]", [False]),
+        ("rd A[tid * 4 * C + r]; wr A[1000000 + tid * 4 * C + r * C + c]", [False, True]),
+    ]
+    for body, want in cases:
+        got = _us_flags(head + body + tail, {"C": 64})
+        assert got[: len(want)] == want, (body, got)
