@@ -317,12 +317,6 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
     s << "  " << (sf32 ? "u32" : "u64") << " sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS
       << "]; bool okP[" << MAPC_MAX_EMITS << "]; u64 accP[" << MAPC_MAX_EMITS << "]; (void)cdP; (void)accP;\n";
-  // 16-bit cells: the tid part of every code from a 2 KB shared table (one
-  // LDS instead of ~35 select/shift instructions per tuple group)
-  if (paired && cell_bytes == 2)
-    s << "  __shared__ unsigned short s_code16_[1024];\n"
-      << "  for (int i = me; i < 1024; i += " << T << ") s_code16_[i] = (unsigned short)code16((u32)i, 0u);\n"
-      << "  __syncthreads();\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
@@ -386,8 +380,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "        bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n";
     // sites whose cell advances by exactly h from tuple 0 to tuple h (32-bit sort fields)
     std::vector<bool> us;
-    if (G == 4 && nocarry && !tid_is_inner && sf32 && pg.n_levels > 0)
-      us = unit_stride_sites(pg.ops, MAPC_REG_K0 + pg.n_levels - 1);
+    if (G == 4 && nocarry && sf32)   // the coordinate that advances by h: tid or the innermost loop's
+      us = unit_stride_sites(pg.ops, tid_is_inner ? MAPC_REG_TID : MAPC_REG_K0 + pg.n_levels - 1);
     us.resize(NE, false);
     s << "        constexpr bool US_[" << NE << "] = {";
     for (int k = 0; k < NE; ++k) s << (k ? ", " : "") << (us[k] ? "true" : "false");
@@ -417,8 +411,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       }
       // the tid part of the 16-bit code once per tuple, outside the sites' guards
       // (inside them NVRTC re-derived it at every site: ~30 instructions each);
-      // code16 reads only the low 10 bits of the tid
-      if (cell_bytes == 2) s << "          const u32 tcd_ = s_code16_[tidv & 1023u];\n";
+      // a 2 KB shared table of the codes instead made 3a/4b 20-30% slower (r1u)
+      if (cell_bytes == 2) s << "          const u32 tcd_ = code16(tidv, 0u);\n";
       s << "          bool act = true;\n";
       if (G == 4) {      // quads of 16-bit cells: accumulate the run starting at tuple 0's cell
         if (h == 0)

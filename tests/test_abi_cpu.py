@@ -193,6 +193,10 @@ def test_unit_stride_sites():
     p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
     m = re.search(r"constexpr bool US_\[\d+\] = \{([^}]*)\}", p.jit_source(0, mode=1))
     assert m and [x.strip() for x in m.group(1).split(",")] == ["true"] * 4
+    # tid innermost (the scans' k * 1024 + tid): the tid advances by h instead
+    inst = config("4a")
+    src4 = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).jit_source(0, mode=1)
+    assert re.search(r"constexpr bool US_\[\d+\] = \{[^}]*true", src4)
     head = "params C; shared A;\nforU r in 0..4 {\n  forU c in 0..C {\n    "
     tail = "\n  }\n}"
     cases = [

@@ -432,3 +432,29 @@ def test_overlapped_and_sequential_direct_pipelines_agree(name, sizes):
     assert sum(x.racy_segments for x in parts) == o.n_racy_segments
     wits = [x.witness.as_tuple() for x in parts if x.witness]
     assert (min(wits) if wits else None) == o.witness
+
+
+def test_fuzz_unit_stride_sites():
+    # fuzz instances whose direct-mode JIT marks a site unit-stride (the run-time
+    # adjacency test folded away at compile time), JIT generate on
+    # the direct path, default and unit chunks, vs the oracle
+    import re
+    bad, picked = [], 0
+    for seed in range(0, 1500):
+        inst, _ = fuzz.random_instance(seed)
+        p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+        if not any("true" in x for c in range(min(p.n_chunks(0), 4))
+                   for x in re.findall(r"US_\[\d+\] = \{([^}]*)\}", p.jit_source(c, 1))):
+            continue
+        o = oracle.check_instance(inst, threads=1)
+        if o.status != 0:
+            continue
+        picked += 1
+        unit = max(1, p.info.max_unit_accesses)
+        for chunk in (0, unit):
+            if chunk and p.n_chunks(chunk) > 16:
+                continue
+            r = p.check_races(detect="direct", gen="jit", chunk_max_accesses=chunk)
+            if _got(r) != _want(o):
+                bad.append((seed, chunk, inst.src, _got(r), _want(o)))
+    assert picked >= 20 and not bad, (picked, bad[:3])
