@@ -759,7 +759,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // side kernels' CTAs.  MAPC_OVERLAP=0 restores the sequential pipeline.
   static const int ovl_env = [] { const char* e = getenv("MAPC_OVERLAP"); return e ? atoi(e) : 1; }();
   static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 12; }();
-  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 2; }();
+  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 3; }();
   const size_t tab_stride = align_up(P.dtab_bytes);
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&

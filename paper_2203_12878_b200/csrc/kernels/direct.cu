@@ -42,6 +42,24 @@ __device__ __forceinline__ bool cell_racy(C c, uint32_t wt) {
   }
 }
 
+// Two 16-bit cells of one 32-bit word at once, without POPC (a quarter-rate
+// pipe: it bounded the scan at ~0.4 ms per 2^29 cells).  The four 7-bit digit
+// fields are spread into the byte lanes of a word whose lane top bits are set
+// as guards (no borrow leaves a lane); three rounds of "clear the lowest set
+// bit" (x & (x - 1), guard restored) leave a nonzero field iff it had >= 4
+// ones; a lane counts only if its cell's kind bit (14, 30) is set.  Nonzero
+// result <=> some cell of the word is racy (same predicate as cell_racy;
+// exhaustive CPU check via mapc_test_racy16_word, tests/test_direct_lemma.py).
+__host__ __device__ __forceinline__ uint32_t racy16_word(uint32_t w) {
+  const uint32_t g = 0x80808080u, one = 0x01010101u;
+  uint32_t x = (w & 0x007F007Fu) | ((w << 1) & 0x7F007F00u) | g;
+  x = (x & (x - one)) | g;
+  x = (x & (x - one)) | g;
+  x = (x & (x - one));
+  const uint32_t k = (w >> 14) & 0x00010001u;        // kind bits of the two cells -> bits 0 and 16
+  return x & (k * 0x7F7Fu);
+}
+
 // Grid-stride over 16-byte vectors of cells, DS_UNROLL vectors in flight per
 // thread; each thread's first racy cell is its smallest (indices increase
 // along the stride).  The common all-clean vector costs a few ALU ops per cell.
@@ -73,8 +91,12 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
       C c[PER];
       memcpy(c, &v[u], 16);
       bool hit = false;
+      if constexpr (sizeof(C) == 2)
+        hit = (racy16_word(v[u].x) | racy16_word(v[u].y) | racy16_word(v[u].z) | racy16_word(v[u].w)) != 0;
+      else {
 #pragma unroll
-      for (int j = 0; j < PER; ++j) hit |= cell_racy(c[j], wt);
+        for (int j = 0; j < PER; ++j) hit |= cell_racy(c[j], wt);
+      }
       if (hit) {
 #pragma unroll
         for (int j = 0; j < PER; ++j)
@@ -202,3 +224,6 @@ extern "C" cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, 
   mapk::k_witness_flat<<<1, mapk::WF_THREADS, 0, s>>>(keys, ctrl, pay_bits, w_tid, cap);
   return cudaGetLastError();
 }
+
+// Host-side check of the SWAR racy test (CPU tests): nonzero iff a cell of w is racy.
+extern "C" uint32_t mapc_test_racy16_word(uint32_t w) { return mapk::racy16_word(w); }

@@ -96,3 +96,21 @@ def test_code16_matches_race_definition():
         for t, k in accs:
             c |= code16(t, int(k))
         assert racy16(c) == racy_by_definition(accs)
+
+
+def test_racy16_word_swar_exhaustive():
+    # the scan's POPC-free test of two 16-bit cells per 32-bit word (direct.cu
+    # racy16_word, exported for this check) against racy16 above: every value of
+    # each cell with the other cell 0 or a random value, and random word pairs
+    import ctypes
+    import paper_2203_12878_b200 as mc
+    f = mc._lib.mapc_test_racy16_word
+    f.argtypes = [ctypes.c_uint32]
+    f.restype = ctypes.c_uint32
+    rng = random.Random(7)
+    for c in range(1 << 16):
+        other = rng.randrange(1 << 16)
+        for w, want in ((c, racy16(c)), (c << 16, racy16(c)),
+                        (c | (other << 16), racy16(c) or racy16(other)),
+                        (other | (c << 16), racy16(c) or racy16(other))):
+            assert (f(w) != 0) == want, hex(w)
