@@ -203,9 +203,8 @@ def ncu_traffic(which):
 ROOFLINE_MODELS = {
     "direct": ("generate fused with the direct-address table reductions (gen_0, mode direct)", "direct",
                "2 x table bytes per launch: every cell of the 2^S-cell table read and written once "
-               "(the per-access red.or are served by L2); with 16-bit cells the kernel is issue-bound "
-               "(see the alu roofline); with u32 cells it was bound by L2 atomic updates of lines that miss "
-               "(profiles/r1k_*_microbench.txt)"),
+               "(the per-access red.or are served by L2); bound by the rate of global red.or.b64 into the "
+               "HBM-resident table (profiles/r1h_red_width_microbench.txt); the issue view is under alu"),
     "onesweep": ("k_rsweep (static-range LSD radix pass)", "rsweep", "16 B per key per active pass (8 read + 8 write)"),
 }
 
@@ -224,10 +223,13 @@ def ncu_direct():
 
 
 def issue_roofline(kern, hbm):
-    """The direct generate with 16-bit cells is bound by instruction issue (ncu: issue
-    ~73% alone): achieved = warp instructions per launch (the committed ncu capture of
-    the bench command) / the live CUDA-event duration, against the issue peak.  The
-    HBM view (algorithmic table bytes) is kept under "hbm"."""
+    """The direct generate: primary view HBM (2 x table bytes per launch over its live
+    CUDA-event time; DRAM traffic = algorithmic in the committed ncu capture).  Since the
+    r1t/r1u instruction cuts it is no longer issue-bound (issue ~61% alone, r1w): what
+    limits it is the rate of global red.or.b64 into an HBM-resident table
+    (profiles/r1h_red_width_microbench.txt).  The issue view -- warp instructions per
+    launch from the same capture over the live duration, against the derived issue
+    peak -- is kept under "alu"."""
     info = ncu_direct()
     inst = info.get("warp_inst_per_launch")
     k = kern.get("direct", {})
@@ -235,12 +237,13 @@ def issue_roofline(kern, hbm):
         return hbm
     per_launch_s = k["ms"] / 1e3 / k["launches"]
     achieved = inst / per_launch_s / 1e9
-    return {"bound": "alu", "kernel": hbm["kernel"], "achieved": achieved, "peak": ISSUE_PEAK_G,
-            "peak_kind": "derived: 148 SMs x 4 schedulers x 1.965 GHz (one warp-instruction per scheduler-cycle)",
-            "unit": "G warp-inst/s", "frac": achieved / ISSUE_PEAK_G, "traffic": hbm["traffic"],
-            "work_model": f"{inst:.4g} warp instructions per launch (ncu smsp__inst_executed of the bench command, "
-                          f"issue active {info.get('issue_active_pct', float('nan')):.0f}% when alone)",
-            "launches": k["launches"], "hbm": {f: hbm[f] for f in ("achieved", "peak", "unit", "frac", "bytes_model")}}
+    out = dict(hbm)
+    out["alu"] = {"achieved": achieved, "peak": ISSUE_PEAK_G,
+                  "peak_kind": "derived: 148 SMs x 4 schedulers x 1.965 GHz (one warp-instruction per scheduler-cycle)",
+                  "unit": "G warp-inst/s", "frac": achieved / ISSUE_PEAK_G,
+                  "work_model": f"{inst:.4g} warp instructions per launch (ncu smsp__inst_executed of the bench "
+                                f"command, issue active {info.get('issue_active_pct', float('nan')):.0f}% when alone)"}
+    return out
 
 
 def kernel_roofline(kern, cls, peak, peak_kind):
