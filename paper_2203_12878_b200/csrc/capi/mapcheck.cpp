@@ -36,7 +36,7 @@ cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long 
                                  uint32_t cell_bytes, cudaStream_t s);
 cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm, cudaStream_t s);
 cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
-                                    MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s, int clear = 0);
+                                    MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s);
 cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
 cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t w_tid,
                                      unsigned long long cap, cudaStream_t s);
@@ -760,8 +760,6 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   static const int ovl_env = [] { const char* e = getenv("MAPC_OVERLAP"); return e ? atoi(e) : 1; }();
   static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 12; }();
   static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 3; }();
-  // 16-bit cells: the scan zeroes the cells it read (one pass instead of scan + clear)
-  static const bool scan_clear = [] { const char* e = getenv("MAPC_SCAN_CLEAR"); return e && e[0] == '1'; }();
   const size_t tab_stride = align_up(P.dtab_bytes);
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&
@@ -833,11 +831,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       // the last chunk's scan has no generate to share the GPU with: full grid
       const bool last = i + 1 == mine.size();
       m = begin_on(MAP_K_DETECT, s2);
-      const bool fuse = scan_clear && ch.cell_bytes == 2 && i + 2 < mine.size();
-      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2,
-                                 fuse ? 1 : 0));
+      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
       end_on(m, s2);
-      if (i + 2 < mine.size() && !fuse) {
+      if (i + 2 < mine.size()) {
         m = begin_on(MAP_K_CLEAR, s2);
         CK(mapc_launch_table_clear(tb, tbytes, n_sms, ovl_side_ctas, s2));
         end_on(m, s2);

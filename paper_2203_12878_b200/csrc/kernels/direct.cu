@@ -64,12 +64,9 @@ __host__ __device__ __forceinline__ uint32_t racy16_word(uint32_t w) {
 // thread; each thread's first racy cell is its smallest (indices increase
 // along the stride).  The common all-clean vector costs a few ALU ops per cell.
 constexpr int DS_UNROLL = 8;
-// CLEAR: also zero every cell after reading it (each 16-byte vector is loaded
-// once, by the thread that then stores the zeros), replacing the separate
-// k_table_clear pass before the table's next use.
-template <typename C, bool CLEAR = false>
+template <typename C>
 __global__ void __launch_bounds__(DS_THREADS)
-k_direct_scan(C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
+k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
   constexpr int PER = 16 / sizeof(C);
   const unsigned long long nvec = cells / PER;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -87,14 +84,6 @@ k_direct_scan(C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCt
                      : "l"(v4 + i));
       else
         v[u] = make_uint4(0, 0, 0, 0);
-    }
-    if constexpr (CLEAR) {
-      asm volatile("" ::: "memory");     // the zero stores stay after this thread's loads
-#pragma unroll
-      for (int u = 0; u < DS_UNROLL; ++u) {
-        const unsigned long long i = i0 + u * stride;
-        if (i < nvec) __stcs(reinterpret_cast<uint4*>(tab) + i, make_uint4(0, 0, 0, 0));
-      }
     }
 
 #pragma unroll
@@ -121,14 +110,10 @@ k_direct_scan(C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCt
   // ragged tail (cells not a multiple of PER)
   for (unsigned long long i = nvec * PER + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cells;
        i += stride)
-  {
-    const C c = tab[i];
-    if constexpr (CLEAR) tab[i] = C(0);
-    if (cell_racy(c, wt)) {
+    if (cell_racy(tab[i], wt)) {
       ++racy;
       best = min(best, i);
     }
-  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     racy += __shfl_xor_sync(0xffffffffu, racy, o);
@@ -218,21 +203,19 @@ extern "C" cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, 
 
 extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes,
                                                uint32_t w_tid, MapcCtrl* ctrl, int n_sms, int ctas_per_sm,
-                                               cudaStream_t s, int clear) {
+                                               cudaStream_t s) {
   if (cells == 0) return cudaSuccess;
   const unsigned long long vec = (cells * cell_bytes + 15) / 16;
   const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
   const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 16);
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  if (cell_bytes == 2 && clear)
-    mapk::k_direct_scan<uint16_t, true><<<grid, mapk::DS_THREADS, 0, s>>>((uint16_t*)tab, cells, w_tid, ctrl);
-  else if (cell_bytes == 2)
-    mapk::k_direct_scan<uint16_t><<<grid, mapk::DS_THREADS, 0, s>>>((uint16_t*)tab, cells, w_tid, ctrl);
+  if (cell_bytes == 2)
+    mapk::k_direct_scan<uint16_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
   else if (cell_bytes == 4)
-    mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((uint32_t*)tab, cells, w_tid, ctrl);
+    mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
   else
     mapk::k_direct_scan<unsigned long long>
-        <<<grid, mapk::DS_THREADS, 0, s>>>((unsigned long long*)tab, cells, w_tid, ctrl);
+        <<<grid, mapk::DS_THREADS, 0, s>>>((const unsigned long long*)tab, cells, w_tid, ctrl);
   return cudaGetLastError();
 }
 
