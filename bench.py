@@ -222,7 +222,12 @@ def ncu_direct():
         return {}
 
 
-def issue_roofline(kern, hbm):
+# Global red.or.b64 ceiling into a 2 GiB (HBM-resident) table, measured on this pool's
+# B200s: 4.03 TB/s of 8-byte payload (profiles/r1h_red_width_microbench.txt).
+RED64_CEILING_TBS = 4.03
+
+
+def issue_roofline(kern, hbm, acc_per_launch=None):
     """The direct generate: primary view HBM (2 x table bytes per launch over its live
     CUDA-event time; DRAM traffic = algorithmic in the committed ncu capture).  Since the
     r1t/r1u instruction cuts it is no longer issue-bound (issue ~61% alone, r1w): what
@@ -238,6 +243,14 @@ def issue_roofline(kern, hbm):
     per_launch_s = k["ms"] / 1e3 / k["launches"]
     achieved = inst / per_launch_s / 1e9
     out = dict(hbm)
+    if acc_per_launch:
+        # 16-bit cells in aligned quads: one red.or.b64 per 4 accesses (5a: every site
+        # unit-stride, every quad aligned)
+        red_tbs = acc_per_launch / 4 * 8 / per_launch_s / 1e12
+        out["red"] = {"achieved": red_tbs, "peak": RED64_CEILING_TBS, "unit": "TB/s of red.or.b64 payload",
+                      "peak_kind": "measured microbenchmark (profiles/r1h_red_width_microbench.txt)",
+                      "frac": red_tbs / RED64_CEILING_TBS,
+                      "work_model": "accesses / 4 red.or.b64 of 8 B per launch"}
     out["alu"] = {"achieved": achieved, "peak": ISSUE_PEAK_G,
                   "peak_kind": "derived: 148 SMs x 4 schedulers x 1.965 GHz (one warp-instruction per scheduler-cycle)",
                   "unit": "G warp-inst/s", "frac": achieved / ISSUE_PEAK_G,
@@ -351,7 +364,8 @@ def main():
     dominant = max(ROOFLINE_MODELS, key=ms_of)
     roofline = kernel_roofline(kern, dominant, peak, peak_kind)
     if dominant == "direct":
-        roofline = issue_roofline(kern, roofline)
+        acc_launch = sum(r.n_accesses for r in results) / max(1, kern.get("direct", {}).get("launches", 0))
+        roofline = issue_roofline(kern, roofline, acc_launch)
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
     pipe_bytes = sum(v["bytes"] for v in kern.values())
     # the dominant kernel alone: the direct path's chunks run one after another
@@ -361,8 +375,10 @@ def main():
         solo = [prog.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank,
                                  world=world, profile=True, detect=args.detect, overlap=False) for _ in range(2)]
         k_solo = kernel_table(solo[1:])
-        r_solo = issue_roofline(k_solo, kernel_roofline(k_solo, "direct", peak, peak_kind))
+        r_solo = issue_roofline(k_solo, kernel_roofline(k_solo, "direct", peak, peak_kind),
+                                solo[1].n_accesses / max(1, k_solo.get("direct", {}).get("launches", 0)))
         roofline["solo"] = {"achieved": r_solo["achieved"], "frac": r_solo["frac"], "unit": r_solo["unit"],
+                            "red_frac": r_solo.get("red", {}).get("frac"),
                             "note": "same kernel, chunks run sequentially (no concurrent scans)"}
     kernels_out = {k: {"ms_per_step": v["ms"] / len(results), "share": v["ms"] / kern_total,
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,
