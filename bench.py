@@ -5,18 +5,24 @@ Workload (BASELINE.json configs[4], the metric's headline config): the
 synthetic 3-deep loop stencil MAP of SURVEY.md §8d, 2^34 accesses
 (blockDim 1024, T=16 barrier phases, R=256 rows/thread, C=1024 columns,
 ping-pong buffers -> DRF), checked exhaustively: one step = generate + radix
-sort + detect over every access of every phase (all of §8 rows a1-a3).
+(detect path chosen per chunk) over every access of every phase.
 The detect path is the library's automatic choice (for 5a: the sort-free
 direct-address table, SURVEY.md §8f NEXT-3 -- every access folded into its
-cell with one atomic OR, the table scanned once); `--detect table|sort` forces
+cell with one atomic OR, the table scanned once; no key is materialised and
+nothing is sorted); `--detect table|sort` forces
 the bucket-table path (partial LSD sort + shared-memory tables) or the full LSD
 sort + segmented scan (the north_star's generate -> sort -> detect), and the
 line also reports both of those paths' throughput on the same run
 ("detect_paths") and the radix pass's roofline ("roofline_sort_path").
 
-Contract: `python bench.py --gpus N --steps K --warmup W` (torchrun for N>1,
-one rank per GPU; chunks are dealt round-robin to ranks, strong scaling on the
-fixed 2^34-access workload).  Rank 0 prints ONE JSON line.  `--impl reference`
+Contract: `python bench.py --gpus N --steps K --warmup W` (one rank per GPU;
+for N>1 under torchrun, or, when started without WORLD_SIZE, bench.py
+re-launches itself under torch.distributed.run with N processes).  The plan is
+cut into >= 2 chunks per rank (map_default_chunk) and every rank runs a
+contiguous, bound-balanced range of chunks (map_rank_chunks) with no data-path
+collective -- strong scaling on the fixed 2^34-access workload; `--mode
+exchange` instead runs the north_star's key exchange (hash-bucketed generate ->
+NCCL all_to_all -> local sort + detect).  Rank 0 prints ONE JSON line.  `--impl reference`
 times the CPU oracle (the only reference this paper has) on a bounded sample.
 """
 from __future__ import annotations
@@ -53,6 +59,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--detect", choices=["auto", "direct", "sort", "table"], default="auto")
     ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect paths")
+    ap.add_argument("--mode", choices=["shard", "exchange"], default="shard",
+                    help="multi-GPU mode: chunk sharding (default) or the key exchange (all_to_all)")
     return ap.parse_args()
 
 
@@ -169,7 +177,7 @@ def reference_arm(args, rank, world):
     tot = sum(times)
     value = n * len(times) / tot / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "ranks": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic", "config": {"workload": workload_desc(inst), "sample": sample_text(samp)},
@@ -293,9 +301,30 @@ def kernel_table(results):
     return kern
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def relaunch(n):
+    """--gpus N > 1 without a torchrun environment: run this script as N ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -304,6 +333,9 @@ def main():
             import torch.distributed as dist
             dist.init_process_group("gloo")
         reference_arm(args, rank, world)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
         return
 
     import torch
@@ -317,11 +349,17 @@ def main():
     inst = config(args.config)
     prog = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
     names = prog.array_names()
+    if not args.chunk:
+        args.chunk = prog.default_chunk(world)
     scratch = torch.empty(prog.scratch_bytes(args.chunk), dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
     n_chunks = prog.n_chunks(args.chunk)
+    my_chunks = prog.rank_chunks(rank, world, args.chunk)
 
     def step(profile=False, detect=args.detect):
+        if args.mode == "exchange" and world > 1:
+            from paper_2203_12878_b200.dist import check_races_exchange
+            return check_races_exchange(prog, scratch, stream, args.chunk)
         r = prog.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank,
                              world=world, profile=profile, detect=detect)
         if world > 1:
@@ -438,7 +476,9 @@ def main():
                 roof_sort["path"] = "table (partial LSD sort + bucket tables)"
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if world > 1:
+        dist.barrier()          # the GPU timing is done on every rank before the CPU leg
+    if rank == 0 and not args.no_cpu_baseline:
         samp = oracle_sample(inst, args.cpu_rows)
         cores = os.cpu_count() or 1
         orc, dt = run_oracle(samp, cores)
@@ -452,9 +492,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max / len(results), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": workload_desc(inst), "n_accesses": r0.n_accesses, "chunks": n_chunks,
-                       "chunk_max_accesses": args.chunk or "default (2^30)", "parallelism": f"chunks dealt over {world} GPU(s)",
-                       "l2": "inputs larger than L2: a 2 GiB direct-address table (or 8 GiB of keys) per chunk "
-                             "vs 126 MB L2; no flush needed",
+                       "chunk_max_accesses": args.chunk, "rank0_chunks": len(my_chunks),
+                       "parallelism": (f"dp{world}: each rank a contiguous bound-balanced range of chunks, no "
+                                       f"data-path collective" if args.mode == "shard" else
+                                       f"key exchange over {world} ranks (all_to_all_single)"),
+                       "l2": "inputs larger than L2: a 1 GiB direct-address table of 16-bit cells (or 8 GiB of "
+                             "keys) per chunk vs 126 MB L2; no flush needed",
                        "verdict": "racy" if r0.verdict else "drf",
                        "witness": list(r0.witness.as_tuple()) if r0.witness else None},
             "roofline": roofline,

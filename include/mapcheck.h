@@ -111,8 +111,9 @@ typedef struct {
   void *scratch;              /* device buffer, >= map_scratch_bytes(p, chunk)        */
   size_t scratch_bytes;
   uint64_t chunk_max_accesses;/* accesses per chunk (0 = library default)            */
-  uint32_t rank, world;       /* shard: process chunks c with c % world == rank
-                                 (world 0 or 1 = all chunks; multi-GPU) */
+  uint32_t rank, world;       /* shard: process rank `rank`'s chunks of `world`
+                                 (map_rank_chunks: a contiguous, bound-balanced range;
+                                 world 0 or 1 = all chunks; multi-GPU) */
   map_kernel_stats *stats;    /* optional per-kernel timings (NULL = off)            */
   uint32_t flags;             /* MAP_GEN_* (generate path); 0 = automatic            */
 } map_exec;
@@ -202,8 +203,12 @@ map_status map_info_get(const map_program *p, map_info *out);
  * accesses (0 = the largest (phase, block) unit of this program). */
 size_t map_scratch_bytes(const map_program *p, uint64_t chunk_max_accesses);
 
-/* Run the whole pipeline (generate -> radix sort -> detect per chunk) on one
- * GPU; blocking.  Writes verdict, counts and timing to *out. */
+/* Run the whole pipeline on one GPU; blocking.  Per chunk: generate, then the
+ * detect path map_exec.flags selects -- by default the sort-free direct-address
+ * table for dense chunks (MAP_DETECT_DIRECT below), else partial sort + bucket
+ * tables or full radix sort + segmented scan.  Writes verdict, counts and
+ * timing to *out.  With chunk_max_accesses == 0 and world > 1 the plan uses
+ * map_default_chunk(p, world) (size the scratch with that value). */
 map_status map_check_races(map_program *p, const map_exec *ex, map_result *out);
 
 /* Canonical witness of the last racy map_check_races; MAP_E_ARG if it was DRF. */
@@ -235,6 +240,17 @@ const char *map_status_str(map_status s);
  * map_chunk_count / map_chunk_info: the plan's chunks (same plan as
  * map_check_races for the same chunk_max_accesses; 0 = library default). */
 map_status map_chunk_count(const map_program *p, uint64_t chunk_max_accesses, uint32_t *n_chunks);
+/* Default chunk capacity (accesses) for a job sharded over `world` ranks: the
+ * single-GPU default (world <= 1), or smaller so that the plan has at least two
+ * chunks per rank where its (phase, block) units allow (PAPER.md:179-182:
+ * phases and blocks are independent units).  0 if p is NULL. */
+uint64_t map_default_chunk(const map_program *p, uint32_t world);
+/* The chunk indices rank `rank` of `world` processes in map_check_races (a
+ * contiguous range balanced by chunk bound): out[cap] (HOST) receives the first
+ * min(cap, *n) of them, *n their number.  chunk_max_accesses 0 = the default
+ * for that world.  Errors: MAP_E_ARG, plan errors as map_check_races. */
+map_status map_rank_chunks(const map_program *p, uint64_t chunk_max_accesses, uint32_t rank, uint32_t world,
+                           uint32_t *out, uint32_t cap, uint32_t *n);
 typedef struct {
   uint32_t phase_lo, phase_hi;   /* inclusive range of barrier phases                 */
   uint32_t block_lo, block_hi;   /* [block_lo, block_hi)                              */

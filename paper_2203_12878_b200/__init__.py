@@ -39,6 +39,7 @@ EXPORTS = (
     "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
     "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
     "map_sort_detect", "map_unpack_witness", "map_array_name", "map_chunk_info", "map_list_races",
+    "map_default_chunk", "map_rank_chunks",
 )
 
 
@@ -120,6 +121,11 @@ _lib.map_sort_detect.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.c_uint32, cty
 _lib.map_sort_detect.restype = ctypes.c_int
 _lib.map_unpack_witness.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint64, ctypes.POINTER(_Witness)]
 _lib.map_unpack_witness.restype = ctypes.c_int
+_lib.map_default_chunk.argtypes = [_P, ctypes.c_uint32]
+_lib.map_default_chunk.restype = ctypes.c_uint64
+_lib.map_rank_chunks.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32,
+                                 ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
+_lib.map_rank_chunks.restype = ctypes.c_int
 _lib.map_chunk_info.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_ChunkDesc)]
 _lib.map_chunk_info.restype = ctypes.c_int
 _lib.map_list_races.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.POINTER(_Witness), ctypes.c_uint64,
@@ -333,6 +339,20 @@ class MapProgram:
             raise MapError(9, _lib.map_last_error(self._h).decode())
         return n
 
+    def default_chunk(self, world: int = 1) -> int:
+        """map_default_chunk: the chunk capacity a `world`-rank job uses by default."""
+        return int(_lib.map_default_chunk(self._h, int(world)))
+
+    def rank_chunks(self, rank: int, world: int, chunk_max_accesses: int = 0):
+        """map_rank_chunks: the chunk indices rank `rank` of `world` processes."""
+        n = ctypes.c_uint32()
+        st = _lib.map_rank_chunks(self._h, int(chunk_max_accesses), int(rank), int(world), None, 0, ctypes.byref(n))
+        if st != 0:
+            raise MapError(st, _lib.map_last_error(self._h).decode())
+        buf = (ctypes.c_uint32 * max(1, n.value))()
+        _lib.map_rank_chunks(self._h, int(chunk_max_accesses), int(rank), int(world), buf, n.value, ctypes.byref(n))
+        return list(buf[:n.value])
+
     def n_chunks(self, chunk_max_accesses: int = 0) -> int:
         c = ctypes.c_uint32()
         st = _lib.map_chunk_count(self._h, int(chunk_max_accesses), ctypes.byref(c))
@@ -347,7 +367,8 @@ class MapProgram:
 
         scratch: a torch uint8 CUDA tensor of >= scratch_bytes() bytes (allocated here if None);
         stream: a torch.cuda.Stream (default: the current stream);
-        rank/world: process only chunks c with c % world == rank (multi-GPU sharding);
+        rank/world: process only rank `rank`'s chunks (rank_chunks; multi-GPU sharding; with
+                    chunk_max_accesses 0 the plan uses default_chunk(world));
         profile: record CUDA events around every launch and return per-kernel-class timings;
         gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised);
         detect: "auto" | "direct" | "table" | "sort" (include/mapcheck.h MAP_DETECT_*);
@@ -356,6 +377,8 @@ class MapProgram:
         if not torch.cuda.is_available():
             raise MapError(6, "no CUDA device (there is no CPU fallback)")
         dev = torch.cuda.current_device() if device is None else int(device)
+        if not chunk_max_accesses and world > 1:
+            chunk_max_accesses = self.default_chunk(world)
         need = self.scratch_bytes(chunk_max_accesses)
         if scratch is None:
             scratch = torch.empty(need, dtype=torch.uint8, device=f"cuda:{dev}")

@@ -341,8 +341,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     for (const MapcOp& op : pg.ops) ne += (op.code & MAPC_CODE_MASK) == VM_EMIT;
     const int NE = std::max(ne, 1);
     const std::string cell =
-        "const u64 idx_ = (u64)(IX) - IDX_LO; if (WI < 64 && (idx_ >> WI) != 0) err |= " +
-        std::to_string(MAPC_ERR_LAYOUT) + "u; " +
+        "u64 idx_ = (u64)(IX) - IDX_LO; if (WI < 64 && (idx_ >> WI) != 0) { err |= " +
+        std::to_string(MAPC_ERR_LAYOUT) + "u; idx_ = 0; } " +
         (sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
               : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
         (cell_bytes == 2 ? std::string("const u32 cd_ = tcd_ | ((u32)(KIND) << 14); ")
@@ -470,8 +470,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "    if (!skip_) {\n";
     }
     s << "    u32 cnt = 0;\n"
-      << "#define EMIT_KEY(IX, ARR, KIND) { const u64 idx_ = (u64)(IX) - IDX_LO; "
-         "if (WI < 64 && (idx_ >> WI) != 0) err |= " << MAPC_ERR_LAYOUT << "u; "
+      << "#define EMIT_KEY(IX, ARR, KIND) { u64 idx_ = (u64)(IX) - IDX_LO; "
+         "if (WI < 64 && (idx_ >> WI) != 0) { err |= " << MAPC_ERR_LAYOUT << "u; idx_ = 0; } "
          "const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; "
          << emit_tail(mode, ch.lay.w_tid, T) << " }\n"
       << "    switch (sg.prog_begin) {\n";

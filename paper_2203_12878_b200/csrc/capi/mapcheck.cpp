@@ -490,6 +490,42 @@ uint64_t default_cap(const map_program* p) {
   return std::max<uint64_t>({want, p->C.max_unit, 1});
 }
 
+// Default chunk capacity for a job sharded over `world` ranks: at least two
+// chunks per rank where the plan's units allow it (every rank busy, and each
+// rank can overlap one chunk's table scan with the next one's generate).
+uint64_t default_cap_world(const map_program* p, uint32_t world) {
+  const uint64_t base = default_cap(p);
+  if (world <= 1) return base;
+  const uint64_t want = (p->C.max_accesses + 2ull * world - 1) / (2ull * world);
+  return std::max<uint64_t>({std::min(base, want), p->C.max_unit, 1});
+}
+
+// The chunks rank `rank` of `world` processes: a contiguous range, split where
+// the running sum of chunk bounds crosses rank/world of the total (chunk c goes
+// to the rank owning the midpoint of its bound), so ranks get equal work and
+// each rank's chunks stay consecutive (the overlapped direct pipeline pairs
+// neighbours).  Ranks beyond the chunk count get none.
+std::vector<size_t> rank_chunks(const Plan& P, uint32_t rank, uint32_t world) {
+  std::vector<size_t> mine;
+  if (world <= 1) {
+    for (size_t c = 0; c < P.chunks.size(); ++c) mine.push_back(c);
+    return mine;
+  }
+  unsigned __int128 total = 0;
+  for (const Chunk& ch : P.chunks) total += std::max<uint64_t>(ch.bound, 1);
+  unsigned __int128 run = 0;
+  for (size_t c = 0; c < P.chunks.size(); ++c) {
+    const uint64_t b = std::max<uint64_t>(P.chunks[c].bound, 1);
+    const unsigned __int128 mid2 = 2 * run + b;                      // 2 x midpoint
+    uint32_t owner = (uint32_t)(mid2 * world / (2 * total));
+    if (P.chunks.size() <= world) owner = (uint32_t)c;               // one chunk per rank
+    if (owner >= world) owner = world - 1;
+    if (owner == rank) mine.push_back(c);
+    run += b;
+  }
+  return mine;
+}
+
 #define CK(expr)                                           \
   do {                                                     \
     cudaError_t e_ = (expr);                               \
@@ -598,7 +634,10 @@ size_t map_scratch_bytes(const map_program* cp, uint64_t chunk_max_accesses) {
 map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) {
   if (!p || !ex || !out) return MAP_E_ARG;
   p->have_witness = false;
-  const uint64_t cap = ex->chunk_max_accesses ? ex->chunk_max_accesses : default_cap(p);
+  const uint32_t world = ex->world ? ex->world : 1;
+  const uint32_t rank = ex->rank;
+  if (rank >= world) return MAP_E_ARG;
+  const uint64_t cap = ex->chunk_max_accesses ? ex->chunk_max_accesses : default_cap_world(p, world);
   map_status st = ensure_plan(p, cap);
   if (st != MAP_OK) return st;
   Plan& P = p->plan;
@@ -616,6 +655,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   CK(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, ex->device));
   cudaStream_t s = (cudaStream_t)ex->stream;
   if (p->pinned_bytes < P.stage_bytes) {
+    // a captured graph reads the staging buffer: it dies with it
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+    p->gkey.clear();
+    p->glast_key.clear();
     if (p->pinned) cudaFreeHost(p->pinned);
     p->pinned = nullptr;
     p->pinned_bytes = 0;
@@ -657,12 +700,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   const int gen_mode = gsel == MAP_GEN_VM    ? 0
                        : gsel == MAP_GEN_JIT ? 1
                                              : (p->C.max_accesses >= (1ull << 23) && P.chunks.size() <= 64 ? 1 : 0);
-  const uint32_t world = ex->world ? ex->world : 1;
-  const uint32_t rank = ex->rank;
-  if (rank >= world) return MAP_E_ARG;
-  std::vector<size_t> mine;          // this rank's chunks (multi-GPU: c % world == rank)
-  for (size_t c = 0; c < P.chunks.size(); ++c)
-    if (c % world == rank) mine.push_back(c);
+  const std::vector<size_t> mine = rank_chunks(P, rank, world);   // this rank's chunks
   if (gen_mode == 1 && !mine.empty()) {
     // the kernels this run needs, per mode: keys (sort / table detect), direct +
     // filter (direct detect), for this rank's chunks only
@@ -834,8 +872,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
       end_on(m, s2);
       if (i + 2 < mine.size()) {
+        // cleared for its next user, chunk i+2, whose table may be larger
+        const Chunk& nx = P.chunks[mine[i + 2]];
         m = begin_on(MAP_K_CLEAR, s2);
-        CK(mapc_launch_table_clear(tb, tbytes, n_sms, ovl_side_ctas, s2));
+        CK(mapc_launch_table_clear(tb, nx.cells * nx.cell_bytes, n_sms, ovl_side_ctas, s2));
         end_on(m, s2);
       }
       m = begin_on(MAP_K_OTHER, s2);
@@ -976,6 +1016,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     const uint64_t plan_for = p->plan_for;
     put(&plan_for, 8); put(&ex->flags, 4); put(&ex->scratch, sizeof(void*)); put(&ex->scratch_bytes, 8);
     put(&ex->stream, sizeof(void*)); put(&ex->device, 4); put(&rank, 4); put(&world, 4); put(&gen_mode, 4);
+    put(&p->pinned, sizeof(void*));
   }
   // (not with the look-back onesweep variant: its epochs must advance every run)
   const bool use_graph = graphs_env && !prof && !mine.empty() && sort_mode == 1;
@@ -1111,7 +1152,23 @@ void map_program_free(map_program* p) {
   delete p;
 }
 
-// ---- stage API: implemented in a later milestone ----
+uint64_t map_default_chunk(const map_program* p, uint32_t world) {
+  return p ? default_cap_world(p, world) : 0;
+}
+
+map_status map_rank_chunks(const map_program* cp, uint64_t chunk_max_accesses, uint32_t rank, uint32_t world,
+                           uint32_t* out, uint32_t cap, uint32_t* n) {
+  if (!cp || !n || (cap && !out) || (world && rank >= world)) return MAP_E_ARG;
+  map_program* p = const_cast<map_program*>(cp);
+  const uint32_t w = world ? world : 1;
+  map_status st = ensure_plan(p, chunk_max_accesses ? chunk_max_accesses : default_cap_world(p, w));
+  if (st != MAP_OK) return st;
+  const std::vector<size_t> mine = rank_chunks(p->plan, rank, w);
+  for (size_t i = 0; i < mine.size() && i < cap; ++i) out[i] = (uint32_t)mine[i];
+  *n = (uint32_t)mine.size();
+  return MAP_OK;
+}
+
 map_status map_chunk_count(const map_program* cp, uint64_t chunk_max_accesses, uint32_t* n_chunks) {
   if (!cp || !n_chunks) return MAP_E_ARG;
   map_program* p = const_cast<map_program*>(cp);

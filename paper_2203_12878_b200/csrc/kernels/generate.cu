@@ -177,8 +177,10 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             if (!(act[v] && valid[v])) continue;
-            const unsigned long long idx = (unsigned long long)AV(v) - lay.idx_lo;
-            if (lay.w_index < 64 && (idx >> lay.w_index) != 0) err |= MAPC_ERR_LAYOUT;
+            unsigned long long idx = (unsigned long long)AV(v) - lay.idx_lo;
+            // outside the layout (a compiler bug guard): flag it and fold into cell 0
+            // of the chunk instead, so no reduction can leave the table
+            if (lay.w_index < 64 && (idx >> lay.w_index) != 0) { err |= MAPC_ERR_LAYOUT; idx = 0; }
             const unsigned long long sf = sg.key_hi + arr + ((unsigned long long)lbv[v] << lay.w_index) + idx;
             if (mode == MAPC_MODE_DIRECT) {
               const unsigned long long code =

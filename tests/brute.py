@@ -263,10 +263,14 @@ def _cond(c, env):
         return True
     if k == "false":
         return False
+    # DESIGN.md R2: both operands of and/or are evaluated (no short circuit), so a
+    # division by zero in either operand is reached whenever the condition is
     if k == "and":
-        return _cond(c[1], env) and _cond(c[2], env)
+        x, y = _cond(c[1], env), _cond(c[2], env)
+        return x and y
     if k == "or":
-        return _cond(c[1], env) or _cond(c[2], env)
+        x, y = _cond(c[1], env), _cond(c[2], env)
+        return x or y
     _, op, a, b = c
     x, y = _num(a, env), _num(b, env)
     return {"=": x == y, "!=": x != y, "<": x < y, "<=": x <= y, ">": x > y, ">=": x >= y}[op]

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_functions():
     with open(os.path.join(ROOT, "include", "mapcheck.h")) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^\s*(?:map_status|size_t|void|const char \*)\s*\**\s*(map_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:map_status|size_t|void|uint64_t|int|const char \*)\s*\**\s*(map_\w+)\s*\(", text, re.M)))
 
 
 def test_header_symbols_exported():
@@ -93,7 +93,7 @@ def test_plans_keep_direct_tables_l2_sized():
     ("rd[", 1), ("forU x 0..3 { rd[x] }", 1), ("rd[x]", 2), ("rd Q[0]", 2),
     ("forU x in 0..2 { forU x in 0..2 { rd[x] } }", 2),
     ("if (tid = 0) { sync } else { skip }", 3), ("forU x in 0..2 { sync }", 3),
-    ("forS x in 0..tid { sync }", 3), ("rd[18446744073709551615 + 1]", 4),
+    ("forS x in 0..tid { sync }", 3), ("rd[18446744073709551615 + 1]", 4), ("rd[18446744073709551616]", 4),
     ("forS x in 0..(1 / 0) { sync }", 5),
 ])
 def test_compile_errors_match_oracle(src, status):
@@ -210,3 +210,9 @@ def test_unit_stride_sites():
     for body, want in cases:
         got = _us_flags(head + body + tail, {"C": 64})
         assert got[: len(want)] == want, (body, got)
+
+
+def test_literal_max_accepted():
+    # 2^64 - 1 is a natural literal on both sides (R3)
+    assert oracle.check("rd[18446744073709551615 - tid]", block=(2, 1, 1)).status == 0
+    mc.MapProgram("rd[18446744073709551615 - tid]", block=(2, 1, 1))

@@ -1,7 +1,7 @@
 """Multi-GPU host logic on CPU: world_size-2 gloo process group.
 
 The GPU step is replaced by per-rank synthetic results (each rank would have
-processed chunks c % world == rank); what is tested is the cross-rank reduction
+processed its share of the chunks, map_rank_chunks); what is tested is the cross-rank reduction
 of paper_2203_12878_b200.dist: summed counts and the lexicographic minimum
 witness, identical on every rank.
 """
@@ -71,17 +71,26 @@ def test_reduce_results_world2(case):
             assert name == ["A", "B"][w[1]]
 
 
-def test_chunk_sharding_covers_all_chunks():
-    # rank r runs chunks c with c % world == r: every chunk exactly once
+@pytest.mark.parametrize("name", ["3a", "3b", "4a", "4b", "5a", "5b"])
+def test_chunk_sharding_covers_all_chunks(name):
+    # map_rank_chunks (the shard map_check_races runs): every chunk exactly once,
+    # contiguous per rank, every rank busy on the large configs, balanced bounds
     import paper_2203_12878_b200 as mc
     from workloads import config
-    inst = config("5a")
-    n = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params).n_chunks()
+    inst = config(name)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
     for world in (1, 2, 4, 8):
-        seen = sorted(c for r in range(world) for c in range(n) if c % world == r)
-        assert seen == list(range(n))
-        per = [sum(1 for c in range(n) if c % world == r) for r in range(world)]
-        assert max(per) - min(per) <= 1
+        chunk = p.default_chunk(world)
+        n = p.n_chunks(chunk)
+        shares = [p.rank_chunks(r, world, chunk) for r in range(world)]
+        assert sorted(c for s in shares for c in s) == list(range(n))
+        for s in shares:
+            assert s == list(range(s[0], s[0] + len(s))) if s else True
+        if world > 1:
+            assert n >= world, (name, world, n)
+            assert all(len(s) >= 1 for s in shares)
+            work = [sum(p.chunk_info(c, chunk)["bound"] for c in s) for s in shares]
+            assert max(work) <= 2 * (sum(work) / world), (name, world, work)
 
 
 # ---- key-exchange mode orchestration (dist.check_races_exchange) -------------

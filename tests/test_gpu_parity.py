@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 import paper_2203_12878_b200 as mc
-from tests.test_oracle import CASES, n_closed, witness_closed
+from tests.test_oracle import CASES, n_closed, racy_closed, witness_closed
 from workloads import config, fuzz
 
 pytestmark = pytest.mark.gpu
@@ -100,9 +100,9 @@ def test_full_size_stencil_properties(name):
     assert r.n_accesses == n_closed(name, inst) == 2**34
     w = witness_closed(name, inst)
     assert (r.witness.as_tuple() if r.witness else None) == w
-    if name == "5b":
-        # every cell of every phase holds the owner's write and a neighbour's read
-        assert r.racy_segments > 0
+    # exact racy-cell count: 0 for 5a, T*B*C*min(R, 2) = 2^25 for 5b (closed form
+    # pinned against the brute force and the oracle in tests/test_oracle.py)
+    assert r.racy_segments == racy_closed(name, inst) == (0 if name == "5a" else 2**25)
 
 
 def test_long_segment_spans_many_tiles():

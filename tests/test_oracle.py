@@ -117,6 +117,52 @@ def witness_closed(name, inst):
         return (0, 0, 0, 0, 0, 1 if p["R"] == 1 else B - 1, WR, RD)
 
 
+def racy_closed(name, inst):
+    """Racy (phase, array, block, index) cells of the stencil configs.  5a: none
+    (ping-pong halves; each cell of the write half has one writer and no reader).
+    5b (in place): row tid*R is read by the owner of row tid*R - 1 (its r+1
+    neighbour) and row tid*R + R - 1 by the owner of row tid*R + R (its r-1
+    neighbour); every other row is touched by its owner only.  So min(R, 2)
+    racy rows of C cells per thread per phase, when there are >= 2 threads."""
+    p, B = inst.params, inst.n_threads
+    if name == "5a":
+        return 0
+    if name == "5b":
+        return p["T"] * B * p["C"] * min(p["R"], 2) if B >= 2 else 0
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("sizes", [dict(block=2, T=1, R=1, C=3), dict(block=4, T=2, R=3, C=5),
+                                   dict(block=8, T=3, R=2, C=4), dict(block=1, T=2, R=3, C=2),
+                                   dict(block=16, T=1, R=5, C=7)])
+@pytest.mark.parametrize("name", ["5a", "5b"])
+def test_stencil_racy_count_closed_form(name, sizes):
+    # pinned against the L0 brute force's all-pairs count and the oracle
+    inst = config(name, **sizes)
+    r = _check(inst)
+    assert r.n_racy_segments == racy_closed(name, inst)
+    assert len(brute.race_list(brute.config_records(inst))) == racy_closed(name, inst)
+
+
+def test_and_or_evaluate_both_operands():
+    # DESIGN.md R2 (P:201 leaves the boolean operators unspecified): both operands
+    # of and/or are evaluated, so the division by zero in the right operand is
+    # reached even though the left one already decides the condition
+    for src in ["if (tid = 9 and 1 / (tid - tid) = 0) { wr[0] } else { skip }",
+                "if (tid < 9 or 1 % (tid - tid) = 0) { wr[0] } else { skip }"]:
+        assert oracle.check(src, block=(4, 1, 1)).status == 5
+    # without the faulting operand both are plain conditions
+    r = oracle.check("if (tid = 2 or tid = 3) { wr[0] } else { skip }", block=(4, 1, 1))
+    assert r.status == 0 and r.witness == (0, 0, 0, 0, 2, 3, WR, WR)
+
+
+def test_literal_bounds():
+    # naturals are exact u64 (DESIGN.md R3): 2^64 - 1 is a literal, 2^64 is not
+    r = oracle.check("rd[18446744073709551615 - tid]", block=(2, 1, 1))
+    assert r.status == 0 and r.n_accesses == 2 and r.verdict == 0
+    assert oracle.check("rd[18446744073709551616]", block=(2, 1, 1)).status == 4
+
+
 @pytest.mark.parametrize("name,sizes", CASES, ids=[f"{n}-{i}" for i, (n, _) in enumerate(CASES)])
 def test_closed_forms(name, sizes):
     inst = config(name, **sizes)

@@ -144,11 +144,16 @@ def random_program(seed: int) -> dict:
     return {"params": params, "arrays": arrays, "body": body}
 
 
-def random_instance(seed: int) -> tuple[Instance, dict]:
-    """(instance, ast) for fuzz seed ``seed``."""
+def random_instance(seed: int, big_block: bool = False) -> tuple[Instance, dict]:
+    """(instance, ast) for fuzz seed ``seed``; ``big_block`` draws blockDim from
+    1025..2048 (as (1024, 2, 1)-shaped or flat dims) instead of <= 16."""
     prog = random_program(seed)
     r = random.Random(seed ^ 0x5EED)
-    block = (r.choice([1, 2, 3, 4, 5, 8, 16]), 1, 1)
+    if big_block:
+        n = r.randint(1025, 2048)
+        block = (1024, 2, 1) if n == 2048 else (n, 1, 1)
+    else:
+        block = (r.choice([1, 2, 3, 4, 5, 8, 16]), 1, 1)
     grid = (r.choice([1, 1, 2]), 1, 1)
     params = {p: r.randint(0, 4) for p in prog["params"]}
     return Instance(f"fuzz{seed}", to_text(prog), grid=grid, block=block, params=params), prog
