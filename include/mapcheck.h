@@ -61,7 +61,8 @@ typedef enum {
   MAP_E_CUDA = 6,    /* CUDA error or no device                                          */
   MAP_E_COMM = 7,    /* reserved for the multi-GPU orchestration (NCCL lives in Python)  */
   MAP_E_ARG = 8,     /* bad argument: null pointer, missing/unknown parameter, ...       */
-  MAP_E_NOMEM = 9    /* scratch too small for one (phase, block) unit                    */
+  MAP_E_NOMEM = 9,   /* scratch too small for one (phase, block) unit                    */
+  MAP_E_TYPE = 10    /* BabyCUDA kernel is not typable (Fig. 6) and no MAP was requested */
 } map_status;
 
 typedef struct map_program map_program;
@@ -278,6 +279,46 @@ map_status map_generate_bucketed(map_program *p, const map_exec *ex, uint32_t ra
 map_status map_sort_detect(map_program *p, const map_exec *ex, uint32_t chunk, void *keys, uint64_t n,
                            uint64_t *packed_witness, uint64_t *racy_segments);
 map_status map_unpack_witness(const map_program *p, uint32_t chunk, uint64_t packed, map_witness *out);
+
+/* ---- BabyCUDA front end ------------------------------
+ * BabyCUDA (Fig. 5) is the data-carrying kernel language the
+ * paper types into MAPs: `A[n] := m` (write), `let y = A[n] in b` (read into y
+ * for the rest of the block), if/else, `for x in n..m [step s]`, skip, `;`, plus
+ * `sync` (the synchronized fragment) and the declarations
+ * `params P, ...;` and `shared A[extent], B, ...;` (grammar: DESIGN.md §3b).
+ *
+ * map_infer: parse `src` (len bytes) and type it with the behavioural type system
+ * of Fig. 6 (t-n, t-b, t-write, t-read, t-seq, t-if, t-for,
+ * t-skip) under V = {tid, bid} u params.  A kernel is typable iff no value read
+ * from an array reaches an array index, a condition or a loop bound (Eq. 1,
+ * PAPER.md:887-891); by Theorem 1 every race reported on a
+ * typable kernel's MAP is then a TRUE alarm.  *ty (HOST, caller-owned) receives
+ * typable, the kind of the first failing premise (MAP_TYPE_DATA_INDEX: a read
+ * value indexes an array; MAP_TYPE_DATA_CONTROL: it decides a condition or a loop
+ * bound), the offending variable and its line:col.
+ * Output: the MAP text (DESIGN.md §3 grammar, input to map_compile) into
+ * map_out[map_cap] (HOST, NUL-terminated, truncated to map_cap - 1; *map_len =
+ * the full length): the t-rules' image of a typable kernel; for an ill-typed
+ * one, when data_domain > 0, the DATA-ABSTRACTED MAP in which a read whose value
+ * reaches a typed position becomes `rd A[n]; forU y in 0..data_domain { u }` (the
+ * value may be anything in [0, data_domain): Faial's view of array data,
+ * PAPER.md:880-885; its races may be false alarms).
+ * Returns MAP_OK, MAP_E_TYPE (ill-typed and data_domain == 0; *ty filled, no
+ * text), MAP_E_PARSE / MAP_E_SCOPE (unbound or shadowing name) / MAP_E_BARRIER
+ * (sync under if, or a loop around a sync whose bounds depend on tid, bid or a
+ * read value) / MAP_E_RANGE (literal >= 2^64) with "line:col: message" in diag,
+ * MAP_E_ARG (null pointers). */
+#define MAP_TYPE_OK 0
+#define MAP_TYPE_DATA_INDEX 1
+#define MAP_TYPE_DATA_CONTROL 2
+typedef struct {
+  int32_t typable;
+  int32_t kind;              /* MAP_TYPE_*                                      */
+  uint32_t line, col;        /* first offending use (1-based)                   */
+  char var[64];              /* its variable (NUL-terminated, truncated)        */
+} map_typing;
+map_status map_infer(const char *src, size_t len, uint64_t data_domain, char *map_out, size_t map_cap,
+                     size_t *map_len, map_typing *ty, char *diag, size_t diag_cap);
 
 #ifdef __cplusplus
 }

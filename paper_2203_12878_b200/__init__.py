@@ -32,14 +32,14 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 STATUS = {
     0: "MAP_OK", 1: "MAP_E_PARSE", 2: "MAP_E_SCOPE", 3: "MAP_E_BARRIER", 4: "MAP_E_RANGE",
-    5: "MAP_E_ARITH", 6: "MAP_E_CUDA", 7: "MAP_E_COMM", 8: "MAP_E_ARG", 9: "MAP_E_NOMEM",
+    5: "MAP_E_ARITH", 6: "MAP_E_CUDA", 7: "MAP_E_COMM", 8: "MAP_E_ARG", 9: "MAP_E_NOMEM", 10: "MAP_E_TYPE",
 }
 
 EXPORTS = (
     "map_compile", "map_info_get", "map_scratch_bytes", "map_check_races", "map_witness_get",
     "map_program_free", "map_status_str", "map_chunk_count", "map_generate_bucketed",
     "map_sort_detect", "map_unpack_witness", "map_array_name", "map_chunk_info", "map_list_races",
-    "map_default_chunk", "map_rank_chunks",
+    "map_default_chunk", "map_rank_chunks", "map_infer",
 )
 
 
@@ -141,6 +141,18 @@ _lib.map_debug_jit_source.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint32, ctyp
 _lib.map_debug_jit_source.restype = ctypes.c_size_t
 _lib.mapc_test_fastdiv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
 _lib.mapc_test_fastdiv.restype = ctypes.c_uint32
+
+
+class _Typing(ctypes.Structure):
+    _fields_ = [("typable", ctypes.c_int32), ("kind", ctypes.c_int32), ("line", ctypes.c_uint32),
+                ("col", ctypes.c_uint32), ("var", ctypes.c_char * 64)]
+
+
+_lib.map_infer.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_size_t,
+                           ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_Typing), ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_infer.restype = ctypes.c_int
+
+TYPE_KINDS = {0: "ok", 1: "data_dependent_index", 2: "data_dependent_control"}
 
 
 class MapError(RuntimeError):
@@ -404,6 +416,37 @@ class MapProgram:
             res.kernels = {k: {"ms": stats.ms[i], "launches": stats.launches[i], "bytes": stats.bytes[i]}
                            for i, k in enumerate(KERNEL_CLASSES)}
         return res
+
+
+@dataclass
+class Inference:
+    """map_infer: the typing outcome of a BabyCUDA kernel and its MAP text."""
+    typable: bool
+    kind: str                     # "ok" | "data_dependent_index" | "data_dependent_control"
+    var: str
+    line: int
+    col: int
+    map_text: Optional[str]       # None when ill-typed and no data domain was given
+
+
+def infer(src: str, data_domain: int = 0) -> Inference:
+    """Type a BabyCUDA kernel (Fig. 6) and infer its MAP (include/mapcheck.h map_infer)."""
+    raw = src.encode()
+    ty = _Typing()
+    n = ctypes.c_size_t()
+    diag = ctypes.create_string_buffer(1024)
+    cap = 4 * len(raw) + 4096
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        st = _lib.map_infer(raw, len(raw), int(data_domain), buf, cap, ctypes.byref(n), ctypes.byref(ty), diag, 1024)
+        if st == 0 and n.value >= cap:
+            cap = n.value + 1
+            continue
+        break
+    if st not in (0, 10):
+        raise MapError(st, diag.value.decode(errors="replace"))
+    return Inference(bool(ty.typable), TYPE_KINDS[ty.kind], ty.var.decode(), ty.line, ty.col,
+                     buf.value.decode() if st == 0 else None)
 
 
 def check(src: str, grid=(1, 1, 1), block=(1, 1, 1), params=None, chunk_max_accesses: int = 0, **kw) -> Result:

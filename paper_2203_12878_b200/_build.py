@@ -13,6 +13,8 @@ SOURCES = [
     "compiler/compile.cpp",
     "capi/mapcheck.cpp",
     "capi/jit.cpp",
+    "capi/bcapi.cpp",
+    "babycuda/bcfront.cpp",
     "kernels/generate.cu",
     "kernels/radix.cu",
     "kernels/detect.cu",
@@ -23,7 +25,7 @@ SOURCES = [
     "kernels/direct.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "kernels/segstate.cuh",
-           "capi/jit.h"]
+           "capi/jit.h", "babycuda/bcfront.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
