@@ -320,6 +320,92 @@ typedef struct {
 map_status map_infer(const char *src, size_t len, uint64_t data_domain, char *map_out, size_t map_cap,
                      size_t *map_len, map_typing *ty, char *diag, size_t diag_cap);
 
+/* ---- BabyCUDA executor and the Theorem-1 differential check (NEXT-2) ---------
+ * map_kernel_compile: parse + type a BabyCUDA kernel (as map_infer) and plan its
+ * execution at the instantiation `inst` (parameters as map_compile; blockDim
+ * <= 1024, CUDA's own limit).  Array extents: as declared (`shared A[n]`), else,
+ * for a typable kernel, the index hull of its inferred MAP; an ill-typed kernel
+ * must declare them (MAP_E_ARG).  The executor kernel is generated as CUDA C and
+ * compiled with NVRTC for sm_100a at the first map_execute.  Errors: as
+ * map_infer, MAP_E_ARG (blockDim > 1024, missing parameter or extent), MAP_E_RANGE
+ * (the access key phase|array|block|index|tid|kind exceeds 64 bits).
+ *
+ * map_execute: run the kernel WITH DATA on the GPU under the semantics of Fig. 5
+ * (PAPER.md:443-589): one CTA per block, CUDA thread t = BabyCUDA thread t; a
+ * read returns lastwrite over the thread's own current record consed onto the
+ * closed phases (own writes of the phase visible, other threads' not,
+ * PAPER.md:482-495), arrays start undefined (bottom reads as 0 and is counted,
+ * DESIGN.md R20), `sync` closes the phase (a cell written by several threads
+ * keeps the smallest writer tid's value, R21).  Every executed access value
+ * (alpha in^ P) is recorded and race-checked exactly as
+ * map_check_races checks a MAP: verdict, canonical witness (map_kernel_witness),
+ * racy cells.  ex->scratch must hold map_kernel_scratch_bytes(k, max_events,
+ * 0, ex->flags) bytes; max_events bounds the executed accesses (typable kernels:
+ * map_kernel_info.max_events is exact).  MAP_EXEC_KEEP_MEMORY (ex->flags) keeps
+ * every block's final array contents for map_kernel_memory.  Errors:
+ * MAP_E_ARITH (division / modulo by zero, loop step zero), MAP_E_RANGE (a value
+ * exceeds 64 bits, or an index reaches its array's extent), MAP_E_NOMEM (more
+ * than max_events accesses -- *out->n_events says how many -- or a thread's
+ * conflict log overflowed), MAP_E_CUDA. */
+typedef struct map_kernel map_kernel;
+map_status map_kernel_compile(const char *src, size_t len, const map_instance *inst, map_kernel **out, char *diag,
+                              size_t diag_cap);
+typedef struct {
+  int32_t typable;           /* Fig. 6 derivation exists                          */
+  uint32_t n_phases, n_arrays, block_threads;
+  uint64_t n_blocks;
+  uint64_t cells_per_block;  /* sum of the array extents                          */
+  uint32_t key_bits;         /* width of the access key                           */
+  uint64_t max_events;       /* accesses of the inferred MAP (typable), else 0     */
+} map_kernel_info;
+map_status map_kernel_info_get(const map_kernel *k, map_kernel_info *out);
+/* Extent (cells) of array `array` as planned (0 if out of range). */
+uint64_t map_kernel_extent(const map_kernel *k, uint32_t array);
+#define MAP_EXEC_KEEP_MEMORY 0x200u
+size_t map_kernel_scratch_bytes(const map_kernel *k, uint64_t max_events, uint64_t lambda_cap, uint32_t flags);
+typedef struct {
+  int32_t verdict;           /* races among the executed accesses                 */
+  int32_t typable;           /* 1: every alarm is a true alarm (Theorem 1)        */
+  uint64_t n_events;         /* accesses executed (multiset)                      */
+  uint64_t n_alpha;          /* distinct access values                            */
+  uint64_t racy_segments;    /* racy (phase, array, block, index) cells           */
+  uint64_t uninit_reads;     /* reads of bottom (lastwrite-undef)                 */
+  uint64_t ambiguous_reads;  /* reads of a cell last written by several threads   */
+  float device_ms;
+  uint32_t gpu_launches;
+} map_exec_result;
+map_status map_execute(map_kernel *k, const map_exec *ex, uint64_t max_events, map_exec_result *out);
+map_status map_kernel_witness(const map_kernel *k, map_witness *out);
+/* Final contents of array `array` of block `block` after the last map_execute
+ * with MAP_EXEC_KEEP_MEMORY on the same scratch: values[i] and defined[i] (HOST,
+ * n <= the array's extent) for indices 0..n-1 (defined 0 = never written). */
+map_status map_kernel_memory(const map_kernel *k, const map_exec *ex, uint32_t block, uint32_t array, uint64_t *values,
+                             uint8_t *defined, uint64_t n);
+/* Theorem 1, checked: execute the kernel (as map_execute) and
+ * compare the SET of executed access values with the set Lambda the MAP program
+ * `lambda` enumerates (compiled from map_infer's text at the same instantiation;
+ * ex_lambda = its own scratch, same device and stream), both sorted on the GPU.
+ * For a typable kernel and its inferred MAP the sets are equal; for an ill-typed
+ * kernel and its data-abstracted MAP, alpha is a subset (the MAP's extra values
+ * are the source of false alarms).  lambda_cap bounds Lambda's keys. */
+typedef struct {
+  uint32_t phase, array, block;
+  uint64_t index;
+  uint32_t tid;
+  uint8_t kind;
+} map_access;
+typedef struct {
+  int32_t equal;                       /* alpha set == Lambda set                       */
+  uint64_t n_alpha, n_lambda;          /* distinct values on each side                  */
+  uint64_t only_alpha, only_lambda;    /* values missing on the other side              */
+  int32_t has_first_alpha, has_first_lambda;
+  map_access first_alpha, first_lambda;/* the smallest such value of each side          */
+  map_exec_result exec;                /* the execution's own result                    */
+} map_diff;
+map_status map_theorem1_diff(map_kernel *k, map_program *lambda, const map_exec *ex, const map_exec *ex_lambda,
+                             uint64_t max_events, uint64_t lambda_cap, map_diff *out);
+void map_kernel_free(map_kernel *k);
+
 #ifdef __cplusplus
 }
 #endif

@@ -461,3 +461,226 @@ def status_str(status: int) -> str:
 def fastdiv_selftest(n: int, d: int) -> int:
     """Host copy of the kernels' invariant-divisor quotient (for CPU tests)."""
     return _lib.mapc_test_fastdiv(n, d)
+
+
+# ---- BabyCUDA executor + Theorem-1 differential check (NEXT-2) ---------------
+class _KInfo(ctypes.Structure):
+    _fields_ = [("typable", ctypes.c_int32), ("n_phases", ctypes.c_uint32), ("n_arrays", ctypes.c_uint32),
+                ("block_threads", ctypes.c_uint32), ("n_blocks", ctypes.c_uint64),
+                ("cells_per_block", ctypes.c_uint64), ("key_bits", ctypes.c_uint32), ("max_events", ctypes.c_uint64)]
+
+
+class _ExecResult(ctypes.Structure):
+    _fields_ = [("verdict", ctypes.c_int32), ("typable", ctypes.c_int32), ("n_events", ctypes.c_uint64),
+                ("n_alpha", ctypes.c_uint64), ("racy_segments", ctypes.c_uint64), ("uninit_reads", ctypes.c_uint64),
+                ("ambiguous_reads", ctypes.c_uint64), ("device_ms", ctypes.c_float), ("gpu_launches", ctypes.c_uint32)]
+
+
+class _Access(ctypes.Structure):
+    _fields_ = [("phase", ctypes.c_uint32), ("array", ctypes.c_uint32), ("block", ctypes.c_uint32),
+                ("index", ctypes.c_uint64), ("tid", ctypes.c_uint32), ("kind", ctypes.c_uint8)]
+
+
+class _Diff(ctypes.Structure):
+    _fields_ = [("equal", ctypes.c_int32), ("n_alpha", ctypes.c_uint64), ("n_lambda", ctypes.c_uint64),
+                ("only_alpha", ctypes.c_uint64), ("only_lambda", ctypes.c_uint64),
+                ("has_first_alpha", ctypes.c_int32), ("has_first_lambda", ctypes.c_int32),
+                ("first_alpha", _Access), ("first_lambda", _Access), ("exec", _ExecResult)]
+
+
+EXEC_KEEP_MEMORY = 0x200
+_lib.map_kernel_compile.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(_Instance), ctypes.POINTER(_P),
+                                    ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_kernel_compile.restype = ctypes.c_int
+_lib.map_kernel_info_get.argtypes = [_P, ctypes.POINTER(_KInfo)]
+_lib.map_kernel_info_get.restype = ctypes.c_int
+_lib.map_kernel_scratch_bytes.argtypes = [_P, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32]
+_lib.map_kernel_scratch_bytes.restype = ctypes.c_size_t
+_lib.map_execute.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.c_uint64, ctypes.POINTER(_ExecResult)]
+_lib.map_execute.restype = ctypes.c_int
+_lib.map_kernel_witness.argtypes = [_P, ctypes.POINTER(_Witness)]
+_lib.map_kernel_witness.restype = ctypes.c_int
+_lib.map_kernel_memory.argtypes = [_P, ctypes.POINTER(_Exec), ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint8), ctypes.c_uint64]
+_lib.map_kernel_memory.restype = ctypes.c_int
+_lib.map_theorem1_diff.argtypes = [_P, _P, ctypes.POINTER(_Exec), ctypes.POINTER(_Exec), ctypes.c_uint64,
+                                   ctypes.c_uint64, ctypes.POINTER(_Diff)]
+_lib.map_theorem1_diff.restype = ctypes.c_int
+_lib.map_kernel_free.argtypes = [_P]
+_lib.map_kernel_free.restype = None
+_lib.map_kernel_last_error.argtypes = [_P]
+_lib.map_kernel_last_error.restype = ctypes.c_char_p
+_lib.map_kernel_debug_source.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_kernel_debug_source.restype = ctypes.c_size_t
+_lib.map_kernel_debug_jit_check.argtypes = [_P, ctypes.c_char_p, ctypes.c_size_t]
+_lib.map_kernel_debug_jit_check.restype = ctypes.c_int
+EXPORTS = EXPORTS + ("map_kernel_compile", "map_kernel_info_get", "map_kernel_scratch_bytes", "map_execute",
+                     "map_kernel_witness", "map_kernel_memory", "map_theorem1_diff", "map_kernel_free")
+
+
+@dataclass
+class ExecResult:
+    verdict: int
+    typable: bool
+    n_events: int
+    n_alpha: int
+    racy_segments: int
+    uninit_reads: int
+    ambiguous_reads: int
+    device_ms: float
+    gpu_launches: int
+    witness: Optional[Witness] = None
+
+
+@dataclass
+class Diff:
+    equal: bool
+    n_alpha: int
+    n_lambda: int
+    only_alpha: int
+    only_lambda: int
+    first_alpha: Optional[tuple]      # (phase, array, block, index, tid, kind)
+    first_lambda: Optional[tuple]
+    exec: ExecResult
+
+
+def _acc(a):
+    return (a.phase, a.array, a.block, a.index, a.tid, a.kind)
+
+
+class Kernel:
+    """A BabyCUDA kernel planned at one instantiation (map_kernel_compile)."""
+
+    def __init__(self, src: str, grid: Sequence[int] = (1, 1, 1), block: Sequence[int] = (1, 1, 1),
+                 params: Optional[Dict[str, int]] = None):
+        params = params or {}
+        names = list(params)
+        self._keep = [n.encode() for n in names]
+        inst = _Instance()
+        inst.grid = _dims(grid)
+        inst.block = _dims(block)
+        inst.n_params = len(names)
+        inst.param_names = (ctypes.c_char_p * max(1, len(names)))(*self._keep)
+        inst.param_values = (ctypes.c_uint64 * max(1, len(names)))(*[int(params[n]) for n in names])
+        h = _P()
+        diag = ctypes.create_string_buffer(1024)
+        raw = src.encode()
+        st = _lib.map_kernel_compile(raw, len(raw), ctypes.byref(inst), ctypes.byref(h), diag, 1024)
+        if st != 0:
+            raise MapError(st, diag.value.decode(errors="replace"))
+        self._h = h
+        self.src, self.grid, self.block, self.params = src, tuple(grid), tuple(block), dict(params)
+        self._scratch = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.map_kernel_free(h)
+            self._h = None
+
+    @property
+    def info(self) -> dict:
+        i = _KInfo()
+        _lib.map_kernel_info_get(self._h, ctypes.byref(i))
+        return {f: getattr(i, f) for f, _ in _KInfo._fields_}
+
+    def source(self) -> str:
+        n = _lib.map_kernel_debug_source(self._h, None, 0)
+        buf = ctypes.create_string_buffer(n + 1)
+        _lib.map_kernel_debug_source(self._h, buf, n + 1)
+        return buf.value.decode()
+
+    def jit_check(self) -> str:
+        """NVRTC-compile the executor (no GPU needed): '' on success, else the log."""
+        buf = ctypes.create_string_buffer(8192)
+        r = _lib.map_kernel_debug_jit_check(self._h, buf, 8192)
+        return "" if r == 0 else (buf.value.decode(errors="replace") or f"status {r}")
+
+    def _ex(self, scratch, stream, flags):
+        import torch
+        dev = scratch.device.index if scratch.device.index is not None else torch.cuda.current_device()
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        return _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
+                     scratch.numel() * scratch.element_size(), 0, 0, 1, None, flags)
+
+    def _err(self, st):
+        raise MapError(st, _lib.map_kernel_last_error(self._h).decode())
+
+    def _result(self, r) -> ExecResult:
+        out = ExecResult(r.verdict, bool(r.typable), r.n_events, r.n_alpha, r.racy_segments, r.uninit_reads,
+                         r.ambiguous_reads, r.device_ms, r.gpu_launches)
+        if r.verdict:
+            w = _Witness()
+            if _lib.map_kernel_witness(self._h, ctypes.byref(w)) == 0:
+                out.witness = Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
+                                      w.array_name.decode())
+        return out
+
+    def execute(self, max_events: int = 0, keep_memory: bool = False, scratch=None, stream=None) -> ExecResult:
+        """Run the kernel with data on the GPU and race-check the executed accesses (map_execute)."""
+        import torch
+        if not torch.cuda.is_available():
+            raise MapError(6, "no CUDA device (there is no CPU fallback)")
+        cap = int(max_events) or max(1, self.info["max_events"]) or 1 << 20
+        flags = EXEC_KEEP_MEMORY if keep_memory else 0
+        need = _lib.map_kernel_scratch_bytes(self._h, cap, 0, flags)
+        if scratch is None:
+            scratch = torch.empty(need, dtype=torch.uint8, device="cuda")
+        self._scratch, self._flags = scratch, flags
+        r = _ExecResult()
+        st = _lib.map_execute(self._h, ctypes.byref(self._ex(scratch, stream, flags)), cap, ctypes.byref(r))
+        if st == 9 and not max_events and r.n_events > cap:        # an ill-typed kernel ran longer: retry once
+            return self.execute(max_events=r.n_events, keep_memory=keep_memory, stream=stream)
+        if st != 0:
+            self._err(st)
+        return self._result(r)
+
+    def memory(self, block: int, array: int, n: int):
+        """Final contents of array `array` of block `block` after execute(keep_memory=True):
+        a list of n values, None where never written."""
+        vals = (ctypes.c_uint64 * max(1, n))()
+        defs = (ctypes.c_uint8 * max(1, n))()
+        st = _lib.map_kernel_memory(self._h, ctypes.byref(self._ex(self._scratch, None, self._flags)), block, array,
+                                    vals, defs, n)
+        if st != 0:
+            self._err(st)
+        return [vals[i] if defs[i] else None for i in range(n)]
+
+    def theorem1_diff(self, lambda_prog: "MapProgram", max_events: int = 0, lambda_cap: int = 0) -> Diff:
+        """Execute and compare the executed access values with the MAP program's Lambda (map_theorem1_diff)."""
+        import torch
+        cap = int(max_events) or max(1, self.info["max_events"]) or 1 << 20
+        lcap = int(lambda_cap) or max(1, lambda_prog.info.max_accesses)
+        scratch = torch.empty(_lib.map_kernel_scratch_bytes(self._h, cap, lcap, 0), dtype=torch.uint8, device="cuda")
+        lscratch = torch.empty(lambda_prog.scratch_bytes(), dtype=torch.uint8, device="cuda")
+        d = _Diff()
+        st = _lib.map_theorem1_diff(self._h, lambda_prog._h, ctypes.byref(self._ex(scratch, None, 0)),
+                                    ctypes.byref(lambda_prog._exec(lscratch, None, 0)), cap, lcap, ctypes.byref(d))
+        if st == 9 and not max_events and d.exec.n_events > cap:
+            return self.theorem1_diff(lambda_prog, max_events=d.exec.n_events, lambda_cap=lambda_cap)
+        if st != 0:
+            self._err(st)
+        return Diff(bool(d.equal), d.n_alpha, d.n_lambda, d.only_alpha, d.only_lambda,
+                    _acc(d.first_alpha) if d.has_first_alpha else None,
+                    _acc(d.first_lambda) if d.has_first_lambda else None, self._result(d.exec))
+
+
+def check_kernel(src: str, grid=(1, 1, 1), block=(1, 1, 1), params=None, data_domain: int = 0) -> dict:
+    """One call: type the BabyCUDA kernel, race-check its MAP on the GPU, and label
+    the verdict -- a race on a typable kernel is a TRUE alarm (Theorem 1,
+    PAPER.md:903-918); on an ill-typed one (checked through the data-abstracted MAP
+    when data_domain > 0) it may be false."""
+    inf = infer(src, data_domain)
+    out = {"typable": inf.typable, "type_error": None if inf.typable else (inf.kind, inf.var, inf.line, inf.col),
+           "map": inf.map_text, "result": None, "true_alarm": None}
+    if inf.map_text is not None:
+        r = MapProgram(inf.map_text, grid, block, params).check_races()
+        out["result"] = r
+        out["true_alarm"] = bool(r.verdict and inf.typable)
+    return out
+
+_lib.map_kernel_extent.argtypes = [_P, ctypes.c_uint32]
+_lib.map_kernel_extent.restype = ctypes.c_uint64
+EXPORTS = EXPORTS + ("map_kernel_extent",)
+Kernel.extents = property(lambda self: [int(_lib.map_kernel_extent(self._h, a)) for a in range(self.info["n_arrays"])])

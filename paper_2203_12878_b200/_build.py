@@ -14,6 +14,8 @@ SOURCES = [
     "capi/mapcheck.cpp",
     "capi/jit.cpp",
     "capi/bcapi.cpp",
+    "capi/execute.cpp",
+    "babycuda/bcgen.cpp",
     "babycuda/bcfront.cpp",
     "kernels/generate.cu",
     "kernels/radix.cu",
@@ -23,9 +25,10 @@ SOURCES = [
     "kernels/table.cu",
     "kernels/listing.cu",
     "kernels/direct.cu",
+    "kernels/bcexec.cu",
 ]
 HEADERS = ["devabi.h", "compiler/front.h", "compiler/compiler.h", "kernels/common.cuh", "kernels/segstate.cuh",
-           "capi/jit.h", "babycuda/bcfront.h"]
+           "capi/jit.h", "babycuda/bcfront.h", "babycuda/bcgen.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

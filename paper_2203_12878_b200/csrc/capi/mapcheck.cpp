@@ -1510,3 +1510,62 @@ const char* map_last_error(const map_program* p) { return p ? p->last_error.c_st
 uint32_t mapc_test_fastdiv(uint32_t n, uint32_t d) { return mapc::fastdiv_apply(n, mapc::make_fastdiv(d)); }
 
 }  // extern "C"
+
+// ---- internal: the MAP's access keys in a global layout (execute.cpp) --------
+// Every chunk of the plan (chunk_max_accesses of ex; all chunks, no shard) is
+// generated with the bytecode VM in keys mode and its keys are re-packed into
+// the global layout [phase | array | block | index | tid | kind] of widths
+// w_out[4] (phase, array, block, index; the payload w_tid + 1 is the program's)
+// and appended to out[cap] (device).  *n = the keys generated (even beyond cap);
+// *n_outside = keys whose index the output layout cannot hold (written as ~0).
+extern "C" cudaError_t mapc_launch_bc_repack(const unsigned long long* in, unsigned long long n, const uint32_t* w_in,
+                                             const unsigned long long* offs, const uint32_t* w_out,
+                                             unsigned long long* out, unsigned long long* n_outside, cudaStream_t s);
+
+extern "C" map_status mapc_internal_lambda_keys(map_program* p, const map_exec* ex, const uint32_t* w_out,
+                                                unsigned long long* out, uint64_t cap, unsigned long long* n_outside,
+                                                uint64_t* n) {
+  if (!p || !ex || !w_out || !out || !n || !n_outside) return MAP_E_ARG;
+  uint64_t total = 0;
+  map_status st0 = ensure_plan(p, ex->chunk_max_accesses ? ex->chunk_max_accesses : default_cap(p));
+  if (st0 != MAP_OK) return st0;
+  for (uint32_t c = 0; c < p->plan.chunks.size(); ++c) {
+    Dev d;
+    map_status st = stage_setup(p, ex, c, &d);
+    if (st != MAP_OK) return st;
+    const Chunk& ch = p->plan.chunks[c];
+    const MapcLayout& L = ch.lay;
+    CK(mapc_upload_ops(ch.ops.data(), ch.ops.size(), d.s));
+    CK(cudaMemcpyAsync(d.segs, ch.segs.data(), ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, d.s));
+    CK(mapc_launch_chunk_init(d.ctrl, ch.dense_total, d.s));
+    if (ch.total_tiles)
+      CK(mapc_launch_generate(d.segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, d.bufA,
+                              d.ctrl, d.n_sms, ch.nreg, ch.max_emits, 0, MAPC_MODE_KEYS, nullptr, 4, d.s));
+    MapcCtrl hc{};
+    CK(cudaMemcpyAsync(&hc, d.ctrl, sizeof(hc), cudaMemcpyDeviceToHost, d.s));
+    CK(cudaStreamSynchronize(d.s));
+    if (hc.err & MAPC_ERR_DIV0) { p->last_error = "division or modulo by zero on a reached path"; return MAP_E_ARITH; }
+    if (hc.err) { p->last_error = "internal consistency check failed"; return MAP_E_RANGE; }
+    if (total + hc.n <= cap) {
+      const uint32_t w_in[5] = {L.w_phase, L.w_array, L.w_block, L.w_index, L.pay_bits};
+      const unsigned long long offs[3] = {ch.phase_lo, ch.b_lo, L.idx_lo};
+      CK(mapc_launch_bc_repack(d.bufA, hc.n, w_in, offs, w_out, out + total, n_outside, d.s));
+    }
+    total += hc.n;
+  }
+  *n = total;
+  return MAP_OK;
+}
+
+// internal: static facts of a compiled program the executor needs
+extern "C" map_status mapc_internal_index_hull(const map_program* p, uint64_t* max_index, uint32_t* n_phases) {
+  if (!p || !max_index || !n_phases) return MAP_E_ARG;
+  uint64_t hi = 0;
+  bool any = false;
+  for (const auto& in : p->C.inst)
+    for (const auto& g : in.groups)
+      if (g.has_emit) { hi = std::max(hi, g.index.hi); any = true; }
+  *max_index = any ? hi : 0;
+  *n_phases = p->C.n_phases;
+  return MAP_OK;
+}

@@ -120,3 +120,37 @@ def test_mutated_texts_same_status_class():
             except mc.MapError as e:
                 got = e.status
             assert got == want, (src, got, want)
+
+
+# ---- NEXT-2 executor planning on the CPU (no GPU: NVRTC compiles without one) --
+
+def test_executor_sources_compile():
+    bad = []
+    kernels = [wb.kernel(n) for n in wb.KERNELS] + [wb.random_kernel(s, ill_typed=ill)[0]
+                                                    for s in range(0, 60, 3) for ill in (False, True)]
+    for inst in kernels:
+        try:
+            k = mc.Kernel(inst.src, inst.grid, inst.block, inst.params)
+        except mc.MapError as e:
+            bad.append((inst.src, str(e)))
+            continue
+        log = k.jit_check()
+        if log:
+            bad.append((inst.src, log[:500]))
+    assert not bad, bad[:2]
+
+
+def test_executor_plan_facts():
+    inst = wb.kernel("transpose", ts=8, rw=4, grid=4)
+    k = mc.Kernel(inst.src, inst.grid, inst.block, inst.params)
+    i = k.info
+    assert i["typable"] == 1 and i["n_phases"] == 2 and i["n_arrays"] == 2 and i["cells_per_block"] == 128
+    assert i["max_events"] == 4 * 32 * 6      # 2 rows per thread: tile write, tile read, out write
+    # ill-typed kernels must declare their extents; blockDim is CUDA's (<= 1024)
+    with pytest.raises(mc.MapError) as e:
+        mc.Kernel("A[tid] := tid; let x = A[tid] in A[x] := 9", block=(8, 1, 1))
+    assert e.value.status == 8
+    mc.Kernel("shared A[8]; A[tid] := tid; let x = A[tid] in A[x] := 9", block=(8, 1, 1))
+    with pytest.raises(mc.MapError) as e:
+        mc.Kernel("shared A[8]; A[0] := 1", block=(1025, 1, 1))
+    assert e.value.status == 8
