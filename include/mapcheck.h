@@ -97,7 +97,8 @@ enum {
   MAP_K_SORT_NEXT = 6,      /* radix passes that also build the next pass's range table */
   MAP_K_DIRECT = 7,         /* generate fused with the direct-address table reductions  */
   MAP_K_CLEAR = 8,          /* direct-address table clear                               */
-  MAP_K_COUNT = 9
+  MAP_K_UNIT = 9,           /* on-chip per-(phase, block) tables: generate + fold + scan */
+  MAP_K_COUNT = 10
 };
 typedef struct {
   float ms[MAP_K_COUNT];
@@ -154,7 +155,16 @@ typedef struct {
 #define MAP_DETECT_SORT 0x10u
 #define MAP_DETECT_TABLE 0x20u
 #define MAP_DETECT_DIRECT 0x40u
-#define MAP_DETECT_MASK 0x70u
+/*   MAP_DETECT_UNIT:  per (phase, block) unit, entirely on chip: one CTA folds
+ *                     the unit's accesses into a shared-memory table of its
+ *                     (array, index) cells (same cell code as DIRECT) and scans
+ *                     it; no table in HBM (SURVEY.md §8f NEXT-3 on chip).  For
+ *                     chunks whose unit table fits MAPC_UNIT_MAX_BYTES and that
+ *                     have enough units (or few accesses), with the specialised
+ *                     generate; AUTO takes it where it applies, other chunks
+ *                     fall back as AUTO. */
+#define MAP_DETECT_UNIT 0x80u
+#define MAP_DETECT_MASK 0xF0u
 
 /* MAP_EXEC_SEQUENTIAL (map_exec.flags): run the direct path's chunks one after
  * another on the caller's stream only (no side stream: each chunk's clear,

@@ -49,7 +49,7 @@ class _Instance(ctypes.Structure):
 
 
 KERNEL_CLASSES = ("generate", "hist", "scan", "onesweep", "detect", "other", "onesweep_next",
-                  "direct", "clear")   # MAP_K_* order
+                  "direct", "clear", "unit")   # MAP_K_* order
 _NK = len(KERNEL_CLASSES)
 
 
@@ -64,7 +64,7 @@ class _Exec(ctypes.Structure):
                 ("flags", ctypes.c_uint32)]
 
 GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
-DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40}   # MAP_DETECT_* (include/mapcheck.h)
+DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40, "unit": 0x80}   # MAP_DETECT_* (mapcheck.h)
 EXEC_SEQUENTIAL = 0x100                                                       # MAP_EXEC_SEQUENTIAL
 
 

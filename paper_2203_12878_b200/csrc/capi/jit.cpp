@@ -228,6 +228,11 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   }
   put(k, ch.segs.size());
   k.append(reinterpret_cast<const char*>(ch.segs.data()), ch.segs.size() * sizeof(MapcSeg));
+  if (mode == MAPC_MODE_UNIT) {
+    put(k, ch.n_blocks);
+    put(k, ch.unit_segs.size());
+    k.append(reinterpret_cast<const char*>(ch.unit_segs.data()), ch.unit_segs.size() * sizeof(MapcSeg));
+  }
   return k;
 }
 
@@ -271,10 +276,135 @@ std::string emit_tail(uint32_t mode, uint32_t w_tid, int T) {
   return s.str();
 }
 
+// Unit mode (MAPC_MODE_UNIT; SURVEY.md §8f NEXT-3 "detect in smem tables per
+// unit ... fully on-chip"): races are intra-(phase, block) and
+// shared arrays are per block (R10), so a (phase, block) unit whose
+// cells (array, index) fit in shared memory is checked entirely on chip: one CTA
+// clears the unit's table, runs every tuple of the unit's segments folding each
+// access into its cell with a shared-memory atomicOr of the same cell code as the
+// HBM table (direct.cu), scans the table (racy cells counted, the smallest racy
+// sort field atomicMin-ed into ctrl->racy_sf) and moves to its next unit.  No
+// table in HBM, no clear and no scan launch.  The witness cell's keys are
+// re-emitted by the filter-mode kernel as on the HBM direct path.
+std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t cell_bytes) {
+  std::ostringstream s;
+  const int T = MAPC_GEN_THREADS;
+  const MapcLayout& L = ch.lay;
+  const uint32_t wu = L.w_array + L.w_index;
+  const uint64_t cells = 1ull << wu;
+  const uint64_t words = cell_bytes == 2 ? (cells + 1) / 2 : cells;
+  const uint64_t nb = std::max<uint64_t>(ch.n_blocks, 1);
+  const uint32_t wt = L.w_tid;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index
+    << "(unsigned long long n_units, unsigned long long* n_ctr, unsigned long long* racy_ctr, "
+       "unsigned long long* racy_sf, u32* err_flag) {\n"
+    << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
+    << "  const u32 WI = " << L.w_index << "u; (void)WI;\n"
+    << "  const u64 IDX_LO = " << L.idx_lo << "ull;\n"
+    << "  const u32 TMASK = " << (wt >= 32 ? 0xFFFFFFFFu : ((1u << wt) - 1u)) << "u; (void)TMASK;\n"
+    << "  __shared__ u32 tab[" << words << "];\n"
+    << "  const int me = threadIdx.x;\n"
+    << "  u32 err = 0, cnt = 0;\n"
+    << "  unsigned long long racy = 0, best = ~0ull;\n"
+    << "  for (unsigned long long u = blockIdx.x; u < n_units; u += gridDim.x) {\n"
+    << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
+    << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) tab[i] = 0u;\n"
+    << "    __syncthreads();\n";
+  // the unit-local cell of an access: (array, index - idx_lo)
+  s << "#define EMIT_KEY(IX, ARR, KIND) { u64 idx_ = (u64)(IX) - IDX_LO; "
+       "if (WI < 64 && (idx_ >> WI) != 0) { err |= " << MAPC_ERR_LAYOUT << "u; idx_ = 0; } "
+       "const u32 c_ = ((u32)(ARR) << WI) | (u32)idx_; ";
+  if (cell_bytes == 2)
+    s << "atomicOr(&tab[c_ >> 1], (tcd_ | ((u32)(KIND) << 14)) << (16u * (c_ & 1u))); ";
+  else
+    s << "atomicOr(&tab[c_], tidv | ((~tidv & TMASK) << " << wt << "u) | ((u32)(KIND) << " << 2 * wt << "u)); ";
+  s << "if (!sg.dense) ++cnt; }\n";
+  auto fd = [](const MapcFastDiv& f) {
+    std::ostringstream o;
+    o << "{" << f.d << "u, " << f.m << "u, " << f.s << "u, " << f.pow2 << "u}";
+    return o.str();
+  };
+  const uint32_t hb = L.w_array + L.w_block + L.w_index;
+  for (const MapcSeg& g : ch.unit_segs) {
+    const JitProgram* pg = nullptr;
+    for (const JitProgram& p : ch.programs)
+      if (p.prog_begin == g.prog_begin) pg = &p;
+    if (!pg) continue;
+    uint64_t tpb = MAPC_GEN_THREADS;   // tuples per block of the segment: blockDim * prod(trips)
+    tpb = g.tid_div.d;
+    for (uint32_t l = 0; l < g.n_levels; ++l) tpb *= g.trip_div[l].d;
+    const uint64_t seg_nb = g.n_tuples / std::max<uint64_t>(tpb, 1);
+    const uint32_t seg_lph = hb >= 64 ? 0u : (uint32_t)(g.key_hi >> hb);
+    s << "    if (lph == " << seg_lph << "u && lb >= " << g.lb0 << "u && lb < " << (uint64_t)g.lb0 + seg_nb << "ull) {\n"
+      << "      const Seg sg = {" << g.tuple_begin << "ull, " << g.n_tuples << "ull, " << g.tile_begin << "ull, "
+      << g.key_begin << "ull, " << g.key_hi << "ull, " << g.prog_begin << "u, " << g.prog_end << "u, " << g.n_levels
+      << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, " << g.tid_inner << "u, {";
+    for (int l = 0; l < 8; ++l) s << (l ? ", " : "") << fd(g.trip_div[l]);
+    s << "}, " << fd(g.tid_div) << "};\n"
+      << "      const u32 t0 = (lb - " << g.lb0 << "u) * " << tpb << "u;\n"
+      << "#pragma unroll 1\n"
+      << "      for (u32 k = me; k < " << tpb << "u; k += " << T << "u) {\n"
+      << "        const u32 t = t0 + k; (void)t;\n"
+      << "        const bool valid = true;\n"
+      << "        u32 rem = t;\n"
+      << "        W r[" << MAPC_NREG << "];\n"
+      << decode_tuple(*pg, "        ");
+    if (cell_bytes == 2) s << "        const u32 tcd_ = code16(tidv, 0u);\n";
+    s << "        bool act = true;\n"
+      << "        u32 e = 0;\n"
+      << program_body(pg->ops, u32)
+      << "        (void)act; (void)e; (void)lbv;\n"
+      << "      }\n"
+      << "    }\n";
+  }
+  s << "#undef EMIT_KEY\n"
+    << "    __syncthreads();\n"
+    << "    const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
+    << "u;\n"
+    << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) {\n"
+    << "      const u32 w = tab[i];\n"
+    << "      if (!w) continue;\n";
+  // cell c = (array, index) -> sort field base_ + (array << (wB + wI)) + index
+  auto cell_sf = [&](const std::string& c) {
+    return "(base_ + (((u64)(" + c + ") >> " + std::to_string(L.w_index) + "u) << " +
+           std::to_string(L.w_block + L.w_index) + "u) + ((u64)(" + c + ") & " +
+           std::to_string(L.w_index >= 32 ? 0xFFFFFFFFull : ((1ull << L.w_index) - 1)) + "ull))";
+  };
+  if (cell_bytes == 2) {
+    s << "#pragma unroll\n"
+      << "      for (u32 h = 0; h < 2u; ++h) {\n"
+      << "        const u32 c = (w >> (16u * h)) & 0xFFFFu;\n"
+      << "        if (((c >> 14) & 1u) && (__popc(c & 0x7Fu) > 3 || __popc((c >> 7) & 0x7Fu) > 3)) {\n"
+      << "          ++racy; const u64 sf = " << cell_sf("2u * i + h") << "; best = sf < best ? sf : best; }\n"
+      << "      }\n";
+  } else {
+    s << "      if (((w >> " << 2 * wt << "u) & 1u) && (w & (w >> " << wt << "u) & TMASK)) {\n"
+      << "        ++racy; const u64 sf = " << cell_sf("i") << "; best = sf < best ? sf : best; }\n";
+  }
+  s << "    }\n"
+    << "    __syncthreads();\n"
+    << "  }\n"
+    << "#pragma unroll\n"
+    << "  for (int o = 16; o; o >>= 1) {\n"
+    << "    racy += __shfl_xor_sync(0xffffffffu, racy, o);\n"
+    << "    const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, best, o); best = b2 < best ? b2 : best;\n"
+    << "    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);\n"
+    << "  }\n"
+    << "  if ((me & 31) == 0) {\n"
+    << "    if (racy) atomicAdd(racy_ctr, racy);\n"
+    << "    if (best != ~0ull) atomicMin(racy_sf, best);\n"
+    << "    if (cnt) atomicAdd(n_ctr, (unsigned long long)cnt);\n"
+    << "  }\n"
+    << "  if (err) atomicOr(err_flag, err);\n"
+    << "}\n";
+  return s.str();
+}
+
 }  // namespace
 
 std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes) {
   static_assert(sizeof(MapcSeg) == 5 * 8 + 8 * 4 + 9 * 16, "Seg layout mirrored in the JIT prelude");
+  if (mode == MAPC_MODE_UNIT) return unit_kernel_source(ch, index, u32, cell_bytes);
   std::ostringstream s;
   const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   // keys staged per thread per tile for compaction: the guarded segments' emits
@@ -641,6 +771,20 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
     out->kernels[i] = it->second.kernels[0];
   }
   return 0;
+}
+
+cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,
+                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag, int n_sms,
+                         cudaStream_t s) {
+  if (n_units == 0) return cudaSuccess;
+  const void* fn = (const void*)h.kernels[chunk];
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
+  if (occ < 1) occ = 1;
+  const unsigned long long capb = (unsigned long long)n_sms * occ;
+  const int grid = (int)(n_units < capb ? n_units : capb);
+  void* args[] = {(void*)&n_units, (void*)&n_ctr, (void*)&racy, (void*)&racy_sf, (void*)&err_flag};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,

@@ -25,6 +25,9 @@ struct JitChunk {
   uint32_t max_emits;
   std::vector<JitProgram> programs;
   std::vector<MapcSeg> segs;      // baked as literals when few (tuple decode and slots fold to constants)
+  // unit mode (MAPC_MODE_UNIT): every segment baked, and the chunk's unit grid
+  std::vector<MapcSeg> unit_segs;
+  uint64_t n_blocks = 0;          // blocks of the chunk (b_hi - b_lo)
 };
 
 struct JitHandle {
@@ -45,5 +48,10 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
                          int n_sms, int max_ctas_per_sm, cudaStream_t s);
+// Unit mode (MAPC_MODE_UNIT): n_units (phase, block) units of the chunk, one CTA
+// each at a time; counts into n_ctr (guarded accesses), racy, racy_sf (atomicMin).
+cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,
+                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag, int n_sms,
+                         cudaStream_t s);
 
 }  // namespace mapj

@@ -105,13 +105,14 @@ struct Chunk {
   uint64_t cells = 0;                       // 2^S
   uint32_t cell_bytes = 4;                  // 2 if w_tid <= 10 (devabi.h code16), 4 if 2 w_tid + 1 <= 32, else 8
   bool direct_ok = false;                   // the table is cheap enough and fits the scratch plan
+  bool unit_ok = false;                     // per-(phase, block) tables fit shared memory (MAPC_MODE_UNIT)
   size_t dev_segs = 0;                      // offset of this chunk's segment table in the all-chunks region
 };
 
 struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
-  mapj::JitHandle jit[3];                    // per generate mode (MAPC_MODE_*); null = not built yet
+  mapj::JitHandle jit[4];                    // per generate mode (MAPC_MODE_*); null = not built yet
   size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
   size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
   size_t off_ctrl2 = 0;                     // second control block (overlapped direct pipeline)
@@ -383,6 +384,21 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       ch.direct_ok = cheap && fits;
       if (ch.direct_ok) dtab = std::max<size_t>(dtab, tb);
     }
+    // On-chip units: the cells of one (phase, block) -- (array, index) -- fit a
+    // shared-memory table, and the chunk has enough units to fill the GPU (or is
+    // small), so one CTA per unit does generate + fold + scan without HBM.
+    {
+      static const bool unit_env = [] { const char* e = getenv("MAPC_UNIT"); return !(e && e[0] == '0'); }();
+      const uint32_t wu = ch.lay.w_array + ch.lay.w_index;
+      const uint64_t n_units = (uint64_t)(ch.phase_hi - ch.phase_lo + 1) * (ch.b_hi - ch.b_lo);
+      ch.unit_ok = unit_env && ch.cell_bytes <= 4 && wu < 20 &&
+                   ((1ull << wu) * ch.cell_bytes) <= MAPC_UNIT_MAX_BYTES && ch.segs.size() <= MAPC_UNIT_MAX_SEGS &&
+                   (n_units >= 2 * 148 || ch.bound <= (1ull << 20)) && ch.bound > 0;
+      if (ch.unit_ok) {
+        ch.jit.unit_segs = ch.segs;
+        ch.jit.n_blocks = ch.b_hi - ch.b_lo;
+      }
+    }
   }
   out.cap = kcap;
   const uint64_t sort_tiles = (kcap + mapc_sort_tile() - 1) / mapc_sort_tile();
@@ -434,7 +450,7 @@ MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~
   bool table = false;
   if (sel == MAP_DETECT_TABLE) {
     table = true;
-  } else if (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT) {
+  } else if (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT || sel == MAP_DETECT_UNIT) {
     const uint32_t S = L.sort_bits;
     table = nk >= (1ull << 16) && (S <= 1 || nk >= (1ull << (S - 1)));
   }
@@ -450,7 +466,14 @@ MapcLayout effective_layout(const Chunk& ch, uint32_t flags, uint64_t n_keys = ~
 // MAP_DETECT_DIRECT, and the chunk's table qualifies; direct.cu).
 bool use_direct(const Chunk& ch, uint32_t flags) {
   const uint32_t sel = flags & MAP_DETECT_MASK;
-  return (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT) && ch.direct_ok;
+  return (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_DIRECT || sel == MAP_DETECT_UNIT) && ch.direct_ok;
+}
+
+// On-chip per-unit tables for this chunk (MAP_DETECT_AUTO or MAP_DETECT_UNIT,
+// the specialised generate, and the chunk's units fit; MAPC_MODE_UNIT).
+bool use_unit(const Chunk& ch, uint32_t flags, int gen_mode) {
+  const uint32_t sel = flags & MAP_DETECT_MASK;
+  return gen_mode == 1 && ch.unit_ok && (sel == MAP_DETECT_AUTO || sel == MAP_DETECT_UNIT);
 }
 
 // Whether a radix pass also accumulates the next pass's range table (k_rsweep
@@ -704,13 +727,16 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   if (gen_mode == 1 && !mine.empty()) {
     // the kernels this run needs, per mode: keys (sort / table detect), direct +
     // filter (direct detect), for this rank's chunks only
-    std::vector<char> want[3];
-    bool any[3] = {false, false, false};
-    for (uint32_t m = 0; m < 3; ++m) want[m].assign(P.chunks.size(), 0);
+    std::vector<char> want[4];
+    bool any[4] = {false, false, false, false};
+    for (uint32_t m = 0; m < 4; ++m) want[m].assign(P.chunks.size(), 0);
     for (size_t c : mine) {
-      const bool d = use_direct(P.chunks[c], ex->flags);
-      for (uint32_t m = 0; m < 3; ++m) {
-        const bool w = d ? m != MAPC_MODE_KEYS : m == MAPC_MODE_KEYS;
+      const bool un = use_unit(P.chunks[c], ex->flags, 1);
+      const bool d = !un && use_direct(P.chunks[c], ex->flags);
+      for (uint32_t m = 0; m < 4; ++m) {
+        const bool w = un  ? (m == MAPC_MODE_UNIT || m == MAPC_MODE_FILTER)
+                       : d ? (m == MAPC_MODE_DIRECT || m == MAPC_MODE_FILTER)
+                           : m == MAPC_MODE_KEYS;
         const bool have = P.jit[m].kernels.size() == P.chunks.size() && P.jit[m].kernels[c] != nullptr;
         if (w && !have) { want[m][c] = 1; any[m] = true; }
       }
@@ -722,14 +748,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       cb.push_back(ch.cell_bytes);
     }
     std::vector<std::thread> builders;
-    std::string logs[3];
-    int rcs[3] = {0, 0, 0};
-    for (uint32_t m = 0; m < 3; ++m)
+    std::string logs[4];
+    int rcs[4] = {0, 0, 0, 0};
+    for (uint32_t m = 0; m < 4; ++m)
       if (any[m])
         builders.emplace_back(
             [&, m]() { rcs[m] = mapj::build_module(jc, p->C.u32_mode, m, cb, want[m], &P.jit[m], &logs[m]); });
     for (auto& t : builders) t.join();
-    for (uint32_t m = 0; m < 3; ++m)
+    for (uint32_t m = 0; m < 4; ++m)
       if (rcs[m] != 0) {
         p->last_error = "specialised generate: " + logs[m];
         return MAP_E_CUDA;
@@ -802,7 +828,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&
              2 * tab_stride <= P.cap * 8;
-  for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags);
+  for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags) && !use_unit(P.chunks[c], ex->flags, gen_mode);
   if (ovl) {
     if (!p->side || p->side_dev != ex->device) {
       if (p->side) cudaStreamDestroy(p->side);
@@ -906,6 +932,29 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     size_t m = begin(MAP_K_OTHER);
     CK(mapc_launch_chunk_init(ctrl, ch.dense_total, s));
     end(m);
+    if (use_unit(ch, ex->flags, gen_mode)) {
+      // on-chip per-(phase, block) tables (jit.cpp, unit mode): generate, fold and
+      // scan in one launch; then the witness cell's keys as on the direct path
+      const uint64_t n_units = (uint64_t)(ch.phase_hi - ch.phase_lo + 1) * (ch.b_hi - ch.b_lo);
+      m = begin(MAP_K_UNIT);
+      CK(mapj::launch_units(P.jit[MAPC_MODE_UNIT], c, n_units, &ctrl->n, &ctrl->racy, &ctrl->racy_sf, &ctrl->err,
+                            n_sms, s));
+      end(m);
+      m = begin(MAP_K_OTHER);
+      launches += 2;
+      st_acc.launches[MAP_K_OTHER] += 2;
+      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s));
+      if (ch.total_tiles) {
+        ++launches;
+        st_acc.launches[MAP_K_OTHER]++;
+        CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
+                              &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s));
+      }
+      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s));
+      CK(mapc_launch_chunk_finish(ctrl, 0, res + c, s));
+      end(m);
+      continue;
+    }
     if (use_direct(ch, ex->flags)) {
       // sort-free direct-address detect (direct.cu): clear the table, fold every
       // access into its cell, scan the table, re-emit the witness cell's keys
@@ -1083,7 +1132,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     r.n_accesses += cr.n;
     r.racy_segments += cr.racy;
     err |= cr.err;
-    if (use_direct(P.chunks[c], ex->flags)) {
+    if (use_unit(P.chunks[c], ex->flags, gen_mode)) {
+      // on-chip units: no algorithmic HBM traffic (the kernel is ALU / shared-memory bound)
+    } else if (use_direct(P.chunks[c], ex->flags)) {
       // direct path: the fused generate reads and writes every cell of the
       // table once (the per-access reductions happen in L2), the clear writes
       // it and the scan reads it
@@ -1488,8 +1539,9 @@ int map_debug_jit_check(const map_program* cp, uint64_t chunk_max_accesses, char
         std::string li;
         std::vector<mapj::JitChunk> one{chunks[i].jit};
         bool bad = false;
-        for (uint32_t mode = 0; mode < 3 && !bad; ++mode)
-          bad = mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode, mode, chunks[i].cell_bytes), &cubin,
+        for (uint32_t mode = 0; mode < 4 && !bad; ++mode)
+          if (mode != MAPC_MODE_UNIT || chunks[i].unit_ok)
+            bad = mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode, mode, chunks[i].cell_bytes), &cubin,
                                     &li) != 0;
         if (bad) {
           std::lock_guard<std::mutex> g(mu);

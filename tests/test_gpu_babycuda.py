@@ -138,8 +138,8 @@ def test_theorem1_eq1_mismatch_and_false_alarm():
     assert not inf.typable
     assert not d.equal and d.only_alpha == 0 and d.only_lambda > 0
     assert d.exec.verdict == 0 and prog.check_races().verdict == 1
-    # the smallest access value only the abstraction has: thread 0 writing A[1] (x = 1)
-    assert d.first_lambda == (0, 0, 0, 1, 0, 1)
+    # the smallest access value only the abstraction has: thread 1 writing A[0] (x = 0)
+    assert d.first_lambda == (0, 0, 0, 0, 1, 1)
     rep = mc.check_kernel(src, block=(8, 1, 1), data_domain=8)
     assert rep["typable"] is False and rep["result"].verdict == 1 and rep["true_alarm"] is False
 
