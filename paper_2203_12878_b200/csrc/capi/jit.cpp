@@ -162,6 +162,15 @@ __device__ __forceinline__ u32 cw7(u32 d) {
   return (u32)(w >> (7u * (d & 7u))) & 0x7Fu;
 }
 __device__ __forceinline__ u32 code16(u32 t, u32 kind) { return cw7(t & 31u) | (cw7((t >> 5) & 31u) << 7) | (kind << 14); }
+// nonzero iff a 16-bit cell of the word is racy (SWAR, same test as direct.cu racy16_word)
+__device__ __forceinline__ u32 racy16w(u32 w) {
+  const u32 g = 0x80808080u, one = 0x01010101u;
+  u32 x = (w & 0x007F007Fu) | ((w << 1) & 0x7F007F00u) | g;
+  x = (x & (x - one)) | g;
+  x = (x & (x - one)) | g;
+  x = (x & (x - one));
+  return x & (((w >> 14) & 0x00010001u) * 0x7F7Fu);
+}
 // Block offset (within the segment) of tuple t: t / (blockDim * prod(trips)).
 __device__ __forceinline__ u32 block_of(u32 t, const Seg& sg) {
   u32 rem = fdiv(t, sg.tid_div);
@@ -201,6 +210,7 @@ std::string prelude() {
 struct Module {
   cudaLibrary_t lib = nullptr;
   std::vector<cudaKernel_t> kernels;
+  int threads = MAPC_GEN_THREADS;
 };
 
 std::mutex g_mu;
@@ -341,19 +351,37 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, " << g.tid_inner << "u, {";
     for (int l = 0; l < 8; ++l) s << (l ? ", " : "") << fd(g.trip_div[l]);
     s << "}, " << fd(g.tid_div) << "};\n"
-      << "      const u32 t0 = (lb - " << g.lb0 << "u) * " << tpb << "u;\n"
-      << "#pragma unroll 1\n"
-      << "      for (u32 k = me; k < " << tpb << "u; k += " << T << "u) {\n"
+      << "      const u32 t0 = (lb - " << g.lb0 << "u) * " << tpb << "u;\n";
+    // Four consecutive tuples per thread when the innermost coordinate's range is a
+    // multiple of 4: they differ only in that coordinate (no carry), so the tuple
+    // is decoded once and NVRTC shares everything that does not depend on it.
+    const bool tid_is_inner = pg->tid_inner || pg->n_levels == 0;
+    const bool quad = pg->inner_range % 4 == 0 && tpb % 4 == 0;
+    const uint32_t inner_reg = tid_is_inner ? MAPC_REG_TID : MAPC_REG_K0 + pg->n_levels - 1;
+    s << "#pragma unroll 1\n"
+      << "      for (u32 k = " << (quad ? "4u * me" : "me") << "; k < " << tpb << "u; k += " << (quad ? 4 * T : T)
+      << "u) {\n"
       << "        const u32 t = t0 + k; (void)t;\n"
       << "        const bool valid = true;\n"
       << "        u32 rem = t;\n"
       << "        W r[" << MAPC_NREG << "];\n"
       << decode_tuple(*pg, "        ");
+    if (quad) {
+      s << "        const W c0_ = r[" << inner_reg << "];\n"
+        << "        const u32 tid0_ = tidv;\n"
+        << "#pragma unroll\n"
+        << "        for (u32 h_ = 0; h_ < 4u; ++h_) {\n";
+      if (tid_is_inner) s << "        tidv = tid0_ + h_;\n";
+      s << "        r[" << inner_reg << "] = c0_ + (W)h_;\n";
+    } else {
+      s << "        {\n";
+    }
     if (cell_bytes == 2) s << "        const u32 tcd_ = code16(tidv, 0u);\n";
     s << "        bool act = true;\n"
       << "        u32 e = 0;\n"
       << program_body(pg->ops, u32)
       << "        (void)act; (void)e; (void)lbv;\n"
+      << (quad ? "        }\n        (void)tid0_;\n" : "        }\n")
       << "      }\n"
       << "    }\n";
   }
@@ -363,7 +391,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
     << "u;\n"
     << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) {\n"
     << "      const u32 w = tab[i];\n"
-    << "      if (!w) continue;\n";
+    << (cell_bytes == 2 ? "      if (!racy16w(w)) continue;\n" : "      if (!w) continue;\n");
   // cell c = (array, index) -> sort field base_ + (array << (wB + wI)) + index
   auto cell_sf = [&](const std::string& c) {
     return "(base_ + (((u64)(" + c + ") >> " + std::to_string(L.w_index) + "u) << " +
@@ -424,8 +452,19 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // on 5a with the blocked, carry-free paired generate (profiles/r1q_probe_minb.txt);
   // MAPC_JIT_MINB overrides (0 = none)
   static const int minb_env = [] { const char* e = getenv("MAPC_JIT_MINB"); return e ? atoi(e) : 10; }();
-  const int minb = mode == MAPC_MODE_DIRECT ? minb_env : 0;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << T;
+  // Per-thread reduction cache (direct mode, 16-bit cells, 32-bit sort fields):
+  // the CTA is two tile-sized halves; half h takes tile 2p + h of the CTA's
+  // p-th tile pair, so a thread's successive tiles are two tiles apart -- for a
+  // row sweep of 1024 columns (5a: 2 tiles per row) the same columns of the next
+  // row.  The aligned-quad red.or.b64 of a site goes through a 4-entry cache of
+  // (quad, OR of codes): a quad touched again before its eviction (5a: the reads
+  // of row x come from rows x-1, x, x+1 of the same thread) is ORed in a
+  // register instead of a second global reduction.  Same cells, same codes: the
+  // table is identical; the evicted and finally flushed entries are plain reds.
+  const int CT = kernel_threads(ch, mode, cell_bytes);
+  const bool rcache = CT != T;
+  const int minb = mode == MAPC_MODE_DIRECT ? (rcache ? std::max(1, minb_env * T / CT) : minb_env) : 0;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << CT;
   if (minb > 0) s << ", " << minb;
   s << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
@@ -438,7 +477,9 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
     << "  __shared__ u64 s_base;\n"
-    << "  const int me = threadIdx.x;\n"
+    << (rcache ? "  const int me = threadIdx.x & " + std::to_string(T - 1) + ", half_ = threadIdx.x / " +
+                     std::to_string(T) + ";\n"
+               : std::string("  const int me = threadIdx.x;\n"))
     << "  u32 err = 0;\n"
     << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
     << "  (void)TMASK; (void)target_ptr;\n";
@@ -450,12 +491,26 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
-  s
-    << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
-                  "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
-                  "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
-                : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n")
-    << "    int lo = 0, hi = n_segs - 1;\n"
+  if (rcache)
+    s << "  u32 rq0_ = ~0u, rq1_ = ~0u, rq2_ = ~0u, rq3_ = ~0u; u64 ra0_ = 0, ra1_ = 0, ra2_ = 0, ra3_ = 0;\n"
+      << "#define RC_RED(Q, A) atomicOr(reinterpret_cast<u64*>(keys) + (Q), (A))\n"
+      << "#define RC_PUT(Q, A) { const u32 q_ = (Q); const u64 a_ = (A); "
+         "if (q_ == rq0_) ra0_ |= a_; else if (q_ == rq1_) ra1_ |= a_; else if (q_ == rq2_) ra2_ |= a_; "
+         "else if (q_ == rq3_) ra3_ |= a_; "
+         "else { if (rq0_ != ~0u) RC_RED(rq0_, ra0_); rq0_ = rq1_; ra0_ = ra1_; rq1_ = rq2_; ra1_ = ra2_; "
+         "rq2_ = rq3_; ra2_ = ra3_; rq3_ = q_; ra3_ = a_; } }\n"
+      << "  const u64 pairs_ = (total_tiles + 1) >> 1;\n"
+      << "  const u64 per_cta_ = (pairs_ + gridDim.x - 1) / gridDim.x;\n"
+      << "  const u64 pend_ = min(pairs_, (u64)(blockIdx.x + 1) * per_cta_);\n"
+      << "  for (u64 pr_ = (u64)blockIdx.x * per_cta_; pr_ < pend_; ++pr_) {\n"
+      << "    const u64 tile = 2 * pr_ + half_;\n"
+      << "    if (tile >= total_tiles) continue;\n";
+  else
+    s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
+                    "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
+                    "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
+                  : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n");
+  s << "    int lo = 0, hi = n_segs - 1;\n"
     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
     ;
   // Direct mode with u32 cells: every thread takes two CONSECUTIVE tuples
@@ -567,7 +622,9 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k) {\n"
         << "          if (!okP[k]) continue;\n"
-        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); continue; }\n"
+        << (rcache ? "          if ((sfP[k] & 3u) == 0) { RC_PUT(sfP[k] >> 2, accP[k]); continue; }\n"
+                   : "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
+                     "continue; }\n")
         << "#pragma unroll\n"
         << "          for (int j = 0; j < 4; ++j) {\n"
         << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"
@@ -675,9 +732,14 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     s << "    const Seg& sg = segs[lo];\n";
     tile_body(s);
   }
-  s
-    << "  }\n"
-    << "  if (err) atomicOr(err_flag, err);\n"
+  s << "  }\n";
+  if (rcache)
+    s << "  if (rq0_ != ~0u) RC_RED(rq0_, ra0_);\n"
+      << "  if (rq1_ != ~0u) RC_RED(rq1_, ra1_);\n"
+      << "  if (rq2_ != ~0u) RC_RED(rq2_, ra2_);\n"
+      << "  if (rq3_ != ~0u) RC_RED(rq3_, ra3_);\n"
+      << "#undef RC_PUT\n#undef RC_RED\n";
+  s << "  if (err) atomicOr(err_flag, err);\n"
     << "}\n";
   return s.str();
 }
@@ -745,6 +807,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
   }
   std::lock_guard<std::mutex> g(g_mu);
   if (out->kernels.size() != nc) out->kernels.assign(nc, nullptr);
+  if (out->threads.size() != nc) out->threads.assign(nc, MAPC_GEN_THREADS);
   for (size_t i = 0; i < nc; ++i) {
     if (!want[i]) continue;
     auto it = g_cache.find(keys[i]);
@@ -754,6 +817,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
         return 1;
       }
       Module m;
+      m.threads = kernel_threads(chunks[i], mode, cell_bytes[i]);
       cudaError_t e = cudaLibraryLoadData(&m.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
       if (e != cudaSuccess) {
         *log = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
@@ -769,6 +833,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
       it = g_cache.emplace(keys[i], std::move(m)).first;
     }
     out->kernels[i] = it->second.kernels[0];
+    out->threads[i] = it->second.threads;
   }
   return 0;
 }
@@ -793,15 +858,25 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
                          int n_sms, int max_ctas_per_sm, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
+  const int threads = chunk < h.threads.size() ? h.threads[chunk] : MAPC_GEN_THREADS;
+  const int tiles_per_cta = threads / MAPC_GEN_THREADS;         // the cached direct generate: two
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0);
   if (occ < 1) occ = 1;
-  if (max_ctas_per_sm > 0 && occ > max_ctas_per_sm) occ = max_ctas_per_sm;
+  // max_ctas_per_sm counts MAPC_GEN_THREADS-sized CTAs (the overlapped pipeline's share)
+  if (max_ctas_per_sm > 0 && occ * tiles_per_cta > max_ctas_per_sm) occ = std::max(1, max_ctas_per_sm / tiles_per_cta);
   const unsigned long long capb = (unsigned long long)n_sms * occ;
-  const int grid = (int)(total_tiles < capb ? total_tiles : capb);
+  const unsigned long long units = (total_tiles + tiles_per_cta - 1) / tiles_per_cta;
+  const int grid = (int)(units < capb ? units : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
                   (void*)&cap, (void*)&target};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
+  return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, s);
+}
+
+int kernel_threads(const JitChunk& ch, uint32_t mode, uint32_t cell_bytes) {
+  static const bool rc_env = [] { const char* e = getenv("MAPC_RED_CACHE"); return !(e && e[0] == '0'); }();
+  const bool rcache = rc_env && mode == MAPC_MODE_DIRECT && cell_bytes == 2 && ch.lay.sort_bits <= 31;
+  return rcache ? 2 * MAPC_GEN_THREADS : MAPC_GEN_THREADS;
 }
 
 }  // namespace mapj

@@ -32,7 +32,13 @@ struct JitChunk {
 
 struct JitHandle {
   std::vector<cudaKernel_t> kernels;   // one per chunk
+  std::vector<int> threads;            // CTA size of each kernel
 };
+
+// CTA size of a chunk's kernel in `mode`: MAPC_GEN_THREADS, or twice that for
+// the direct generate with the per-thread reduction cache (two tiles per CTA
+// step, see chunk_kernel_source).
+int kernel_threads(const JitChunk& ch, uint32_t mode, uint32_t cell_bytes);
 
 // mode: MAPC_MODE_KEYS (keys -> key buffer), MAPC_MODE_DIRECT (red.or into the
 // direct-address table passed as `keys`, cells of cell_bytes), MAPC_MODE_FILTER

@@ -1,25 +1,36 @@
-"""Device throughput of every config family at full size (every detect path)."""
+"""Device throughput of every config family at full size (every detect path).
+
+Usage: python scripts/probe_configs.py [names...] [--paths auto,unit,direct,table,sort]"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2203_12878_b200 as mc
 from workloads import config, CONFIG_NAMES
 
-for name in CONFIG_NAMES:
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+paths = ("auto", "unit", "direct", "table", "sort")
+for a in sys.argv[1:]:
+    if a.startswith("--paths="):
+        paths = tuple(a.split("=", 1)[1].split(","))
+for name in (args or CONFIG_NAMES):
+    if name.startswith("5"):
+        continue
     inst = config(name)
     p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
     scratch = torch.empty(p.scratch_bytes(), dtype=torch.uint8, device="cuda")
     out = {"cfg": name}
-    for det in ("auto", "direct", "table", "sort"):
-        p.check_races(scratch=scratch, detect=det)
+    for det in paths:
+        gen = "jit" if det == "unit" else "auto"
+        p.check_races(scratch=scratch, detect=det, gen=gen)
         ms = []
-        for _ in range(3):
-            r = p.check_races(scratch=scratch, detect=det)
+        for _ in range(5):
+            r = p.check_races(scratch=scratch, detect=det, gen=gen)
             ms.append(r.device_ms)
         best = min(ms)
-        out[det] = {"ms": round(best, 3), "G_acc_s": round(r.n_accesses / best / 1e6, 2),
-                    "res": [r.verdict, r.witness.as_tuple() if r.witness else None, r.racy_segments]}
+        k = p.check_races(scratch=scratch, detect=det, gen=gen, profile=True).kernels
+        out[det] = {"ms": round(best, 4), "G_acc_s": round(r.n_accesses / best / 1e6, 2),
+                    "res": [r.verdict, r.witness.as_tuple() if r.witness else None, r.racy_segments],
+                    "top": sorted(((v["ms"], c) for c, v in k.items() if v["launches"]), reverse=True)[:3]}
     out["n"] = r.n_accesses
-    out["verdict"] = r.verdict
     out["chunks"] = r.n_chunks
     print(json.dumps(out), flush=True)
