@@ -210,7 +210,6 @@ std::string prelude() {
 struct Module {
   cudaLibrary_t lib = nullptr;
   std::vector<cudaKernel_t> kernels;
-  int threads = MAPC_GEN_THREADS;
 };
 
 std::mutex g_mu;
@@ -238,7 +237,7 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   }
   put(k, ch.segs.size());
   k.append(reinterpret_cast<const char*>(ch.segs.data()), ch.segs.size() * sizeof(MapcSeg));
-  if (mode == MAPC_MODE_UNIT) {
+  if (mode == MAPC_MODE_UNIT || mode == MAPC_MODE_UNITF) {
     put(k, ch.n_blocks);
     put(k, ch.unit_segs.size());
     k.append(reinterpret_cast<const char*>(ch.unit_segs.data()), ch.unit_segs.size() * sizeof(MapcSeg));
@@ -296,7 +295,10 @@ std::string emit_tail(uint32_t mode, uint32_t w_tid, int T) {
 // sort field atomicMin-ed into ctrl->racy_sf) and moves to its next unit.  No
 // table in HBM, no clear and no scan launch.  The witness cell's keys are
 // re-emitted by the filter-mode kernel as on the HBM direct path.
-std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t cell_bytes) {
+std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t cell_bytes, bool filter) {
+  // filter = MAPC_MODE_UNITF: re-emit the keys of the witness cell (sort field
+  // *target_ptr) from the tuples of its unit only -- the unit-mode counterpart of
+  // the filter generate, which would walk every tile of the chunk.
   std::ostringstream s;
   const int T = MAPC_GEN_THREADS;
   const MapcLayout& L = ch.lay;
@@ -305,43 +307,67 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   const uint64_t words = cell_bytes == 2 ? (cells + 1) / 2 : cells;
   const uint64_t nb = std::max<uint64_t>(ch.n_blocks, 1);
   const uint32_t wt = L.w_tid;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index
-    << "(unsigned long long n_units, unsigned long long* n_ctr, unsigned long long* racy_ctr, "
-       "unsigned long long* racy_sf, u32* err_flag) {\n"
-    << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
+  const uint32_t hb = L.w_array + L.w_block + L.w_index;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index;
+  if (filter)
+    s << "(const unsigned long long* target_ptr, unsigned long long* keys, unsigned long long* n_ctr, "
+         "unsigned long long cap, u32* err_flag) {\n";
+  else
+    s << "(unsigned long long n_units, unsigned long long* n_ctr, unsigned long long* racy_ctr, "
+         "unsigned long long* racy_sf, u32* err_flag) {\n";
+  s << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
     << "  const u32 WI = " << L.w_index << "u; (void)WI;\n"
     << "  const u64 IDX_LO = " << L.idx_lo << "ull;\n"
     << "  const u32 TMASK = " << (wt >= 32 ? 0xFFFFFFFFu : ((1u << wt) - 1u)) << "u; (void)TMASK;\n"
-    << "  __shared__ u32 tab[" << words << "];\n"
     << "  const int me = threadIdx.x;\n"
-    << "  u32 err = 0, cnt = 0;\n"
-    << "  unsigned long long racy = 0, best = ~0ull;\n"
-    << "  for (unsigned long long u = blockIdx.x; u < n_units; u += gridDim.x) {\n"
-    << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
-    << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) tab[i] = 0u;\n"
-    << "    __syncthreads();\n";
-  // the unit-local cell of an access: (array, index - idx_lo)
+    << "  u32 err = 0, cnt = 0;\n";
+  if (filter) {
+    s << "  const unsigned long long target = *target_ptr;\n"
+      << "  if (target == ~0ull) return;\n"
+      << "  const u32 lph = " << (hb >= 64 ? "0u" : "(u32)(target >> " + std::to_string(hb) + "u)") << ";\n"
+      << "  const u32 lb = (u32)((target >> WI) & " << ((1ull << L.w_block) - 1) << "ull);\n"
+      << "  const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
+      << "u;\n"
+      << "  {\n";
+  } else {
+    s << "  __shared__ u32 tab[" << words << "];\n"
+      << "  unsigned long long racy = 0, best = ~0ull;\n"
+      << "  for (unsigned long long u = blockIdx.x; u < n_units; u += gridDim.x) {\n"
+      << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
+      << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) tab[i] = 0u;\n"
+      << "    __syncthreads();\n";
+  }
   s << "#define EMIT_KEY(IX, ARR, KIND) { u64 idx_ = (u64)(IX) - IDX_LO; "
-       "if (WI < 64 && (idx_ >> WI) != 0) { err |= " << MAPC_ERR_LAYOUT << "u; idx_ = 0; } "
-       "const u32 c_ = ((u32)(ARR) << WI) | (u32)idx_; ";
-  if (cell_bytes == 2)
-    s << "atomicOr(&tab[c_ >> 1], (tcd_ | ((u32)(KIND) << 14)) << (16u * (c_ & 1u))); ";
-  else
-    s << "atomicOr(&tab[c_], tidv | ((~tidv & TMASK) << " << wt << "u) | ((u32)(KIND) << " << 2 * wt << "u)); ";
-  s << "if (!sg.dense) ++cnt; }\n";
+       "if (WI < 64 && (idx_ >> WI) != 0) { err |= " << MAPC_ERR_LAYOUT << "u; idx_ = 0; } ";
+  if (filter) {
+    // the access's sort field; matches are appended (warp-aggregated slot reservation)
+    s << "const u64 sf_ = base_ + ((u64)(ARR) << " << L.w_block + L.w_index << "u) + idx_; "
+         "const bool hit_ = sf_ == target; const u32 hm_ = __ballot_sync(__activemask(), hit_); "
+         "if (hit_) { const u32 ln_ = me & 31u, ld_ = __ffs(hm_) - 1u; u64 b_ = 0; "
+         "if (ln_ == ld_) b_ = atomicAdd(n_ctr, (u64)__popc(hm_)); b_ = __shfl_sync(hm_, b_, ld_); "
+         "const u64 pos_ = b_ + __popc(hm_ & ((1u << ln_) - 1u)); "
+         "if (pos_ < cap) keys[pos_] = (sf_ << " << L.pay_bits << "u) | ((u64)tidv << 1) | (KIND); else err |= "
+      << MAPC_ERR_CAPACITY << "u; } }\n";
+  } else {
+    // the unit-local cell of an access: (array, index - idx_lo)
+    s << "const u32 c_ = ((u32)(ARR) << WI) | (u32)idx_; ";
+    if (cell_bytes == 2)
+      s << "atomicOr(&tab[c_ >> 1], (tcd_ | ((u32)(KIND) << 14)) << (16u * (c_ & 1u))); ";
+    else
+      s << "atomicOr(&tab[c_], tidv | ((~tidv & TMASK) << " << wt << "u) | ((u32)(KIND) << " << 2 * wt << "u)); ";
+    s << "if (!sg.dense) ++cnt; }\n";
+  }
   auto fd = [](const MapcFastDiv& f) {
     std::ostringstream o;
     o << "{" << f.d << "u, " << f.m << "u, " << f.s << "u, " << f.pow2 << "u}";
     return o.str();
   };
-  const uint32_t hb = L.w_array + L.w_block + L.w_index;
   for (const MapcSeg& g : ch.unit_segs) {
     const JitProgram* pg = nullptr;
     for (const JitProgram& p : ch.programs)
       if (p.prog_begin == g.prog_begin) pg = &p;
     if (!pg) continue;
-    uint64_t tpb = MAPC_GEN_THREADS;   // tuples per block of the segment: blockDim * prod(trips)
-    tpb = g.tid_div.d;
+    uint64_t tpb = g.tid_div.d;        // tuples per block of the segment: blockDim * prod(trips)
     for (uint32_t l = 0; l < g.n_levels; ++l) tpb *= g.trip_div[l].d;
     const uint64_t seg_nb = g.n_tuples / std::max<uint64_t>(tpb, 1);
     const uint32_t seg_lph = hb >= 64 ? 0u : (uint32_t)(g.key_hi >> hb);
@@ -358,9 +384,12 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
     const bool tid_is_inner = pg->tid_inner || pg->n_levels == 0;
     const bool quad = pg->inner_range % 4 == 0 && tpb % 4 == 0;
     const uint32_t inner_reg = tid_is_inner ? MAPC_REG_TID : MAPC_REG_K0 + pg->n_levels - 1;
+    const uint32_t step = quad ? 4 : 1;
+    const std::string first = filter ? "(blockIdx.x * " + std::to_string(T) + "u + me) * " + std::to_string(step) + "u"
+                                     : std::to_string(step) + "u * me";
+    const std::string stride = filter ? "gridDim.x * " + std::to_string(T * step) + "u" : std::to_string(T * step) + "u";
     s << "#pragma unroll 1\n"
-      << "      for (u32 k = " << (quad ? "4u * me" : "me") << "; k < " << tpb << "u; k += " << (quad ? 4 * T : T)
-      << "u) {\n"
+      << "      for (u32 k = " << first << "; k < " << tpb << "u; k += " << stride << ") {\n"
       << "        const u32 t = t0 + k; (void)t;\n"
       << "        const bool valid = true;\n"
       << "        u32 rem = t;\n"
@@ -376,7 +405,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
     } else {
       s << "        {\n";
     }
-    if (cell_bytes == 2) s << "        const u32 tcd_ = code16(tidv, 0u);\n";
+    if (cell_bytes == 2 && !filter) s << "        const u32 tcd_ = code16(tidv, 0u);\n";
     s << "        bool act = true;\n"
       << "        u32 e = 0;\n"
       << program_body(pg->ops, u32)
@@ -385,8 +414,15 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "      }\n"
       << "    }\n";
   }
-  s << "#undef EMIT_KEY\n"
-    << "    __syncthreads();\n"
+  s << "#undef EMIT_KEY\n";
+  if (filter) {
+    s << "  }\n"
+      << "  (void)cnt;\n"
+      << "  if (err) atomicOr(err_flag, err);\n"
+      << "}\n";
+    return s.str();
+  }
+  s << "    __syncthreads();\n"
     << "    const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
     << "u;\n"
     << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) {\n"
@@ -432,7 +468,8 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
 
 std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes) {
   static_assert(sizeof(MapcSeg) == 5 * 8 + 8 * 4 + 9 * 16, "Seg layout mirrored in the JIT prelude");
-  if (mode == MAPC_MODE_UNIT) return unit_kernel_source(ch, index, u32, cell_bytes);
+  if (mode == MAPC_MODE_UNIT || mode == MAPC_MODE_UNITF)
+    return unit_kernel_source(ch, index, u32, cell_bytes, mode == MAPC_MODE_UNITF);
   std::ostringstream s;
   const int T = MAPC_GEN_THREADS, V = MAPC_GEN_V;
   // keys staged per thread per tile for compaction: the guarded segments' emits
@@ -452,19 +489,12 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // on 5a with the blocked, carry-free paired generate (profiles/r1q_probe_minb.txt);
   // MAPC_JIT_MINB overrides (0 = none)
   static const int minb_env = [] { const char* e = getenv("MAPC_JIT_MINB"); return e ? atoi(e) : 10; }();
-  // Per-thread reduction cache (direct mode, 16-bit cells, 32-bit sort fields):
-  // the CTA is two tile-sized halves; half h takes tile 2p + h of the CTA's
-  // p-th tile pair, so a thread's successive tiles are two tiles apart -- for a
-  // row sweep of 1024 columns (5a: 2 tiles per row) the same columns of the next
-  // row.  The aligned-quad red.or.b64 of a site goes through a 4-entry cache of
-  // (quad, OR of codes): a quad touched again before its eviction (5a: the reads
-  // of row x come from rows x-1, x, x+1 of the same thread) is ORed in a
-  // register instead of a second global reduction.  Same cells, same codes: the
-  // table is identical; the evicted and finally flushed entries are plain reds.
-  const int CT = kernel_threads(ch, mode, cell_bytes);
-  const bool rcache = CT != T;
-  const int minb = mode == MAPC_MODE_DIRECT ? (rcache ? std::max(1, minb_env * T / CT) : minb_env) : 0;
-  s << "extern \"C\" __global__ void __launch_bounds__(" << CT;
+  // (A per-thread 4-entry cache of aligned quads, which halves 5a's global
+  // red.or.b64 count by folding the three reads of a row in registers, was
+  // measured 25% SLOWER: the direct generate is bound by the table's DRAM
+  // read-modify-write traffic, not by the reduction count -- DESIGN.md §6.1.)
+  const int minb = mode == MAPC_MODE_DIRECT ? minb_env : 0;
+  s << "extern \"C\" __global__ void __launch_bounds__(" << T;
   if (minb > 0) s << ", " << minb;
   s << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
@@ -477,9 +507,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     << "  __shared__ u64 stage[" << stage_emits << " * " << T << "];\n"
     << "  __shared__ u32 scan_tmp[" << T / 32 + 1 << "];\n"
     << "  __shared__ u64 s_base;\n"
-    << (rcache ? "  const int me = threadIdx.x & " + std::to_string(T - 1) + ", half_ = threadIdx.x / " +
-                     std::to_string(T) + ";\n"
-               : std::string("  const int me = threadIdx.x;\n"))
+    << "  const int me = threadIdx.x;\n"
     << "  u32 err = 0;\n"
     << "  const u64 TMASK = " << (ch.lay.w_tid >= 64 ? ~0ull : ((1ull << ch.lay.w_tid) - 1)) << "ull;\n"
     << "  (void)TMASK; (void)target_ptr;\n";
@@ -491,22 +519,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
-  if (rcache)
-    s << "  u32 rq0_ = ~0u, rq1_ = ~0u, rq2_ = ~0u, rq3_ = ~0u; u64 ra0_ = 0, ra1_ = 0, ra2_ = 0, ra3_ = 0;\n"
-      << "#define RC_RED(Q, A) atomicOr(reinterpret_cast<u64*>(keys) + (Q), (A))\n"
-      << "#define RC_PUT(Q, A) { const u32 q_ = (Q); const u64 a_ = (A); "
-         "if (q_ == rq0_) ra0_ |= a_; else if (q_ == rq1_) ra1_ |= a_; else if (q_ == rq2_) ra2_ |= a_; "
-         "else if (q_ == rq3_) ra3_ |= a_; "
-         "else { if (rq0_ != ~0u) RC_RED(rq0_, ra0_); rq0_ = rq1_; ra0_ = ra1_; rq1_ = rq2_; ra1_ = ra2_; "
-         "rq2_ = rq3_; ra2_ = ra3_; rq3_ = q_; ra3_ = a_; } }\n"
-      << "  const u64 pairs_ = (total_tiles + 1) >> 1;\n"
-      << "  const u64 per_cta_ = (pairs_ + gridDim.x - 1) / gridDim.x;\n"
-      << "  const u64 pend_ = min(pairs_, (u64)(blockIdx.x + 1) * per_cta_);\n"
-      << "  for (u64 pr_ = (u64)blockIdx.x * per_cta_; pr_ < pend_; ++pr_) {\n"
-      << "    const u64 tile = 2 * pr_ + half_;\n"
-      << "    if (tile >= total_tiles) continue;\n";
-  else
-    s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
+  s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
                     "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
                     "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
                   : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n");
@@ -622,9 +635,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k) {\n"
         << "          if (!okP[k]) continue;\n"
-        << (rcache ? "          if ((sfP[k] & 3u) == 0) { RC_PUT(sfP[k] >> 2, accP[k]); continue; }\n"
-                   : "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
-                     "continue; }\n")
+        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
+           "continue; }\n"
         << "#pragma unroll\n"
         << "          for (int j = 0; j < 4; ++j) {\n"
         << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"
@@ -733,12 +745,6 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     tile_body(s);
   }
   s << "  }\n";
-  if (rcache)
-    s << "  if (rq0_ != ~0u) RC_RED(rq0_, ra0_);\n"
-      << "  if (rq1_ != ~0u) RC_RED(rq1_, ra1_);\n"
-      << "  if (rq2_ != ~0u) RC_RED(rq2_, ra2_);\n"
-      << "  if (rq3_ != ~0u) RC_RED(rq3_, ra3_);\n"
-      << "#undef RC_PUT\n#undef RC_RED\n";
   s << "  if (err) atomicOr(err_flag, err);\n"
     << "}\n";
   return s.str();
@@ -807,7 +813,6 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
   }
   std::lock_guard<std::mutex> g(g_mu);
   if (out->kernels.size() != nc) out->kernels.assign(nc, nullptr);
-  if (out->threads.size() != nc) out->threads.assign(nc, MAPC_GEN_THREADS);
   for (size_t i = 0; i < nc; ++i) {
     if (!want[i]) continue;
     auto it = g_cache.find(keys[i]);
@@ -817,7 +822,6 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
         return 1;
       }
       Module m;
-      m.threads = kernel_threads(chunks[i], mode, cell_bytes[i]);
       cudaError_t e = cudaLibraryLoadData(&m.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
       if (e != cudaSuccess) {
         *log = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
@@ -833,7 +837,6 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
       it = g_cache.emplace(keys[i], std::move(m)).first;
     }
     out->kernels[i] = it->second.kernels[0];
-    out->threads[i] = it->second.threads;
   }
   return 0;
 }
@@ -852,31 +855,32 @@ cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 
+cudaError_t launch_unit_filter(const JitHandle& h, size_t chunk, const unsigned long long* target,
+                               unsigned long long* keys, unsigned long long* n_ctr, unsigned long long cap,
+                               unsigned int* err_flag, unsigned long long unit_accesses, int n_sms, cudaStream_t s) {
+  const void* fn = (const void*)h.kernels[chunk];
+  const unsigned long long per_cta = 4ull * MAPC_GEN_THREADS;
+  unsigned long long grid = (unit_accesses + per_cta - 1) / per_cta;
+  grid = std::max<unsigned long long>(1, std::min<unsigned long long>(grid, (unsigned long long)n_sms));
+  void* args[] = {(void*)&target, (void*)&keys, (void*)&n_ctr, (void*)&cap, (void*)&err_flag};
+  return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(MAPC_GEN_THREADS), args, 0, s);
+}
+
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
                          int n_sms, int max_ctas_per_sm, cudaStream_t s) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
-  const int threads = chunk < h.threads.size() ? h.threads[chunk] : MAPC_GEN_THREADS;
-  const int tiles_per_cta = threads / MAPC_GEN_THREADS;         // the cached direct generate: two
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
   if (occ < 1) occ = 1;
-  // max_ctas_per_sm counts MAPC_GEN_THREADS-sized CTAs (the overlapped pipeline's share)
-  if (max_ctas_per_sm > 0 && occ * tiles_per_cta > max_ctas_per_sm) occ = std::max(1, max_ctas_per_sm / tiles_per_cta);
+  if (max_ctas_per_sm > 0 && occ > max_ctas_per_sm) occ = max_ctas_per_sm;
   const unsigned long long capb = (unsigned long long)n_sms * occ;
-  const unsigned long long units = (total_tiles + tiles_per_cta - 1) / tiles_per_cta;
-  const int grid = (int)(units < capb ? units : capb);
+  const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
                   (void*)&cap, (void*)&target};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, s);
-}
-
-int kernel_threads(const JitChunk& ch, uint32_t mode, uint32_t cell_bytes) {
-  static const bool rc_env = [] { const char* e = getenv("MAPC_RED_CACHE"); return !(e && e[0] == '0'); }();
-  const bool rcache = rc_env && mode == MAPC_MODE_DIRECT && cell_bytes == 2 && ch.lay.sort_bits <= 31;
-  return rcache ? 2 * MAPC_GEN_THREADS : MAPC_GEN_THREADS;
+  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 
 }  // namespace mapj

@@ -32,13 +32,7 @@ struct JitChunk {
 
 struct JitHandle {
   std::vector<cudaKernel_t> kernels;   // one per chunk
-  std::vector<int> threads;            // CTA size of each kernel
 };
-
-// CTA size of a chunk's kernel in `mode`: MAPC_GEN_THREADS, or twice that for
-// the direct generate with the per-thread reduction cache (two tiles per CTA
-// step, see chunk_kernel_source).
-int kernel_threads(const JitChunk& ch, uint32_t mode, uint32_t cell_bytes);
 
 // mode: MAPC_MODE_KEYS (keys -> key buffer), MAPC_MODE_DIRECT (red.or into the
 // direct-address table passed as `keys`, cells of cell_bytes), MAPC_MODE_FILTER
@@ -59,5 +53,10 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
 cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,
                          unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag, int n_sms,
                          cudaStream_t s);
+// Unit filter (MAPC_MODE_UNITF): the keys of cell *target from its unit's tuples
+// (unit_accesses bounds them; sets the grid), appended to keys[cap], counted in *n_ctr.
+cudaError_t launch_unit_filter(const JitHandle& h, size_t chunk, const unsigned long long* target,
+                               unsigned long long* keys, unsigned long long* n_ctr, unsigned long long cap,
+                               unsigned int* err_flag, unsigned long long unit_accesses, int n_sms, cudaStream_t s);
 
 }  // namespace mapj

@@ -10,6 +10,7 @@
 // (R10): the canonical witness is the
 // lexicographic minimum of the per-chunk witnesses, taken on the host.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -112,7 +113,7 @@ struct Chunk {
 struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
-  mapj::JitHandle jit[4];                    // per generate mode (MAPC_MODE_*); null = not built yet
+  mapj::JitHandle jit[5];                    // per generate mode (MAPC_MODE_*); null = not built yet
   size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
   size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
   size_t off_ctrl2 = 0;                     // second control block (overlapped direct pipeline)
@@ -127,6 +128,14 @@ struct Plan {
 };
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// NVTX range for the host-side stages (visible in nsys / ncu timelines)
+struct NvtxRange {
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace
 
@@ -656,6 +665,7 @@ size_t map_scratch_bytes(const map_program* cp, uint64_t chunk_max_accesses) {
 
 map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) {
   if (!p || !ex || !out) return MAP_E_ARG;
+  NvtxRange nvtx_run("map_check_races");
   p->have_witness = false;
   const uint32_t world = ex->world ? ex->world : 1;
   const uint32_t rank = ex->rank;
@@ -727,14 +737,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   if (gen_mode == 1 && !mine.empty()) {
     // the kernels this run needs, per mode: keys (sort / table detect), direct +
     // filter (direct detect), for this rank's chunks only
-    std::vector<char> want[4];
-    bool any[4] = {false, false, false, false};
-    for (uint32_t m = 0; m < 4; ++m) want[m].assign(P.chunks.size(), 0);
+    std::vector<char> want[5];
+    bool any[5] = {false, false, false, false, false};
+    for (uint32_t m = 0; m < 5; ++m) want[m].assign(P.chunks.size(), 0);
     for (size_t c : mine) {
       const bool un = use_unit(P.chunks[c], ex->flags, 1);
       const bool d = !un && use_direct(P.chunks[c], ex->flags);
-      for (uint32_t m = 0; m < 4; ++m) {
-        const bool w = un  ? (m == MAPC_MODE_UNIT || m == MAPC_MODE_FILTER)
+      for (uint32_t m = 0; m < 5; ++m) {
+        const bool w = un  ? (m == MAPC_MODE_UNIT || m == MAPC_MODE_UNITF)
                        : d ? (m == MAPC_MODE_DIRECT || m == MAPC_MODE_FILTER)
                            : m == MAPC_MODE_KEYS;
         const bool have = P.jit[m].kernels.size() == P.chunks.size() && P.jit[m].kernels[c] != nullptr;
@@ -748,14 +758,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       cb.push_back(ch.cell_bytes);
     }
     std::vector<std::thread> builders;
-    std::string logs[4];
-    int rcs[4] = {0, 0, 0, 0};
-    for (uint32_t m = 0; m < 4; ++m)
+    std::string logs[5];
+    int rcs[5] = {0, 0, 0, 0, 0};
+    for (uint32_t m = 0; m < 5; ++m)
       if (any[m])
         builders.emplace_back(
             [&, m]() { rcs[m] = mapj::build_module(jc, p->C.u32_mode, m, cb, want[m], &P.jit[m], &logs[m]); });
     for (auto& t : builders) t.join();
-    for (uint32_t m = 0; m < 4; ++m)
+    for (uint32_t m = 0; m < 5; ++m)
       if (rcs[m] != 0) {
         p->last_error = "specialised generate: " + logs[m];
         return MAP_E_CUDA;
@@ -864,6 +874,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     }
     for (size_t i = 0; i < mine.size(); ++i) {
       const size_t c = mine[i];
+      NvtxRange nvtx_chunk("chunk " + std::to_string(c) + " direct (overlapped)");
       const Chunk& ch = P.chunks[c];
       const MapcLayout L = effective_layout(ch, ex->flags);
       const int b = (int)(i & 1);
@@ -925,6 +936,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   for (size_t c : mine) {
     if (ovl) break;
     const Chunk& ch = P.chunks[c];
+    NvtxRange nvtx_chunk("chunk " + std::to_string(c) +
+                         (use_unit(ch, ex->flags, gen_mode) ? " unit" : use_direct(ch, ex->flags) ? " direct" : " keys"));
     const MapcLayout L = effective_layout(ch, ex->flags);
     CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
     CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, s));
@@ -947,8 +960,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       if (ch.total_tiles) {
         ++launches;
         st_acc.launches[MAP_K_OTHER]++;
-        CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, segs, (int)ch.segs.size(), ch.total_tiles, bufA, &ctrl->nf,
-                              &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s));
+        CK(mapj::launch_unit_filter(P.jit[MAPC_MODE_UNITF], c, &ctrl->wit_sf, bufA, &ctrl->nf, L.cap, &ctrl->err,
+                                    (ch.bound + n_units - 1) / std::max<uint64_t>(n_units, 1), n_sms, s));
       }
       CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s));
       CK(mapc_launch_chunk_finish(ctrl, 0, res + c, s));
@@ -1539,8 +1552,8 @@ int map_debug_jit_check(const map_program* cp, uint64_t chunk_max_accesses, char
         std::string li;
         std::vector<mapj::JitChunk> one{chunks[i].jit};
         bool bad = false;
-        for (uint32_t mode = 0; mode < 4 && !bad; ++mode)
-          if (mode != MAPC_MODE_UNIT || chunks[i].unit_ok)
+        for (uint32_t mode = 0; mode < 5 && !bad; ++mode)
+          if ((mode != MAPC_MODE_UNIT && mode != MAPC_MODE_UNITF) || chunks[i].unit_ok)
             bad = mapj::compile_cubin(mapj::module_source(one, p->C.u32_mode, mode, chunks[i].cell_bytes), &cubin,
                                     &li) != 0;
         if (bad) {

@@ -46,6 +46,7 @@
 #define MAPC_MODE_DIRECT 1u    // fold every access into its cell of the direct-address table (direct.cu)
 #define MAPC_MODE_FILTER 2u    // re-emit only the keys whose sort field is ctrl->racy_sf (witness cell)
 #define MAPC_MODE_UNIT 3u      // per (phase, block) unit: fold its accesses into a shared-memory table and scan it (JIT only)
+#define MAPC_MODE_UNITF 4u     // unit mode's filter: re-emit the witness cell's keys from its unit's tuples only
 #define MAPC_UNIT_MAX_BYTES 32768u  // table bytes of one unit (static shared memory)
 #define MAPC_UNIT_MAX_SEGS 8u       // segments of a unit-mode chunk (baked as literals)
 

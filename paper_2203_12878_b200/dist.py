@@ -24,9 +24,18 @@ from typing import Optional
 import torch
 import torch.distributed as dist
 
-from . import MapProgram, Result, Witness
+from . import MapError, MapProgram, Result, Witness
 
 _NONE = -1
+MAP_E_COMM = 7          # include/mapcheck.h: a failed collective (NCCL / gloo)
+
+
+def _comm(fn, *args, **kw):
+    """Run a torch.distributed collective; a failure becomes MapError(MAP_E_COMM)."""
+    try:
+        return fn(*args, **kw)
+    except (RuntimeError, ValueError) as e:          # NCCL / gloo errors surface as RuntimeError
+        raise MapError(MAP_E_COMM, f"{getattr(fn, '__name__', 'collective')}: {e}") from e
 
 
 def _pack(r: Result, device) -> torch.Tensor:
@@ -39,7 +48,7 @@ def reduce_results(local: Result, array_names, group=None, device="cpu") -> Resu
     world = dist.get_world_size(group)
     mine = _pack(local, device)
     bufs = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(bufs, mine, group=group)
+    _comm(dist.all_gather, bufs, mine, group=group)
     rows = [b.cpu().tolist() for b in bufs]
     n = sum(r[1] for r in rows)
     racy = sum(r[2] for r in rows)
@@ -75,11 +84,11 @@ def _exchange_chunk(prog: MapProgram, chunk: int, scratch, stream, chunk_max_acc
     counts = prog.generate_bucketed(chunk, rank, world, out, scratch, stream, chunk_max_accesses)
     send = torch.tensor(counts, dtype=torch.int64, device=device)
     recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)                  # counts
+    _comm(dist.all_to_all_single, recv, send, group=group)            # counts
     rsizes = [int(x) for x in recv.tolist()]
     got = torch.empty(max(sum(rsizes), 1), dtype=torch.int64, device=device)
-    dist.all_to_all_single(got[:sum(rsizes)], out[:sum(counts)], output_split_sizes=rsizes,
-                           input_split_sizes=counts, group=group)      # keys, bucketed by hash
+    _comm(dist.all_to_all_single, got[:sum(rsizes)], out[:sum(counts)], output_split_sizes=rsizes,
+          input_split_sizes=counts, group=group)                       # keys, bucketed by hash
     packed, racy = prog.sort_detect(chunk, got, sum(rsizes), scratch, stream, chunk_max_accesses)
     return packed, racy, sum(rsizes)
 

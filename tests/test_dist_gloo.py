@@ -163,3 +163,13 @@ def test_exchange_routing(world):
             assert keys == want                      # every key arrives once, at its hash owner
         assert (verdict, n, racy) == (1, total, total)
         assert w == (0, 0, 0, 0, 0, 1, 0, 1)         # global min over chunks and ranks
+
+
+def test_collective_failure_maps_to_map_e_comm():
+    # a collective that fails (here: no process group) surfaces as MAP_E_COMM (7)
+    from paper_2203_12878_b200 import MapError
+    from paper_2203_12878_b200.dist import _comm
+    assert not dist.is_initialized()
+    with pytest.raises(MapError) as e:
+        _comm(dist.all_gather, [torch.empty(3)], torch.zeros(3))
+    assert e.value.status == 7 and "all_gather" in str(e.value)
