@@ -10,10 +10,10 @@ namespace {
 const char* kPrelude = R"(
 typedef unsigned int u32;
 typedef unsigned long long u64;
-struct BcCtl { u64 n_keys, uninit, ambiguous; u32 err, pad; };
+struct BcCtl { u64 n_keys, max_block, uninit, ambiguous; u32 err, pad; };   // = bcg::BcCtl
 struct St {
   u64* mem; u64* cval; u32* own; u32* minw; u32* claims; unsigned char* st; u64* logb;
-  u32* s_nclaim; u32* s_conf;
+  u32* s_nclaim; u32* s_conf; u32* s_nkeys;
   u64* keys; u64 cap; BcCtl* ctl;
   u32 nlog, err, tid, phase;
   u64 uninit, ambig, blk;
@@ -34,14 +34,15 @@ __device__ __forceinline__ u64 bc_shr(u64 a, u64 b) { return b >= 64 ? 0ull : a 
 __device__ __forceinline__ u64 bc_min(u64 a, u64 b) { return a < b ? a : b; }
 __device__ __forceinline__ u64 bc_max(u64 a, u64 b) { return a > b ? a : b; }
 
-// one access value into the alpha buffer (warp-aggregated slot reservation)
+// one access value into the block's region of the alpha buffer (S.keys = the
+// region, S.cap its size; warp-aggregated slot reservation on a shared counter)
 __device__ __forceinline__ void bc_emit(St& S, u64 key) {
   const u32 m = __activemask();
   const u32 lane = S.tid & 31u, lead = __ffs(m) - 1u;
-  u64 b = 0;
-  if (lane == lead) b = atomicAdd(&S.ctl->n_keys, (u64)__popc(m));
+  u32 b = 0;
+  if (lane == lead) b = atomicAdd(S.s_nkeys, (u32)__popc(m));
   b = __shfl_sync(m, b, lead);
-  const u64 p = b + __popc(m & ((1u << lane) - 1u));
+  const u64 p = (u64)b + __popc(m & ((1u << lane) - 1u));
   if (p < S.cap) S.keys[p] = key;
 }
 
@@ -237,9 +238,9 @@ std::string kernel_source(const bcf::Kernel& K, const Plan& P) {
     << kPrelude;
   const uint64_t n = P.n_cells;
   o << "extern \"C\" __global__ void __launch_bounds__(" << P.block_threads
-    << ") bc_exec(u64* keys, u64 cap, BcCtl* ctl, unsigned char* slots, u64 slot_bytes, u64* mem_out, "
+    << ") bc_exec(u64* keys, u64 block_cap, BcCtl* ctl, unsigned char* slots, u64 slot_bytes, u64* mem_out, "
        "unsigned char* st_out) {\n"
-    << "  __shared__ u32 s_nclaim, s_conf;\n"
+    << "  __shared__ u32 s_nclaim, s_conf, s_nkeys;\n"
     << "  St S;\n"
     << "  unsigned char* base = slots + (u64)blockIdx.x * slot_bytes;\n"
     << "  S.mem = (u64*)base;\n"
@@ -250,21 +251,28 @@ std::string kernel_source(const bcf::Kernel& K, const Plan& P) {
     << "  S.st = base + " << 2 * align16(n * 8) + 3 * align16(n * 4) << "ull;\n"
     << "  S.logb = (u64*)(base + " << 2 * align16(n * 8) + 3 * align16(n * 4) + align16(n) << "ull) + (u64)threadIdx.x * "
     << 2 * P.k_log << "ull;\n"
-    << "  S.s_nclaim = &s_nclaim; S.s_conf = &s_conf;\n"
-    << "  S.keys = keys; S.cap = cap; S.ctl = ctl;\n"
+    << "  S.s_nclaim = &s_nclaim; S.s_conf = &s_conf; S.s_nkeys = &s_nkeys;\n"
+    << "  S.cap = block_cap; S.ctl = ctl;\n"
     << "  S.nlog = 0; S.err = 0; S.tid = threadIdx.x; S.phase = 0; S.uninit = 0; S.ambig = 0;\n";
   for (size_t i = 0; i < K.params.size(); ++i)
     o << "  const u64 P_" << K.params[i] << " = " << P.params[i] << "ull; (void)P_" << K.params[i] << ";\n";
+  // each block's accesses go to its own region of the alpha buffer (block_cap
+  // keys; unused slots keep the host's all-ones fill and sort last), counted on a
+  // shared counter: no global atomic per access
   o << "  for (u64 c = threadIdx.x; c < " << n << "ull; c += blockDim.x) { S.own[c] = 0u; S.minw[c] = 0xFFFFFFFFu; }\n"
     << "  for (u64 blk = blockIdx.x; blk < " << P.n_blocks << "ull; blk += gridDim.x) {\n"
     << "    for (u64 c = threadIdx.x; c < " << n << "ull; c += blockDim.x) S.st[c] = 0;\n"
-    << "    if (threadIdx.x == 0) { s_nclaim = 0u; s_conf = 0u; }\n"
+    << "    if (threadIdx.x == 0) { s_nclaim = 0u; s_conf = 0u; s_nkeys = 0u; }\n"
     << "    __syncthreads();\n"
-    << "    S.blk = blk; S.phase = 0;\n"
+    << "    S.blk = blk; S.phase = 0; S.keys = keys + blk * block_cap;\n"
     << "    {\n";
   g.stmt(K.body.get(), "      ");
   o << "    }\n"
     << "    bc_sync(S);                       // commit the last phase\n"
+    << "    if (threadIdx.x == 0) {\n"
+    << "      atomicAdd(&ctl->n_keys, (u64)s_nkeys);\n"
+    << "      atomicMax(&ctl->max_block, (u64)s_nkeys);\n"
+    << "    }\n"
     << "    if (mem_out)\n"
     << "      for (u64 c = threadIdx.x; c < " << n << "ull; c += blockDim.x) {\n"
     << "        mem_out[blk * " << n << "ull + c] = S.mem[c]; st_out[blk * " << n << "ull + c] = S.st[c]; }\n"

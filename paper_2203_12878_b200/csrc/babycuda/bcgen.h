@@ -40,6 +40,7 @@ struct Plan {
   std::vector<uint64_t> offsets;         // first cell of each array in a block's slot
   uint64_t n_cells = 0;
   uint32_t k_log = 16;                   // conflict-log entries per thread
+  uint64_t block_bound = 0;              // accesses per block, bounded by the inferred MAP (0 = unknown)
   Layout lay;
 };
 
@@ -52,6 +53,7 @@ constexpr uint32_t ERR_LOG = 8u;        // a thread's conflict log overflowed
 // The executor's control block (device).
 struct BcCtl {
   unsigned long long n_keys;            // accesses executed (alpha keys emitted, incl. beyond capacity)
+  unsigned long long max_block;         // most accesses of one block (its region of the alpha buffer)
   unsigned long long uninit;            // reads of bottom
   unsigned long long ambiguous;         // reads of a value committed by a multi-writer phase
   unsigned int err;

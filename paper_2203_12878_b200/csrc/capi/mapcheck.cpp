@@ -165,6 +165,7 @@ struct map_program {
   int cap_dev = -1;
   std::string gkey, glast_key;
   uint32_t g_launches = 0;
+  uint64_t default_cap_cache = 0;    // default_cap(), computed once
   uint64_t g_h2d = 0;
   map_kernel_stats g_stats{};
   ~map_program() {
@@ -516,10 +517,25 @@ uint64_t default_cap(const map_program* p) {
   // is cut in (at least) two chunks so that the direct pipeline can overlap one
   // chunk's table scan with the other's generate (3b: 197 -> 218 G acc/s,
   // profiles/r1r_chunking.jsonl)
+  if (p->default_cap_cache) return p->default_cap_cache;
   uint64_t want = std::min<uint64_t>(p->C.max_accesses, 1ull << 30);
-  if (p->C.max_accesses >= (1ull << 25) && p->C.max_accesses <= (1ull << 31))
-    want = std::min<uint64_t>(want, (p->C.max_accesses + 1) / 2);
-  return std::max<uint64_t>({want, p->C.max_unit, 1});
+  if (p->C.max_accesses >= (1ull << 25) && p->C.max_accesses <= (1ull << 31)) {
+    // ... unless every chunk of the uncut plan runs on chip (unit mode: no table
+    // scan to overlap, and one chunk saves its fixed launches; 3a 0.231 -> ms)
+    bool all_unit = false;
+    {
+      Plan whole;
+      std::string why;
+      const uint64_t full = std::max<uint64_t>({want, p->C.max_unit, 1});
+      if (make_plan(p->C, full, &whole, &why) == MAP_OK && !whole.chunks.empty()) {
+        all_unit = true;
+        for (const Chunk& ch : whole.chunks) all_unit = all_unit && ch.unit_ok;
+      }
+    }
+    if (!all_unit) want = std::min<uint64_t>(want, (p->C.max_accesses + 1) / 2);
+  }
+  const_cast<map_program*>(p)->default_cap_cache = std::max<uint64_t>({want, p->C.max_unit, 1});
+  return p->default_cap_cache;
 }
 
 // Default chunk capacity for a job sharded over `world` ranks: at least two
