@@ -59,6 +59,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--detect", choices=["auto", "direct", "sort", "table"], default="auto")
     ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect paths")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip timing the other BASELINE.json config families (context, not the metric)")
     ap.add_argument("--mode", choices=["shard", "exchange"], default="shard",
                     help="multi-GPU mode: chunk sharding (default) or the key exchange (all_to_all)")
     return ap.parse_args()
@@ -475,6 +477,24 @@ def main():
                 roof_sort = kernel_roofline(k_alt, "onesweep", peak, peak_kind)
                 roof_sort["path"] = "table (partial LSD sort + bucket tables)"
 
+    # the other config families at full size (context for the same metric; the
+    # library's automatic path, CUDA-graph replays, best of 3 device times)
+    others = None
+    if not args.no_other_configs and world == 1 and args.mode == "shard":
+        others = {}
+        for name in ("3a", "3b", "4a", "4b", "4c", "4d", "2b", "1a"):
+            oi = config(name)
+            op = mc.MapProgram(oi.src, oi.grid, oi.block, oi.params)
+            osc = torch.empty(op.scratch_bytes(), dtype=torch.uint8, device="cuda")
+            for _ in range(2):
+                orr = op.check_races(scratch=osc, stream=stream)
+            ms_o = min(op.check_races(scratch=osc, stream=stream).device_ms for _ in range(3))
+            prof = op.check_races(scratch=osc, stream=stream, profile=True).kernels
+            path = max((v["ms"], k) for k, v in prof.items() if k in ("unit", "direct", "onesweep", "detect"))[1]
+            others[name] = {"G_acc_s": orr.n_accesses / ms_o / 1e6, "ms": ms_o, "n_accesses": orr.n_accesses,
+                            "verdict": "racy" if orr.verdict else "drf", "main_kernel": path}
+            del osc
+
     cpu = None
     if world > 1:
         dist.barrier()          # the GPU timing is done on every rank before the CPU leg
@@ -510,6 +530,7 @@ def main():
                              "frac": pipe_bytes / (ms_max / 1e3) / 1e9 / peak if peak else None,
                              "note": "algorithmic bytes of every kernel of the timed steps / the steps' device time "
                                      "(the direct pipeline overlaps the table scans with the next generate)"},
+            "other_configs": others,
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -329,7 +329,12 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       // cells) once the chunk is big enough to amortise its fixed cost (>= 2^23
       // accesses): the table's atomics then mostly hit L2 (4a: 92 -> 121 G acc/s,
       // profiles/r1n_chunking.jsonl).
-      if (j > i && acc >= (1ull << 23) && L.sort_bits >= 24) break;
+      // (Not for chunks that will run on chip -- per-(phase, block) units that fit
+      // shared memory and fill the GPU, §5.13 -- which have no table at all.)
+      const uint64_t unit_cell_bytes = C.w_tid <= MAPC_CW16_MAX_WT ? 2 : 4;
+      const bool on_chip = L.w_array + L.w_index < 20 &&
+                           ((1ull << (L.w_array + L.w_index)) * unit_cell_bytes) <= MAPC_UNIT_MAX_BYTES && G >= 2 * 148;
+      if (j > i && acc >= (1ull << 23) && L.sort_bits >= 24 && !on_chip) break;
       acc += (uint64_t)nb;
       ilo = nlo; ihi = nhi; ops += ph[j].ops;
       Lok = L;
