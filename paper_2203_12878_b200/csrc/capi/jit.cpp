@@ -652,7 +652,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   };
   // the per-tile body, emitted once per baked segment (fields as literals) and
   // once generic (fields loaded from segs[])
-  auto tile_body = [&](std::ostringstream& s) {
+  // (only_prog >= 0: a baked segment -- only its own program is emitted)
+  auto tile_body = [&](std::ostringstream& s, int64_t only_prog) {
     s << "    const u32 tl0 = (u32)(tile - sg.tile_begin) * " << V * T << "u;\n";
     if (mode == MAPC_MODE_FILTER) {
       // the witness cell lies in one phase and one block: tiles of other phases
@@ -675,6 +676,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
          << emit_tail(mode, ch.lay.w_tid, T) << " }\n"
       << "    switch (sg.prog_begin) {\n";
     for (const JitProgram& pg : ch.programs) {
+      if (only_prog >= 0 && pg.prog_begin != (uint32_t)only_prog) continue;
       if (paired) {
         paired_case(s, pg);
         continue;
@@ -732,17 +734,14 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         << "u, " << g.b0 << "u, " << g.lb0 << "u, " << g.n_emits << "u, " << g.dense << "u, " << g.tid_inner << "u, {";
       for (int l = 0; l < 8; ++l) s << (l ? ", " : "") << fd(g.trip_div[l]);
       s << "}, " << fd(g.tid_div) << "};\n";
-      tile_body(s);
+      tile_body(s, g.prog_begin);
       s << "    break; }\n";
     }
-    s << "    default: {\n"
-      << "    const Seg& sg = segs[lo];\n";
-    tile_body(s);
-    s << "    break; }\n"
+    s << "    default: break;\n"        // every segment of the chunk is baked
       << "    }\n";
   } else {
     s << "    const Seg& sg = segs[lo];\n";
-    tile_body(s);
+    tile_body(s, -1);
   }
   s << "  }\n";
   s << "  if (err) atomicOr(err_flag, err);\n"

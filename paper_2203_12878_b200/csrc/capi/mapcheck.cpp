@@ -380,7 +380,9 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.lay.cap = kcap;
     ch.jit.lay = ch.lay;
     ch.jit.max_emits = ch.max_emits;
-    if (ch.segs.size() <= 4) ch.jit.segs = ch.segs;
+    // segments baked into the specialised kernels as literals (fields fold to
+    // constants; otherwise every tile loads its segment from global memory)
+    if (ch.segs.size() <= MAPC_JIT_BAKE_SEGS) ch.jit.segs = ch.segs;
     // direct-address table: 2^S cells.  Worth it when its estimated time --
     // a fixed ~25 us, the table written (clear) and read (scan) at ~6 TB/s, the
     // generate at ~1.5 ps per access -- beats the keys pipelines' (~40 us fixed,

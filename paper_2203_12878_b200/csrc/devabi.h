@@ -49,6 +49,7 @@
 #define MAPC_MODE_UNITF 4u     // unit mode's filter: re-emit the witness cell's keys from its unit's tuples only
 #define MAPC_UNIT_MAX_BYTES 32768u  // table bytes of one unit (static shared memory)
 #define MAPC_UNIT_MAX_SEGS 8u       // segments of a unit-mode chunk (baked as literals)
+#define MAPC_JIT_BAKE_SEGS 16u      // segments of a chunk baked as literals into its specialised kernels
 
 enum MapcOpcode : uint8_t {
   VM_ADD = 0, VM_SUB,   /* monus */

@@ -185,3 +185,25 @@ def test_graph_replay_two_programs_share_scratch():
         for detect in ("auto", "sort"):
             assert _got(pa.check_races(scratch=scratch, detect=detect)) == oa, (i, detect)
             assert _got(pb.check_races(scratch=scratch, detect=detect)) == ob, (i, detect)
+
+
+# ---- the multi-GPU shard plan, run rank by rank on one GPU --------------------
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("inst", [config("3b", ts=32, rw=8, grid=512), config("4b", n=1 << 14, bs=256),
+                                  config("5b", block=64, T=6, R=4, C=64), config("2b")],
+                         ids=["3b", "4b", "5b", "2b"])
+def test_rank_shards_cover_the_plan(inst, world):
+    # every rank's share (map_rank_chunks under the world-aware default chunk) run in
+    # turn: the counts add up to the oracle's and the smallest witness is the oracle's,
+    # on the unit, direct and sort paths
+    o = oracle.check_instance(inst)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    chunk = p.default_chunk(world)
+    assert sorted(c for r in range(world) for c in p.rank_chunks(r, world, chunk)) == list(range(p.n_chunks(chunk)))
+    for gen, det in [("jit", "auto"), ("jit", "direct"), ("vm", "sort")]:
+        parts = [p.check_races(rank=r, world=world, gen=gen, detect=det) for r in range(world)]
+        assert sum(x.n_accesses for x in parts) == o.n_accesses, (gen, det)
+        assert sum(x.racy_segments for x in parts) == o.n_racy_segments
+        wits = [x.witness.as_tuple() for x in parts if x.witness]
+        assert (min(wits) if wits else None) == o.witness
