@@ -523,9 +523,16 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
                     "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
                     "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
                   : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n");
-  s << "    int lo = 0, hi = n_segs - 1;\n"
-    << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n"
-    ;
+  if (!ch.segs.empty()) {
+    // baked segments: the tile's segment from the literal segment starts (no
+    // dependent loads of segs[] per tile)
+    s << "    int lo = 0";
+    for (size_t i = 1; i < ch.segs.size(); ++i) s << " + (tile >= " << ch.segs[i].tile_begin << "ull)";
+    s << "; (void)n_segs;\n";
+  } else {
+    s << "    int lo = 0, hi = n_segs - 1;\n"
+      << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1; }\n";
+  }
   // Direct mode with u32 cells: every thread takes two CONSECUTIVE tuples
   // (t, t+1) of the tile; an access site whose two cells are adjacent and
   // 8-byte aligned (sf, sf + 1; sf even -- the unit-stride innermost loops of
