@@ -162,6 +162,18 @@ __device__ __forceinline__ u32 cw7(u32 d) {
   return (u32)(w >> (7u * (d & 7u))) & 0x7Fu;
 }
 __device__ __forceinline__ u32 code16(u32 t, u32 kind) { return cw7(t & 31u) | (cw7((t >> 5) & 31u) << 7) | (kind << 14); }
+// thread-block clusters: rank, barrier (all threads of every CTA), and a
+// fire-and-forget OR into word `off` of CTA `rank`'s copy of `tab` (DSMEM)
+__device__ __forceinline__ u32 cl_rank() { u32 r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_or(u32* tab, u32 rank, u32 off, u32 v) {
+  const u32 local = (u32)__cvta_generic_to_shared(tab + off);
+  u32 remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" :: "r"(remote), "r"(v) : "memory");
+}
 // nonzero iff a 16-bit cell of the word is racy (SWAR, same test as direct.cu racy16_word)
 __device__ __forceinline__ u32 racy16w(u32 w) {
   const u32 g = 0x80808080u, one = 0x01010101u;
@@ -238,6 +250,8 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   put(k, ch.segs.size());
   k.append(reinterpret_cast<const char*>(ch.segs.data()), ch.segs.size() * sizeof(MapcSeg));
   if (mode == MAPC_MODE_UNIT || mode == MAPC_MODE_UNITF) {
+    put(k, ch.unit_cluster);
+    put(k, ch.unit_threads);
     put(k, ch.n_blocks);
     put(k, ch.unit_segs.size());
     k.append(reinterpret_cast<const char*>(ch.unit_segs.data()), ch.unit_segs.size() * sizeof(MapcSeg));
@@ -300,7 +314,6 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   // *target_ptr) from the tuples of its unit only -- the unit-mode counterpart of
   // the filter generate, which would walk every tile of the chunk.
   std::ostringstream s;
-  const int T = MAPC_GEN_THREADS;
   const MapcLayout& L = ch.lay;
   const uint32_t wu = L.w_array + L.w_index;
   const uint64_t cells = 1ull << wu;
@@ -308,6 +321,15 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   const uint64_t nb = std::max<uint64_t>(ch.n_blocks, 1);
   const uint32_t wt = L.w_tid;
   const uint32_t hb = L.w_array + L.w_block + L.w_index;
+  // cluster units (K > 1): the unit's table is spread over the shared memory of a
+  // K-CTA thread-block cluster, CTA r holding words [r*WPC, (r+1)*WPC); an access
+  // ORs into its word's owner through distributed shared memory (mapa +
+  // red.shared::cluster); cluster barriers separate clear, fold and scan
+  const uint32_t K = filter ? 1u : std::max(1u, ch.unit_cluster);
+  const int T = filter ? MAPC_GEN_THREADS : (int)ch.unit_threads;
+  const uint64_t wpc = words / K;
+  uint32_t log_wpc = 0;
+  while ((1ull << log_wpc) < wpc) ++log_wpc;
   s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index;
   if (filter)
     s << "(const unsigned long long* target_ptr, unsigned long long* keys, unsigned long long* n_ctr, "
@@ -329,13 +351,22 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "  const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
       << "u;\n"
       << "  {\n";
-  } else {
+  } else if (K == 1) {
     s << "  __shared__ u32 tab[" << words << "];\n"
+      << "  const u32 crank_ = 0u; (void)crank_;\n"
       << "  unsigned long long racy = 0, best = ~0ull;\n"
       << "  for (unsigned long long u = blockIdx.x; u < n_units; u += gridDim.x) {\n"
       << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
       << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) tab[i] = 0u;\n"
       << "    __syncthreads();\n";
+  } else {
+    s << "  extern __shared__ u32 tab[];        // this CTA's " << wpc << " words of the unit table\n"
+      << "  const u32 crank_ = cl_rank();\n"
+      << "  unsigned long long racy = 0, best = ~0ull;\n"
+      << "  for (unsigned long long u = blockIdx.x / " << K << "u; u < n_units; u += gridDim.x / " << K << "u) {\n"
+      << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
+      << "    for (u32 i = me; i < " << wpc << "u; i += " << T << "u) tab[i] = 0u;\n"
+      << "    cl_sync();\n";
   }
   s << "#define EMIT_KEY(IX, ARR, KIND) { u64 idx_ = (u64)(IX) - IDX_LO; "
        "if (WI < 64 && (idx_ >> WI) != 0) { err |= " << MAPC_ERR_LAYOUT << "u; idx_ = 0; } ";
@@ -351,10 +382,14 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   } else {
     // the unit-local cell of an access: (array, index - idx_lo)
     s << "const u32 c_ = ((u32)(ARR) << WI) | (u32)idx_; ";
-    if (cell_bytes == 2)
-      s << "atomicOr(&tab[c_ >> 1], (tcd_ | ((u32)(KIND) << 14)) << (16u * (c_ & 1u))); ";
+    const std::string w = cell_bytes == 2 ? "(c_ >> 1)" : "c_";
+    const std::string v = cell_bytes == 2 ? "(tcd_ | ((u32)(KIND) << 14)) << (16u * (c_ & 1u))"
+                                          : "tidv | ((~tidv & TMASK) << " + std::to_string(wt) + "u) | ((u32)(KIND) << " +
+                                                std::to_string(2 * wt) + "u)";
+    if (K == 1)
+      s << "atomicOr(&tab[" << w << "], " << v << "); ";
     else
-      s << "atomicOr(&tab[c_], tidv | ((~tidv & TMASK) << " << wt << "u) | ((u32)(KIND) << " << 2 * wt << "u)); ";
+      s << "cl_or(tab, " << w << " >> " << log_wpc << "u, " << w << " & " << wpc - 1 << "u, " << v << "); ";
     s << "if (!sg.dense) ++cnt; }\n";
   }
   auto fd = [](const MapcFastDiv& f) {
@@ -386,8 +421,9 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
     const uint32_t inner_reg = tid_is_inner ? MAPC_REG_TID : MAPC_REG_K0 + pg->n_levels - 1;
     const uint32_t step = quad ? 4 : 1;
     const std::string first = filter ? "(blockIdx.x * " + std::to_string(T) + "u + me) * " + std::to_string(step) + "u"
-                                     : std::to_string(step) + "u * me";
-    const std::string stride = filter ? "gridDim.x * " + std::to_string(T * step) + "u" : std::to_string(T * step) + "u";
+                                     : "(crank_ * " + std::to_string(T) + "u + me) * " + std::to_string(step) + "u";
+    const std::string stride = filter ? "gridDim.x * " + std::to_string(T * step) + "u"
+                                      : std::to_string((uint64_t)K * T * step) + "u";
     s << "#pragma unroll 1\n"
       << "      for (u32 k = " << first << "; k < " << tpb << "u; k += " << stride << ") {\n"
       << "        const u32 t = t0 + k; (void)t;\n"
@@ -422,11 +458,12 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "}\n";
     return s.str();
   }
-  s << "    __syncthreads();\n"
+  s << (K == 1 ? "    __syncthreads();\n" : "    cl_sync();\n")
     << "    const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
     << "u;\n"
-    << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) {\n"
-    << "      const u32 w = tab[i];\n"
+    << "    for (u32 il = me; il < " << wpc << "u; il += " << T << "u) {\n"
+    << "      const u32 i = crank_ * " << wpc << "u + il;      // the word's index in the unit table\n"
+    << "      const u32 w = tab[il];\n"
     << (cell_bytes == 2 ? "      if (!racy16w(w)) continue;\n" : "      if (!w) continue;\n");
   // cell c = (array, index) -> sort field base_ + (array << (wB + wI)) + index
   auto cell_sf = [&](const std::string& c) {
@@ -446,7 +483,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "        ++racy; const u64 sf = " << cell_sf("i") << "; best = sf < best ? sf : best; }\n";
   }
   s << "    }\n"
-    << "    __syncthreads();\n"
+    << (K == 1 ? "    __syncthreads();\n" : "")
     << "  }\n"
     << "#pragma unroll\n"
     << "  for (int o = 16; o; o >>= 1) {\n"
@@ -848,17 +885,44 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 }
 
 cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,
-                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag, int n_sms,
-                         cudaStream_t s) {
+                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag,
+                         uint32_t cluster, uint32_t threads, size_t smem, int n_sms, cudaStream_t s) {
   if (n_units == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MAPC_GEN_THREADS, 0);
-  if (occ < 1) occ = 1;
-  const unsigned long long capb = (unsigned long long)n_sms * occ;
-  const int grid = (int)(n_units < capb ? n_units : capb);
   void* args[] = {(void*)&n_units, (void*)&n_ctr, (void*)&racy, (void*)&racy_sf, (void*)&err_flag};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
+  if (cluster <= 1) {
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)threads, 0);
+    if (occ < 1) occ = 1;
+    const unsigned long long capb = (unsigned long long)n_sms * occ;
+    const int grid = (int)(n_units < capb ? n_units : capb);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, 0, s);
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cluster > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(cluster * n_units));
+  int max_clusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg);
+  if (e != cudaSuccess) return e;
+  if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+  const unsigned long long active = std::min<unsigned long long>(n_units, (unsigned long long)max_clusters);
+  cfg.gridDim = dim3((unsigned)(cluster * active));
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_unit_filter(const JitHandle& h, size_t chunk, const unsigned long long* target,

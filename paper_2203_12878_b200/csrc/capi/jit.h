@@ -28,6 +28,9 @@ struct JitChunk {
   // unit mode (MAPC_MODE_UNIT): every segment baked, and the chunk's unit grid
   std::vector<MapcSeg> unit_segs;
   uint64_t n_blocks = 0;          // blocks of the chunk (b_hi - b_lo)
+  uint32_t unit_cluster = 1;      // CTAs per unit: 1 = the unit's table in one CTA's shared memory,
+                                  // K > 1 = spread over a K-CTA cluster (distributed shared memory)
+  uint32_t unit_threads = 128;    // threads per CTA of the unit kernel
 };
 
 struct JitHandle {
@@ -50,9 +53,11 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
                          int n_sms, int max_ctas_per_sm, cudaStream_t s);
 // Unit mode (MAPC_MODE_UNIT): n_units (phase, block) units of the chunk, one CTA
 // each at a time; counts into n_ctr (guarded accesses), racy, racy_sf (atomicMin).
+// cluster = CTAs per unit (thread-block cluster, DSMEM table when > 1), threads per
+// CTA, smem = dynamic shared bytes per CTA (cluster > 1).
 cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,
-                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag, int n_sms,
-                         cudaStream_t s);
+                         unsigned long long* racy, unsigned long long* racy_sf, unsigned int* err_flag,
+                         uint32_t cluster, uint32_t threads, size_t smem, int n_sms, cudaStream_t s);
 // Unit filter (MAPC_MODE_UNITF): the keys of cell *target from its unit's tuples
 // (unit_accesses bounds them; sets the grid), appended to keys[cap], counted in *n_ctr.
 cudaError_t launch_unit_filter(const JitHandle& h, size_t chunk, const unsigned long long* target,

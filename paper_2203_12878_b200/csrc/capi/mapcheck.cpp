@@ -107,6 +107,7 @@ struct Chunk {
   uint32_t cell_bytes = 4;                  // 2 if w_tid <= 10 (devabi.h code16), 4 if 2 w_tid + 1 <= 32, else 8
   bool direct_ok = false;                   // the table is cheap enough and fits the scratch plan
   bool unit_ok = false;                     // per-(phase, block) tables fit shared memory (MAPC_MODE_UNIT)
+  size_t unit_smem = 0;                     // dynamic shared bytes per CTA of a cluster unit
   size_t dev_segs = 0;                      // offset of this chunk's segment table in the all-chunks region
 };
 
@@ -332,8 +333,9 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       // (Not for chunks that will run on chip -- per-(phase, block) units that fit
       // shared memory and fill the GPU, §5.13 -- which have no table at all.)
       const uint64_t unit_cell_bytes = C.w_tid <= MAPC_CW16_MAX_WT ? 2 : 4;
-      const bool on_chip = L.w_array + L.w_index < 20 &&
-                           ((1ull << (L.w_array + L.w_index)) * unit_cell_bytes) <= MAPC_UNIT_MAX_BYTES && G >= 2 * 148;
+      const uint64_t unit_bytes = L.w_array + L.w_index < 24 ? (1ull << (L.w_array + L.w_index)) * unit_cell_bytes : ~0ull;
+      const bool on_chip = (unit_bytes <= MAPC_UNIT_MAX_BYTES && G >= 2 * 148) ||
+                           unit_bytes <= (uint64_t)MAPC_CLUSTER_MAX * MAPC_CLUSTER_CTA_BYTES;
       if (j > i && acc >= (1ull << 23) && L.sort_bits >= 24 && !on_chip) break;
       acc += (uint64_t)nb;
       ilo = nlo; ihi = nhi; ops += ph[j].ops;
@@ -406,14 +408,26 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     // small), so one CTA per unit does generate + fold + scan without HBM.
     {
       static const bool unit_env = [] { const char* e = getenv("MAPC_UNIT"); return !(e && e[0] == '0'); }();
+      static const bool cluster_env = [] { const char* e = getenv("MAPC_CLUSTER"); return !(e && e[0] == '0'); }();
       const uint32_t wu = ch.lay.w_array + ch.lay.w_index;
       const uint64_t n_units = (uint64_t)(ch.phase_hi - ch.phase_lo + 1) * (ch.b_hi - ch.b_lo);
-      ch.unit_ok = unit_env && ch.cell_bytes <= 4 && wu < 20 &&
-                   ((1ull << wu) * ch.cell_bytes) <= MAPC_UNIT_MAX_BYTES && ch.segs.size() <= MAPC_UNIT_MAX_SEGS &&
-                   (n_units >= 2 * 148 || ch.bound <= (1ull << 20)) && ch.bound > 0;
+      const uint64_t ubytes = wu < 40 ? (1ull << wu) * ch.cell_bytes : ~0ull;
+      // one CTA's shared memory, or a cluster of up to 16 CTAs (<= 192 KB each)
+      uint32_t K = 1;
+      if (ubytes > MAPC_UNIT_MAX_BYTES) {
+        K = 2;
+        while (K < MAPC_CLUSTER_MAX && ubytes / K > MAPC_CLUSTER_CTA_BYTES) K *= 2;
+      }
+      const bool fits = ubytes <= MAPC_UNIT_MAX_BYTES ||
+                        (cluster_env && ubytes / K <= MAPC_CLUSTER_CTA_BYTES && ubytes % K == 0);
+      ch.unit_ok = unit_env && ch.cell_bytes <= 4 && wu < 24 && fits && ch.segs.size() <= MAPC_UNIT_MAX_SEGS &&
+                   (n_units * K >= 2 * 148 || ch.bound <= (1ull << 20)) && ch.bound > 0;
       if (ch.unit_ok) {
         ch.jit.unit_segs = ch.segs;
         ch.jit.n_blocks = ch.b_hi - ch.b_lo;
+        ch.jit.unit_cluster = K;
+        ch.jit.unit_threads = K > 1 ? MAPC_CLUSTER_THREADS : MAPC_GEN_THREADS;
+        ch.unit_smem = K > 1 ? ubytes / K : 0;
       }
     }
   }
@@ -974,7 +988,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       const uint64_t n_units = (uint64_t)(ch.phase_hi - ch.phase_lo + 1) * (ch.b_hi - ch.b_lo);
       m = begin(MAP_K_UNIT);
       CK(mapj::launch_units(P.jit[MAPC_MODE_UNIT], c, n_units, &ctrl->n, &ctrl->racy, &ctrl->racy_sf, &ctrl->err,
-                            n_sms, s));
+                            ch.jit.unit_cluster, ch.jit.unit_threads, ch.unit_smem, n_sms, s));
       end(m);
       m = begin(MAP_K_OTHER);
       launches += 2;

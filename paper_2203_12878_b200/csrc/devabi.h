@@ -48,7 +48,10 @@
 #define MAPC_MODE_UNIT 3u      // per (phase, block) unit: fold its accesses into a shared-memory table and scan it (JIT only)
 #define MAPC_MODE_UNITF 4u     // unit mode's filter: re-emit the witness cell's keys from its unit's tuples only
 #define MAPC_UNIT_MAX_BYTES 32768u  // table bytes of one unit (static shared memory)
-#define MAPC_UNIT_MAX_SEGS 8u       // segments of a unit-mode chunk (baked as literals)
+#define MAPC_UNIT_MAX_SEGS 64u      // segments of a unit-mode chunk (baked as literals)
+#define MAPC_CLUSTER_MAX 16u         // CTAs per cluster unit (non-portable cluster size)
+#define MAPC_CLUSTER_CTA_BYTES 196608u  // unit-table bytes per CTA of a cluster unit
+#define MAPC_CLUSTER_THREADS 512u    // threads per CTA of a cluster unit
 #define MAPC_JIT_BAKE_SEGS 16u      // segments of a chunk baked as literals into its specialised kernels
 
 enum MapcOpcode : uint8_t {

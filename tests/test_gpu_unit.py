@@ -65,3 +65,37 @@ def test_unit_u32_cells_and_two_arrays():
         o = _want(oracle.check(src, grid=(grid, 1, 1), block=(1024, 2, 1)))
         r = mc.check(src, grid=(grid, 1, 1), block=(1024, 2, 1), gen="jit", detect="unit", profile=True)
         assert _got(r) == o and r.kernels["unit"]["launches"] > 0
+
+
+# ---- cluster units: the unit table spread over a thread-block cluster (DSMEM) ----
+
+@pytest.mark.parametrize("name,n", [("4b", 1 << 15), ("4d", 1 << 17), ("4c", 1 << 18), ("4b", 1 << 19),
+                                    ("4d", 1 << 20)])
+def test_cluster_units(name, n):
+    # unit tables of 64 KB .. 2 MB: clusters of 2 .. 16 CTAs
+    inst = config(name, n=n, bs=1024)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    src = p.jit_source(0, 3)
+    assert "extern __shared__" in src, (name, n)             # the cluster variant is what runs
+    o = _want(oracle.check_instance(inst))
+    for gen, det in [("jit", "auto"), ("jit", "unit")]:
+        r = p.check_races(gen=gen, detect=det, profile=True)
+        assert _got(r) == o and r.kernels["unit"]["launches"] > 0, (name, n, det)
+
+
+def test_cluster_unit_fuzz_wide_index():
+    # fuzz programs with a wide, sparse index range per unit (x * 4096 + ...): cluster tables
+    bad, ran = [], 0
+    for seed in range(0, 120, 3):
+        inst, _ = fuzz.random_instance(seed)
+        src = inst.src.replace("rd[", "rd[65536 + ").replace("wr[", "wr[65536 + ")
+        src = src.replace(" A[", " A[200000 - ").replace(" B[", " B[200000 - ") if "shared" in src else src
+        o = oracle.check(src, inst.grid, inst.block, inst.params)
+        if o.status != 0:
+            continue
+        p = mc.MapProgram(src, inst.grid, inst.block, inst.params)
+        r = p.check_races(gen="jit", detect="unit", profile=True)
+        ran += r.kernels["unit"]["launches"] > 0
+        if _got(r) != _want(o):
+            bad.append((seed, src, _got(r), _want(o)))
+    assert not bad, bad[:3]
