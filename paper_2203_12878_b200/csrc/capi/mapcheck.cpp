@@ -188,6 +188,13 @@ struct PhaseInfo {
   size_t ops = 0;
 };
 
+// Cluster units are opt-in (MAPC_CLUSTER=1): measured 2.7-9x SLOWER than the
+// L2-resident direct tables on configs 4b/4c/4d.
+bool cluster_units_enabled() {
+  static const bool on = [] { const char* e = getenv("MAPC_CLUSTER"); return e && e[0] == '1'; }();
+  return on;
+}
+
 bool layout_fits(const mapc::Compiled& C, uint32_t ph_span, uint64_t nb, uint64_t ilo, uint64_t ihi, MapcLayout* out) {
   MapcLayout L{};
   L.w_phase = bits_for(ph_span);
@@ -335,7 +342,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       const uint64_t unit_cell_bytes = C.w_tid <= MAPC_CW16_MAX_WT ? 2 : 4;
       const uint64_t unit_bytes = L.w_array + L.w_index < 24 ? (1ull << (L.w_array + L.w_index)) * unit_cell_bytes : ~0ull;
       const bool on_chip = (unit_bytes <= MAPC_UNIT_MAX_BYTES && G >= 2 * 148) ||
-                           unit_bytes <= (uint64_t)MAPC_CLUSTER_MAX * MAPC_CLUSTER_CTA_BYTES;
+                           (cluster_units_enabled() && unit_bytes <= (uint64_t)MAPC_CLUSTER_MAX * MAPC_CLUSTER_CTA_BYTES);
       if (j > i && acc >= (1ull << 23) && L.sort_bits >= 24 && !on_chip) break;
       acc += (uint64_t)nb;
       ilo = nlo; ihi = nhi; ops += ph[j].ops;
@@ -408,7 +415,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     // small), so one CTA per unit does generate + fold + scan without HBM.
     {
       static const bool unit_env = [] { const char* e = getenv("MAPC_UNIT"); return !(e && e[0] == '0'); }();
-      static const bool cluster_env = [] { const char* e = getenv("MAPC_CLUSTER"); return !(e && e[0] == '0'); }();
+      const bool cluster_env = cluster_units_enabled();
       const uint32_t wu = ch.lay.w_array + ch.lay.w_index;
       const uint64_t n_units = (uint64_t)(ch.phase_hi - ch.phase_lo + 1) * (ch.b_hi - ch.b_lo);
       const uint64_t ubytes = wu < 40 ? (1ull << wu) * ch.cell_bytes : ~0ull;
@@ -421,7 +428,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
       const bool fits = ubytes <= MAPC_UNIT_MAX_BYTES ||
                         (cluster_env && ubytes / K <= MAPC_CLUSTER_CTA_BYTES && ubytes % K == 0);
       ch.unit_ok = unit_env && ch.cell_bytes <= 4 && wu < 24 && fits && ch.segs.size() <= MAPC_UNIT_MAX_SEGS &&
-                   (n_units * K >= 2 * 148 || ch.bound <= (1ull << 20)) && ch.bound > 0;
+                   (n_units * K >= 2 * 148 || ch.bound <= (1ull << 20) || K > 1) && ch.bound > 0;
       if (ch.unit_ok) {
         ch.jit.unit_segs = ch.segs;
         ch.jit.n_blocks = ch.b_hi - ch.b_lo;
