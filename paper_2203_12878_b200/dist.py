@@ -75,8 +75,9 @@ def check_races_distributed(prog: MapProgram, scratch=None, stream=None, chunk_m
     return reduce_results(local, names, group=group, device=dev)
 
 
-def _exchange_chunk(prog: MapProgram, chunk: int, scratch, stream, chunk_max_accesses: int, group, device):
-    """One chunk of the key-exchange mode: (packed witness or None, racy count, n keys)."""
+def _exchange_start(prog, chunk, scratch, stream, chunk_max_accesses, group, device):
+    """Generate chunk `chunk`'s slice bucketed by destination, swap the counts, and
+    START the key all_to_all (async_op): returns the in-flight state."""
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     bound = prog.chunk_info(chunk, chunk_max_accesses)["bound"]
@@ -84,27 +85,63 @@ def _exchange_chunk(prog: MapProgram, chunk: int, scratch, stream, chunk_max_acc
     counts = prog.generate_bucketed(chunk, rank, world, out, scratch, stream, chunk_max_accesses)
     send = torch.tensor(counts, dtype=torch.int64, device=device)
     recv = torch.empty_like(send)
-    _comm(dist.all_to_all_single, recv, send, group=group)            # counts
+    _comm(dist.all_to_all_single, recv, send, group=group)            # counts (small, blocking)
     rsizes = [int(x) for x in recv.tolist()]
     got = torch.empty(max(sum(rsizes), 1), dtype=torch.int64, device=device)
-    _comm(dist.all_to_all_single, got[:sum(rsizes)], out[:sum(counts)], output_split_sizes=rsizes,
-          input_split_sizes=counts, group=group)                       # keys, bucketed by hash
-    packed, racy = prog.sort_detect(chunk, got, sum(rsizes), scratch, stream, chunk_max_accesses)
-    return packed, racy, sum(rsizes)
+    work = _comm(dist.all_to_all_single, got[:sum(rsizes)], out[:sum(counts)], output_split_sizes=rsizes,
+                 input_split_sizes=counts, group=group, async_op=True)   # keys, bucketed by hash
+    return {"chunk": chunk, "out": out, "got": got, "n": sum(rsizes), "work": work, "scratch": scratch,
+            "stream": stream}
+
+
+def _exchange_finish(prog, st, chunk_max_accesses):
+    """Wait for a chunk's keys and sort + detect them: (packed witness or None, racy, n)."""
+    if st["stream"] is not None:                     # the sort's stream waits for the transfer
+        with torch.cuda.stream(st["stream"]):
+            _comm(st["work"].wait)
+    else:
+        _comm(st["work"].wait)
+    packed, racy = prog.sort_detect(st["chunk"], st["got"], st["n"], st["scratch"], st["stream"], chunk_max_accesses)
+    return packed, racy, st["n"]
 
 
 def check_races_exchange(prog: MapProgram, scratch, stream=None, chunk_max_accesses: int = 0,
-                         group=None) -> Result:
-    """Key-exchange mode over all chunks; every rank returns the global result."""
+                         group=None, scratch2=None) -> Result:
+    """Key-exchange mode over all chunks; every rank returns the global result.
+
+    Software-pipelined two deep (the exchange "must overlap with
+    K3 of the previous phase"): chunk c's keys travel (an async all_to_all)
+    while chunk c-1's received keys are sorted and race-checked, each chunk on
+    its own scratch buffer and CUDA stream (scratch2: a second buffer of the same
+    size; allocated here when None on a GPU)."""
     device = scratch.device
+    cuda = device.type == "cuda"
+    if cuda and scratch2 is None:
+        scratch2 = torch.empty_like(scratch)
+    scratches = [scratch, scratch2 if scratch2 is not None else scratch]
+    streams = [stream, torch.cuda.Stream(device=device)] if cuda else [None, None]
     best, n_total, racy_total = None, 0, 0
-    for c in range(prog.n_chunks(chunk_max_accesses)):
-        packed, racy, n = _exchange_chunk(prog, c, scratch, stream, chunk_max_accesses, group, device)
+
+    def fold(c, res):
+        nonlocal best, n_total, racy_total
+        packed, racy, n = res
         racy_total += racy
         n_total += n
         if packed is not None:
             w = prog.unpack_witness(c, packed).as_tuple()
             best = w if best is None or w < best else best
+
+    pending = None
+    for c in range(prog.n_chunks(chunk_max_accesses)):
+        slot = c % 2 if scratch2 is not None else 0
+        st = _exchange_start(prog, c, scratches[slot], streams[slot], chunk_max_accesses, group, device)
+        if pending is not None:                       # the previous chunk, under this chunk's transfer
+            fold(pending["chunk"], _exchange_finish(prog, pending, chunk_max_accesses))
+        pending = st
+    if pending is not None:
+        fold(pending["chunk"], _exchange_finish(prog, pending, chunk_max_accesses))
+    if cuda:
+        torch.cuda.current_stream(device).wait_stream(streams[1])
     local = Result(verdict=1 if best else 0, n_accesses=n_total, racy_segments=racy_total,
                    n_chunks=prog.n_chunks(chunk_max_accesses), device_ms=0.0, gpu_launches=0)
     if best:

@@ -458,3 +458,35 @@ def test_fuzz_unit_stride_sites():
             if _got(r) != _want(o):
                 bad.append((seed, chunk, inst.src, _got(r), _want(o)))
     assert picked >= 20 and not bad, (picked, bad[:3])
+
+
+# ---- the key-exchange mode through real torch.distributed (NCCL, world 1) ------
+
+@pytest.mark.parametrize("name", ["3b", "4b", "5b", "2b"])
+def test_exchange_mode_real_nccl_world1(name):
+    # dist.check_races_exchange end to end on one GPU with a real NCCL process group of
+    # one rank: the pipelined path (async all_to_all under the previous chunk's sort,
+    # two scratch buffers and streams) gives the oracle's result, also with unit chunks
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2203_12878_b200.dist import check_races_exchange
+    sizes = dict(CASES)[name] if name in dict(CASES) else {}
+    inst = config(name, **sizes)
+    o = oracle.check_instance(inst)
+    if not dist.is_initialized():
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(sk.getsockname()[1])
+        sk.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    unit = max(1, p.info.max_unit_accesses)
+    for chunk in (0, unit):
+        if chunk and p.n_chunks(chunk) > 64:
+            continue
+        scratch = torch.empty(p.scratch_bytes(chunk), dtype=torch.uint8, device="cuda")
+        r = check_races_exchange(p, scratch, chunk_max_accesses=chunk)
+        assert (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments) == \
+               (o.verdict, o.witness, o.n_accesses, o.n_racy_segments), (name, chunk)
