@@ -8,11 +8,13 @@ import oracle
 import paper_2203_12878_b200 as mc
 from workloads import fuzz
 
-a, b = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (0, 1000)
-combos = [("auto", "auto"), ("direct", "vm"), ("direct", "jit"), ("table", "vm"), ("sort", "vm")]
+args = [x for x in sys.argv[1:] if not x.startswith("--")]
+a, b = (int(args[0]), int(args[1])) if len(args) > 1 else (0, 1000)
+combos = [("auto", "auto"), ("direct", "vm"), ("direct", "jit"), ("unit", "jit"), ("table", "vm"), ("sort", "vm")]
+big = "--big" in sys.argv          # blockDim 1025..2048 (u32 cells)
 bad, n, t0 = 0, 0, time.time()
 for seed in range(a, b):
-    inst, _ = fuzz.random_instance(seed)
+    inst, _ = fuzz.random_instance(seed, big_block=big)
     o = oracle.check_instance(inst, threads=1)
     if o.status != 0:
         continue
