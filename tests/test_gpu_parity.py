@@ -490,3 +490,9 @@ def test_exchange_mode_real_nccl_world1(name):
         r = check_races_exchange(p, scratch, chunk_max_accesses=chunk)
         assert (r.verdict, r.witness.as_tuple() if r.witness else None, r.n_accesses, r.racy_segments) == \
                (o.verdict, o.witness, o.n_accesses, o.n_racy_segments), (name, chunk)
+
+
+def teardown_module(module):
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
