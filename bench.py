@@ -495,6 +495,23 @@ def main():
                             "verdict": "racy" if orr.verdict else "drf", "main_kernel": path}
             del osc
 
+    # NEXT-2 context: a data-carrying BabyCUDA transpose at config-3 scale (2^16 blocks
+    # x 256 threads) executed on the GPU (Fig. 5 semantics) and its executed access set
+    # checked against the inferred MAP's (Theorem 1)
+    next2 = None
+    if not args.no_other_configs and world == 1 and args.mode == "shard":
+        from workloads import babycuda as wb
+        ki = wb.kernel("transpose", ts=32, rw=8, grid=65536)
+        kern = mc.Kernel(ki.src, ki.grid, ki.block, ki.params)
+        kern.execute()
+        ex_ms = min(kern.execute().device_ms for _ in range(3))
+        kr = kern.execute()
+        diff = kern.theorem1_diff(mc.MapProgram(mc.infer(ki.src).map_text, ki.grid, ki.block, ki.params))
+        next2 = {"kernel": "BabyCUDA tiled transpose 32x32, 2^16 blocks x 256 threads (workloads/babycuda.py)",
+                 "executed_accesses": kr.n_events, "exec_ms": ex_ms, "G_events_s": kr.n_events / ex_ms / 1e6,
+                 "typable": kr.typable, "theorem1_equal": diff.equal, "access_values": diff.n_alpha,
+                 "verdict": "racy" if kr.verdict else "drf"}
+
     cpu = None
     if world > 1:
         dist.barrier()          # the GPU timing is done on every rank before the CPU leg
@@ -531,6 +548,7 @@ def main():
                              "note": "algorithmic bytes of every kernel of the timed steps / the steps' device time "
                                      "(the direct pipeline overlaps the table scans with the next generate)"},
             "other_configs": others,
+            "babycuda_executor": next2,
             "gpu_launches": launches,
             "e2e": e2e,
             "cpu_baseline": cpu,
