@@ -556,12 +556,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
-  // (experiment, MAPC_GEN_EVICT_LAST=1: the quad reductions carry an L2 evict-last
-  // policy, so the table rows a CTA re-touches outlive the concurrent scan's stream)
-  static const bool red_hint_env = [] { const char* e = getenv("MAPC_GEN_EVICT_LAST"); return e && e[0] == '1'; }();
-  const bool red_hint = red_hint_env && paired && cell_bytes == 2;
-  if (red_hint)
-    s << "  unsigned long long rpol_; asm volatile(\"createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\" : \"=l\"(rpol_));\n";
+  // (L2 eviction-priority hints -- evict-last on these reductions, evict-first on the
+  // concurrent scan and clear -- were measured without effect: profiles/r2r_l2_hints_ab.jsonl)
   s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
                     "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
                     "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
@@ -685,11 +681,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k) {\n"
         << "          if (!okP[k]) continue;\n"
-        << (red_hint ? "          if ((sfP[k] & 3u) == 0) { asm volatile(\"red.relaxed.gpu.global.or.L2::cache_hint.b64 "
-                       "[%0], %1, %2;\" :: \"l\"(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2)), \"l\"(accP[k]), "
-                       "\"l\"(rpol_) : \"memory\"); continue; }\n"
-                     : "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), "
-                       "accP[k]); continue; }\n")
+        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
+           "continue; }\n"
         << "#pragma unroll\n"
         << "          for (int j = 0; j < 4; ++j) {\n"
         << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"

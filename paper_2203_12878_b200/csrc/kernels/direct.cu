@@ -64,14 +64,10 @@ __host__ __device__ __forceinline__ uint32_t racy16_word(uint32_t w) {
 // thread; each thread's first racy cell is its smallest (indices increase
 // along the stride).  The common all-clean vector costs a few ALU ops per cell.
 constexpr int DS_UNROLL = 8;
-// EF: the table is streamed with an L2 evict-first policy, so the scan's 1 GB does
-// not push the concurrent generate's hot rows out of L2 (MAPC_SCAN_EVICT_FIRST).
-template <typename C, bool EF>
+template <typename C>
 __global__ void __launch_bounds__(DS_THREADS)
 k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
   constexpr int PER = 16 / sizeof(C);
-  unsigned long long pol = 0;
-  if constexpr (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const unsigned long long nvec = cells / PER;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   unsigned long long best = ~0ull, racy = 0;
@@ -82,16 +78,11 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
 #pragma unroll
     for (int u = 0; u < DS_UNROLL; ++u) {
       const unsigned long long i = i0 + u * stride;
-      if (i < nvec) {
-        if constexpr (EF)
-          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                       : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
-                       : "l"(v4 + i), "l"(pol));
-        else
-          asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
-                       : "l"(v4 + i));
-      } else
+      if (i < nvec)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(v4 + i));
+      else
         v[u] = make_uint4(0, 0, 0, 0);
     }
 
@@ -184,23 +175,10 @@ __global__ void k_witness_gate(MapcCtrl* __restrict__ ctrl, uint32_t* __restrict
 }
 
 // Table reset: 16-byte stores over the cells (the table region is 256-B aligned).
-template <bool EF>
 __global__ void k_table_clear(uint4* __restrict__ tab, unsigned long long n16) {
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  unsigned long long pol = 0;
-  if constexpr (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
-    if constexpr (EF)
-      asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %1, %1, %1}, %2;" :: "l"(tab + i), "r"(0u), "l"(pol)
-                   : "memory");
-    else
-      tab[i] = make_uint4(0, 0, 0, 0);
-  }
-}
-
-bool scan_evict_first() {
-  static const bool on = [] { const char* e = getenv("MAPC_SCAN_EVICT_FIRST"); return e && e[0] == '1'; }();
-  return on;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    tab[i] = make_uint4(0, 0, 0, 0);
 }
 
 }  // namespace mapk
@@ -213,10 +191,7 @@ extern "C" cudaError_t mapc_launch_table_clear(void* tab, unsigned long long byt
   if (n16 == 0) return cudaSuccess;
   const unsigned long long want = (n16 + 255) / 256;
   const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 8);
-  if (mapk::scan_evict_first())
-    mapk::k_table_clear<true><<<(int)(want < cap ? want : cap), 256, 0, s>>>((uint4*)tab, n16);
-  else
-    mapk::k_table_clear<false><<<(int)(want < cap ? want : cap), 256, 0, s>>>((uint4*)tab, n16);
+  mapk::k_table_clear<<<(int)(want < cap ? want : cap), 256, 0, s>>>((uint4*)tab, n16);
   return cudaGetLastError();
 }
 
@@ -234,17 +209,13 @@ extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long lo
   const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
   const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 16);
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  const bool ef = mapk::scan_evict_first();
-  if (cell_bytes == 2) {
-    if (ef) mapk::k_direct_scan<uint16_t, true><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
-    else mapk::k_direct_scan<uint16_t, false><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
-  } else if (cell_bytes == 4) {
-    if (ef) mapk::k_direct_scan<uint32_t, true><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
-    else mapk::k_direct_scan<uint32_t, false><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
-  } else {
-    mapk::k_direct_scan<unsigned long long, false>
+  if (cell_bytes == 2)
+    mapk::k_direct_scan<uint16_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
+  else if (cell_bytes == 4)
+    mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
+  else
+    mapk::k_direct_scan<unsigned long long>
         <<<grid, mapk::DS_THREADS, 0, s>>>((const unsigned long long*)tab, cells, w_tid, ctrl);
-  }
   return cudaGetLastError();
 }
 
