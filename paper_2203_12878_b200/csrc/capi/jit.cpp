@@ -13,7 +13,6 @@
 #include <nvrtc.h>
 
 #include <algorithm>
-#include <cstddef>
 #include <cstdlib>
 #include <atomic>
 #include <cstdint>
@@ -183,11 +182,6 @@ __device__ __forceinline__ u32 racy16w(u32 w) {
   x = (x & (x - one)) | g;
   x = (x & (x - one));
   return x & (((w >> 14) & 0x00010001u) * 0x7F7Fu);
-}
-// racy bits of the two 16-bit cells of a word: bit 0 = low cell, bit 1 = high cell
-__device__ __forceinline__ u32 racy16_pair(u32 w) {
-  const u32 r = racy16w(w);
-  return (u32)((r & 0xFFFFu) != 0u) | ((u32)((r >> 16) != 0u) << 1);
 }
 // Block offset (within the segment) of tuple t: t / (blockDim * prod(trips)).
 __device__ __forceinline__ u32 block_of(u32 t, const Seg& sg) {
@@ -564,24 +558,6 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       << "  if (target == ~0ull) return;\n";
   // (L2 eviction-priority hints -- evict-last on these reductions, evict-first on the
   // concurrent scan and clear -- were measured without effect: profiles/r2r_l2_hints_ab.jsonl)
-  // Scan-free direct mode (direct_atom): every reduction returns the cell's old value
-  // (atom.or instead of red.or); the racy predicate is monotone under OR, so exactly
-  // one update per racy cell turns it racy -- counting those transitions and taking the
-  // smallest such cell gives the table scan's racy count and smallest racy cell.
-  const bool atom16 = mode == MAPC_MODE_DIRECT && paired && direct_atom(cell_bytes, ch.lay);
-  if (atom16)
-    s << "  unsigned long long racyA_ = 0, bestA_ = ~0ull;\n"
-      << "#define ATOM_NOTE_(T, SF0) { if (T) { racyA_ += __popc(T); const u64 s_ = (u64)(SF0) + (u64)(__ffs(T) - 1); "
-         "bestA_ = s_ < bestA_ ? s_ : bestA_; } }\n"
-      << "#define ATOM_Q(Q, V, SF0) { const u64 v_ = (V); "
-         "const u64 o_ = atomicOr(reinterpret_cast<u64*>(keys) + (Q), v_); const u64 n_ = o_ | v_; "
-         "if ((n_ & 0x4000400040004000ull) && n_ != o_) { "
-         "const u32 t_ = (racy16_pair((u32)n_) & ~racy16_pair((u32)o_)) | "
-         "((racy16_pair((u32)(n_ >> 32)) & ~racy16_pair((u32)(o_ >> 32))) << 2); ATOM_NOTE_(t_, SF0) } }\n"
-      << "#define ATOM_1(SF, CD) { const u32 v_ = (u32)(CD) << (16u * (u32)((SF) & 1u)); "
-         "const u32 o_ = atomicOr(reinterpret_cast<u32*>(keys) + ((SF) >> 1), v_); const u32 n_ = o_ | v_; "
-         "if ((n_ & 0x40004000u) && n_ != o_) { const u32 t_ = (racy16_pair(n_) & ~racy16_pair(o_)) != 0u ? 1u : 0u; "
-         "ATOM_NOTE_(t_, SF) } }\n";
   s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
                     "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
                     "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
@@ -619,7 +595,6 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         "if (!sg.dense) ++cnt; ";
     // one cell's reduction: u32 cells are words; 16-bit cells are halves of a word
     auto red1 = [&](const std::string& sf, const std::string& cd) {
-      if (atom16) return "ATOM_1(" + sf + ", " + cd + ");";
       return cell_bytes == 2 ? "atomicOr(reinterpret_cast<u32*>(keys) + (" + sf + " >> 1), " + cd + " << (16u * (u32)(" +
                                    sf + " & 1u)));"
                              : "atomicOr(reinterpret_cast<u32*>(keys) + " + sf + ", " + cd + ");";
@@ -706,9 +681,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k) {\n"
         << "          if (!okP[k]) continue;\n"
-        << (atom16 ? "          if ((sfP[k] & 3u) == 0) { ATOM_Q(sfP[k] >> 2, accP[k], sfP[k]); continue; }\n"
-                   : "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), "
-                     "accP[k]); continue; }\n")
+        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
+           "continue; }\n"
         << "#pragma unroll\n"
         << "          for (int j = 0; j < 4; ++j) {\n"
         << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"
@@ -816,25 +790,9 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     tile_body(s, -1);
   }
   s << "  }\n";
-  if (atom16)     // the chunk's racy cells and smallest racy cell (ctrl->racy, ctrl->racy_sf)
-    s << "#undef ATOM_Q\n#undef ATOM_1\n#undef ATOM_NOTE_\n"
-      << "#pragma unroll\n"
-      << "  for (int o_ = 16; o_; o_ >>= 1) {\n"
-      << "    racyA_ += __shfl_xor_sync(0xffffffffu, racyA_, o_);\n"
-      << "    const unsigned long long b_ = __shfl_xor_sync(0xffffffffu, bestA_, o_); bestA_ = b_ < bestA_ ? b_ : bestA_;\n"
-      << "  }\n"
-      << "  if ((threadIdx.x & 31) == 0) {\n"
-      << "    if (racyA_) atomicAdd(n_ctr + " << offsetof(MapcCtrl, racy) / 8 << ", racyA_);\n"
-      << "    if (bestA_ != ~0ull) atomicMin(n_ctr + " << offsetof(MapcCtrl, racy_sf) / 8 << ", bestA_);\n"
-      << "  }\n";
   s << "  if (err) atomicOr(err_flag, err);\n"
     << "}\n";
   return s.str();
-}
-
-bool direct_atom(uint32_t cell_bytes, const MapcLayout& lay) {
-  static const bool on = [] { const char* e = getenv("MAPC_DIRECT_ATOM"); return e && e[0] == '1'; }();
-  return on && cell_bytes == 2 && lay.sort_bits <= 31;
 }
 
 std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, uint32_t cell_bytes) {

@@ -37,12 +37,6 @@ struct JitHandle {
   std::vector<cudaKernel_t> kernels;   // one per chunk
 };
 
-// Scan-free direct mode (MAPC_DIRECT_ATOM=1; 16-bit cells, 32-bit sort fields): the
-// direct generate counts racy cells itself (atom.or returning the old cell, one
-// racy transition per racy cell) into ctrl->racy / ctrl->racy_sf, so the chunk's
-// table scan is skipped.
-bool direct_atom(uint32_t cell_bytes, const MapcLayout& lay);
-
 // mode: MAPC_MODE_KEYS (keys -> key buffer), MAPC_MODE_DIRECT (red.or into the
 // direct-address table passed as `keys`, cells of cell_bytes), MAPC_MODE_FILTER
 // (only keys with sort field *target, compacted; n_ctr counts them).

@@ -949,11 +949,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       // zeroes the cells it read was measured 2.5x slower: profiles/r1k_*)
       // the last chunk's scan has no generate to share the GPU with: full grid
       const bool last = i + 1 == mine.size();
-      if (!mapj::direct_atom(ch.cell_bytes, ch.lay)) {      // (scan-free mode: the generate counted)
-        m = begin_on(MAP_K_DETECT, s2);
-        CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
-        end_on(m, s2);
-      }
+      m = begin_on(MAP_K_DETECT, s2);
+      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
+      end_on(m, s2);
       if (i + 2 < mine.size()) {
         // cleared for its next user, chunk i+2, whose table may be larger
         const Chunk& nx = P.chunks[mine[i + 2]];
@@ -1031,11 +1029,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
                                   n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
         end(m);
       }
-      if (gen_mode != 1 || !mapj::direct_atom(ch.cell_bytes, ch.lay)) {   // (scan-free mode: the generate counted)
-        m = begin(MAP_K_DETECT);
-        CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s));
-        end(m);
-      }
+      m = begin(MAP_K_DETECT);
+      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s));
+      end(m);
       m = begin(MAP_K_OTHER);
       launches += 2;
       st_acc.launches[MAP_K_OTHER] += 2;
@@ -1202,8 +1198,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       const uint64_t tbytes = P.chunks[c].cells * P.chunks[c].cell_bytes;
       st_acc.bytes[MAP_K_DIRECT] += 2 * tbytes;
       st_acc.bytes[MAP_K_CLEAR] += tbytes;
-      if (gen_mode != 1 || !mapj::direct_atom(P.chunks[c].cell_bytes, P.chunks[c].lay))
-        st_acc.bytes[MAP_K_DETECT] += tbytes;
+      st_acc.bytes[MAP_K_DETECT] += tbytes;
     } else {
     st_acc.bytes[MAP_K_GENERATE] += 8 * cr.n;
     // the histogram reads that ran: k_hist_ranges, and k_range_hist per later pass
