@@ -19,6 +19,7 @@
 #include <thread>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -627,6 +628,27 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     if (G == 4 && nocarry && sf32)   // the coordinate that advances by h: tid or the innermost loop's
       us = unit_stride_sites(pg.ops, tid_is_inner ? MAPC_REG_TID : MAPC_REG_K0 + pg.n_levels - 1);
     us.resize(NE, false);
+    // site pairs whose index is the same value (same register, not rewritten between
+    // them, or the same literal) in the same array: their quads are merged in registers
+    // before the flush, one red.or.b64 instead of two (4b/5b/2b: a read and a write of
+    // the same cell by the same thread)
+    std::vector<std::pair<int, int>> same_cell;
+    if (G == 4) {
+      std::vector<std::tuple<int, uint64_t, uint32_t, uint32_t>> site;   // (is_imm, reg/imm, version, array)
+      std::vector<uint32_t> ver(MAPC_NREG, 0);
+      for (const MapcOp& op : pg.ops) {
+        const uint32_t c = op.code & MAPC_CODE_MASK;
+        if (c == VM_EMIT) {
+          const bool imm = op.code & MAPC_A_IMM;
+          site.emplace_back(imm ? 1 : 0, imm ? op.imm : op.a, imm ? 0u : ver[op.a % MAPC_NREG], op.aux >> 1);
+        } else if (c != VM_ACT) {
+          ++ver[op.dst % MAPC_NREG];
+        }
+      }
+      for (size_t a = 0; a < site.size(); ++a)
+        for (size_t b = a + 1; b < site.size(); ++b)
+          if (site[a] == site[b]) same_cell.emplace_back((int)a, (int)b);
+    }
     s << "        constexpr bool US_[" << NE << "] = {";
     for (int k = 0; k < NE; ++k) s << (k ? ", " : "") << (us[k] ? "true" : "false");
     s << "}; (void)US_;\n";
@@ -677,6 +699,10 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
         << "          (void)act;\n"
         << "        }\n";
     }
+    for (const auto& pr : same_cell)
+      s << "        if (okP[" << pr.first << "] && okP[" << pr.second << "] && sfP[" << pr.first << "] == sfP["
+        << pr.second << "]) { accP[" << pr.first << "] |= accP[" << pr.second << "]; okP[" << pr.second
+        << "] = false; }\n";
     if (G == 4)          // one red.or.b64 over an aligned quad, else the run's cells one by one
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k) {\n"
