@@ -46,6 +46,7 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
   __shared__ unsigned long long s_base;
   const int me = threadIdx.x;
   uint32_t err = 0;
+  unsigned long long cnt_all = 0;                 // direct mode: guarded accesses, added once at the end
   // filter mode: only the keys of the witness cell (none if the chunk is DRF)
   const unsigned long long target = mode == MAPC_MODE_FILTER ? ctrl->wit_sf : ~0ull;
   if (mode == MAPC_MODE_FILTER && target == ~0ull) return;
@@ -211,10 +212,7 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
 #undef VLOOP
     }
     if (mode == MAPC_MODE_DIRECT) {                   // only the count: the accesses are in the table
-      if (!dense) {
-        const uint32_t wsum = __reduce_add_sync(0xffffffffu, cnt);
-        if ((me & 31) == 0 && wsum) atomicAdd(&ctrl->n, (unsigned long long)wsum);
-      }
+      if (!dense) cnt_all += cnt;
     } else if (!dense) {                              // uniform across the CTA
       uint32_t total;
       const uint32_t excl = block_excl_scan<T>(cnt, scan_tmp, &total);
@@ -230,6 +228,12 @@ k_generate2(const MapcSeg* __restrict__ segs, int n_segs, unsigned long long til
     }
   }
 #undef RG
+  if (mode == MAPC_MODE_DIRECT) {
+    // (one atomicAdd per warp and launch: per tile, they serialised in the counter's L2 slice)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt_all += __shfl_xor_sync(0xffffffffu, cnt_all, o);
+    if ((me & 31) == 0 && cnt_all) atomicAdd(&ctrl->n, cnt_all);
+  }
   if (err) atomicOr(&ctrl->err, err);
 }
 
