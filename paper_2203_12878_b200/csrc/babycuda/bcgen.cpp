@@ -253,7 +253,8 @@ std::string kernel_source(const bcf::Kernel& K, const Plan& P) {
     << 2 * P.k_log << "ull;\n"
     << "  S.s_nclaim = &s_nclaim; S.s_conf = &s_conf; S.s_nkeys = &s_nkeys;\n"
     << "  S.cap = block_cap; S.ctl = ctl;\n"
-    << "  S.nlog = 0; S.err = 0; S.tid = threadIdx.x; S.phase = 0; S.uninit = 0; S.ambig = 0;\n";
+    << "  S.nlog = 0; S.err = 0; S.tid = threadIdx.x; S.phase = 0; S.uninit = 0; S.ambig = 0;\n"
+    << "  u64 keys_all = 0, keys_max = 0;      // this CTA's blocks (one atomic each at the end)\n";
   for (size_t i = 0; i < K.params.size(); ++i)
     o << "  const u64 P_" << K.params[i] << " = " << P.params[i] << "ull; (void)P_" << K.params[i] << ";\n";
   // each block's accesses go to its own region of the alpha buffer (block_cap
@@ -270,14 +271,15 @@ std::string kernel_source(const bcf::Kernel& K, const Plan& P) {
   o << "    }\n"
     << "    bc_sync(S);                       // commit the last phase\n"
     << "    if (threadIdx.x == 0) {\n"
-    << "      atomicAdd(&ctl->n_keys, (u64)s_nkeys);\n"
-    << "      atomicMax(&ctl->max_block, (u64)s_nkeys);\n"
+    << "      keys_all += s_nkeys;\n"
+    << "      keys_max = s_nkeys > keys_max ? (u64)s_nkeys : keys_max;\n"
     << "    }\n"
     << "    if (mem_out)\n"
     << "      for (u64 c = threadIdx.x; c < " << n << "ull; c += blockDim.x) {\n"
     << "        mem_out[blk * " << n << "ull + c] = S.mem[c]; st_out[blk * " << n << "ull + c] = S.st[c]; }\n"
     << "    __syncthreads();\n"
     << "  }\n"
+    << "  if (threadIdx.x == 0 && keys_all) { atomicAdd(&ctl->n_keys, keys_all); atomicMax(&ctl->max_block, keys_max); }\n"
     << "  if (S.uninit) atomicAdd(&ctl->uninit, S.uninit);\n"
     << "  if (S.ambig) atomicAdd(&ctl->ambiguous, S.ambig);\n"
     << "  if (S.err) atomicOr(&ctl->err, S.err);\n"
