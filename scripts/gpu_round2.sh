@@ -1,6 +1,6 @@
 set -x
-python -m pytest tests -m gpu -q > gpurun_out/r2i_gpu_tests.log 2>&1; echo tests_rc=$?; tail -3 gpurun_out/r2i_gpu_tests.log
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2i_smoke.log 2>&1; echo smoke_rc=$?; tail -2 gpurun_out/r2i_smoke.log
-python bench.py > gpurun_out/r2i_bench.json 2> gpurun_out/r2i_bench.err; echo bench_rc=$?; cut -c1-400 gpurun_out/r2i_bench.json
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2i_bench_ref.json 2>&1; echo ref_rc=$?; cut -c1-300 gpurun_out/r2i_bench_ref.json
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2i_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-alt-path --no-other-configs > gpurun_out/r2i_ncu_ll.log 2>&1; echo ll_rc=$?
+python -m pytest tests -m gpu -q > gpurun_out/${TAG:-r2}_gpu_tests.log 2>&1; echo tests_rc=$?; tail -3 gpurun_out/${TAG:-r2}_gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG:-r2}_smoke.log 2>&1; echo smoke_rc=$?; tail -2 gpurun_out/${TAG:-r2}_smoke.log
+python bench.py > gpurun_out/${TAG:-r2}_bench.json 2> gpurun_out/${TAG:-r2}_bench.err; echo bench_rc=$?; cut -c1-400 gpurun_out/${TAG:-r2}_bench.json
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG:-r2}_bench_ref.json 2>&1; echo ref_rc=$?; cut -c1-300 gpurun_out/${TAG:-r2}_bench_ref.json
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG:-r2}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-alt-path --no-other-configs > gpurun_out/${TAG:-r2}_ncu_ll.log 2>&1; echo ll_rc=$?
