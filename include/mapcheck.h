@@ -122,7 +122,9 @@ typedef struct {
 
 /* Generate path (map_exec.flags): the bytecode VM, or kernels specialised from
  * the same bytecode with NVRTC at first use (cached per process).  AUTO picks
- * the specialised kernels for plans of >= 2^23 accesses in <= 64 chunks. */
+ * the specialised kernels for plans of >= 2^23 accesses whose chunks need <= 64
+ * distinct kernels (chunks differing only in data the kernel does not bake,
+ * e.g. the phases of a time loop, share one). */
 #define MAP_GEN_AUTO 0u
 #define MAP_GEN_VM 1u
 #define MAP_GEN_JIT 2u

@@ -19,6 +19,7 @@
 #include <thread>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 #include <mutex>
 #include <sstream>
@@ -866,11 +867,12 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
   std::vector<std::string> keys(nc), srcs(nc);
   for (size_t i = 0; i < nc; ++i)
     if (want[i]) keys[i] = chunk_key(chunks[i], u32, mode, cell_bytes[i]);
-  std::vector<int> need;
+  std::vector<int> need;                       // one chunk per distinct uncached kernel
   {
     std::lock_guard<std::mutex> g(g_mu);
+    std::set<std::string> seen;
     for (size_t i = 0; i < nc; ++i)
-      if (want[i] && !g_cache.count(keys[i])) need.push_back((int)i);
+      if (want[i] && !g_cache.count(keys[i]) && seen.insert(keys[i]).second) need.push_back((int)i);
   }
   for (int i : need) srcs[i] = prelude() + chunk_kernel_source(chunks[i], 0, u32, mode, cell_bytes[i]);
   std::vector<std::vector<char>> cubins(nc);
@@ -891,14 +893,15 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
   }
   std::lock_guard<std::mutex> g(g_mu);
   if (out->kernels.size() != nc) out->kernels.assign(nc, nullptr);
+  for (int i : need)                           // load the new kernels first
+    if (rc[i] != 0) {
+      *log = logs[i];
+      return 1;
+    }
   for (size_t i = 0; i < nc; ++i) {
     if (!want[i]) continue;
     auto it = g_cache.find(keys[i]);
     if (it == g_cache.end()) {
-      if (rc[i] != 0) {
-        *log = logs[i];
-        return 1;
-      }
       Module m;
       cudaError_t e = cudaLibraryLoadData(&m.lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
       if (e != cudaSuccess) {
@@ -917,6 +920,12 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
     out->kernels[i] = it->second.kernels[0];
   }
   return 0;
+}
+
+size_t distinct_kernels(const std::vector<JitChunk>& chunks, bool u32) {
+  std::set<std::string> k;
+  for (const JitChunk& ch : chunks) k.insert(chunk_key(ch, u32, MAPC_MODE_DIRECT, 0));
+  return k.size();
 }
 
 cudaError_t launch_units(const JitHandle& h, size_t chunk, unsigned long long n_units, unsigned long long* n_ctr,

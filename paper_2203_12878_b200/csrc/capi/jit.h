@@ -45,6 +45,9 @@ std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_
 int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log);
 // Compile (or fetch from the process-wide cache) the kernels of the chunks with
 // want[i] != 0 for one mode; out->kernels has one entry per chunk (null = not built).
+// Number of distinct specialised kernels the chunks need (chunks that differ only
+// in data the kernel does not bake share one; build_module compiles each once).
+size_t distinct_kernels(const std::vector<JitChunk>& chunks, bool u32);
 int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, const std::vector<uint32_t>& cell_bytes,
                  const std::vector<char>& want, JitHandle* out, std::string* log);
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,

@@ -115,6 +115,7 @@ struct Plan {
   uint64_t cap = 0;                         // max keys of any chunk
   std::vector<Chunk> chunks;
   mapj::JitHandle jit[5];                    // per generate mode (MAPC_MODE_*); null = not built yet
+  size_t jit_distinct = 0;                  // distinct specialised kernels of the chunks (0 = not counted)
   size_t off_dtab = 0, dtab_bytes = 0;      // direct-address table (overlays key buffer B when it fits)
   size_t off_gate = 0;                      // witness gate word (direct.cu k_witness_gate)
   size_t off_ctrl2 = 0;                     // second control block (overlapped direct pipeline)
@@ -771,12 +772,19 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // amortised), the bytecode VM otherwise (map_exec.flags, MAP_GEN_*).
   const uint32_t gsel = ex->flags & 3u;
   // (AUTO: the NVRTC compile, once per process, is amortised over plans of
-  // >= 2^23 accesses in at most 64 chunks -- 4a/4b/4d run 1.3-1.4x faster than
-  // on the VM, profiles/r1q_gen_vm_jit.jsonl; a plan cut into thousands of
-  // small chunks would compile thousands of kernels)
+  // >= 2^23 accesses needing at most 64 distinct kernels -- 4a/4b/4d run
+  // 1.3-1.4x faster than on the VM, profiles/r1q_gen_vm_jit.jsonl; chunks that
+  // differ only in unbaked data share a kernel (5a at T = 128: 128 chunks, 2
+  // kernels); a plan needing thousands of distinct kernels stays on the VM)
+  if (gsel == MAP_GEN_AUTO && P.jit_distinct == 0 && p->C.max_accesses >= (1ull << 23)) {
+    std::vector<mapj::JitChunk> jc;
+    jc.reserve(P.chunks.size());
+    for (auto& ch : P.chunks) jc.push_back(ch.jit);
+    P.jit_distinct = mapj::distinct_kernels(jc, p->C.u32_mode);
+  }
   const int gen_mode = gsel == MAP_GEN_VM    ? 0
                        : gsel == MAP_GEN_JIT ? 1
-                                             : (p->C.max_accesses >= (1ull << 23) && P.chunks.size() <= 64 ? 1 : 0);
+                                             : (p->C.max_accesses >= (1ull << 23) && P.jit_distinct <= 64 ? 1 : 0);
   const std::vector<size_t> mine = rank_chunks(P, rank, world);   // this rank's chunks
   if (gen_mode == 1 && !mine.empty()) {
     // the kernels this run needs, per mode: keys (sort / table detect), direct +

@@ -207,3 +207,24 @@ def test_rank_shards_cover_the_plan(inst, world):
         assert sum(x.racy_segments for x in parts) == o.n_racy_segments
         wits = [x.witness.as_tuple() for x in parts if x.witness]
         assert (min(wits) if wits else None) == o.witness
+
+
+# ---- many-chunk plans: AUTO takes the specialised generate when the chunks share kernels
+
+@pytest.mark.parametrize("name", ["5a", "5b"])
+def test_many_phase_plan_auto_takes_jit(name):
+    """5a/5b at T = 80 phases (80 chunks, 2 distinct kernels): AUTO must give the VM's
+    results (verdict, witness, count, racy cells = the closed forms) and run the
+    specialised generate (profiles/r2y_l2_5a.jsonl: 7x faster than the VM here)."""
+    T, R, C = 80, 32, 256
+    inst = config(name, T=T, R=R, C=C)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    assert p.n_chunks() > 64
+    vm = p.check_races(gen="vm")
+    auto = p.check_races()
+    assert _got(auto) == _got(vm)
+    assert auto.n_accesses == 1024 * R * C * 4 * T
+    assert auto.racy_segments == (0 if name == "5a" else 2 * 1024 * C * T)
+    t_vm = min(p.check_races(gen="vm").device_ms for _ in range(3))
+    t_auto = min(p.check_races().device_ms for _ in range(3))
+    assert t_auto * 2 < t_vm, (t_auto, t_vm)
