@@ -330,6 +330,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   const uint32_t K = filter ? 1u : std::max(1u, ch.unit_cluster);
   const int T = filter ? MAPC_GEN_THREADS : (int)ch.unit_threads;
   const uint64_t wpc = words / K;
+  const uint64_t words_k1 = (words + 31) / 32 * 32;   // K == 1: whole 32-word swizzle rows
   uint32_t log_wpc = 0;
   while ((1ull << log_wpc) < wpc) ++log_wpc;
   s << "extern \"C\" __global__ void __launch_bounds__(" << T << ") gen_" << index;
@@ -354,13 +355,18 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
       << "u;\n"
       << "  {\n";
   } else if (K == 1) {
-    s << "  __shared__ u32 tab[" << words << "];\n"
+    // one CTA per unit: the table's words are XOR-swizzled (word w lives at
+    // w ^ ((w >> 5) & 31), a permutation inside each 32-word row, so the table is
+    // padded to whole rows) -- column-wise sites (3a's transposed reads: lanes 16
+    // words apart) spread over all 32 banks instead of 2; the scan zeroes each word
+    // after reading it, so the table is cleared once per CTA, not per unit
+    s << "  __shared__ u32 tab[" << words_k1 << "];\n"
       << "  const u32 crank_ = 0u; (void)crank_;\n"
       << "  unsigned long long racy = 0, best = ~0ull;\n"
+      << "  for (u32 i = me; i < " << words_k1 << "u; i += " << T << "u) tab[i] = 0u;\n"
+      << "  __syncthreads();\n"
       << "  for (unsigned long long u = blockIdx.x; u < n_units; u += gridDim.x) {\n"
-      << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n"
-      << "    for (u32 i = me; i < " << words << "u; i += " << T << "u) tab[i] = 0u;\n"
-      << "    __syncthreads();\n";
+      << "    const u32 lph = (u32)(u / " << nb << "ull), lb = (u32)(u % " << nb << "ull);\n";
   } else {
     s << "  extern __shared__ u32 tab[];        // this CTA's " << wpc << " words of the unit table\n"
       << "  const u32 crank_ = cl_rank();\n"
@@ -389,7 +395,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
                                           : "tidv | ((~tidv & TMASK) << " + std::to_string(wt) + "u) | ((u32)(KIND) << " +
                                                 std::to_string(2 * wt) + "u)";
     if (K == 1)
-      s << "atomicOr(&tab[" << w << "], " << v << "); ";
+      s << "{ const u32 w_ = " << w << "; atomicOr(&tab[w_ ^ ((w_ >> 5) & 31u)], " << v << "); } ";
     else
       s << "cl_or(tab, " << w << " >> " << log_wpc << "u, " << w << " & " << wpc - 1 << "u, " << v << "); ";
     s << "if (!sg.dense) ++cnt; }\n";
@@ -463,9 +469,11 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   s << (K == 1 ? "    __syncthreads();\n" : "    cl_sync();\n")
     << "    const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
     << "u;\n"
-    << "    for (u32 il = me; il < " << wpc << "u; il += " << T << "u) {\n"
-    << "      const u32 i = crank_ * " << wpc << "u + il;      // the word's index in the unit table\n"
+    << "    for (u32 il = me; il < " << (K == 1 ? words_k1 : wpc) << "u; il += " << T << "u) {\n"
+    << (K == 1 ? "      const u32 i = il ^ ((il >> 5) & 31u);   // the word's index in the unit table (unswizzled)\n"
+               : "      const u32 i = crank_ * " + std::to_string(wpc) + "u + il;      // the word's index in the unit table\n")
     << "      const u32 w = tab[il];\n"
+    << (K == 1 ? "      tab[il] = 0u;\n" : "")
     << (cell_bytes == 2 ? "      if (!racy16w(w)) continue;\n" : "      if (!w) continue;\n");
   // cell c = (array, index) -> sort field base_ + (array << (wB + wI)) + index
   auto cell_sf = [&](const std::string& c) {
