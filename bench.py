@@ -61,6 +61,8 @@ def parse_args():
     ap.add_argument("--no-alt-path", action="store_true", help="skip timing the other detect paths")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing the other BASELINE.json config families (context, not the metric)")
+    ap.add_argument("--plain-scratch", action="store_true",
+                    help="scratch in plain device memory (torch.empty) instead of map_scratch_alloc's compressible memory")
     ap.add_argument("--mode", choices=["shard", "exchange"], default="shard",
                     help="multi-GPU mode: chunk sharding (default) or the key exchange (all_to_all)")
     return ap.parse_args()
@@ -353,7 +355,18 @@ def main():
     names = prog.array_names()
     if not args.chunk:
         args.chunk = prog.default_chunk(world)
-    scratch = torch.empty(prog.scratch_bytes(args.chunk), dtype=torch.uint8, device="cuda")
+    # scratch (key buffers / direct tables) from the library's allocator helper:
+    # compressible device memory when the driver grants it (the tables are cleared
+    # to zero before every chunk; zero lines compress -- include/mapcheck.h
+    # map_scratch_alloc), plain device memory with --plain-scratch
+    if args.plain_scratch:
+        scratch = torch.empty(prog.scratch_bytes(args.chunk), dtype=torch.uint8, device="cuda")
+        scratch_kind = "plain device memory (torch.empty)"
+    else:
+        scratch = mc.alloc_scratch(prog.scratch_bytes(args.chunk))
+        scratch_kind = ("compressible device memory (map_scratch_alloc, generic compression granted)"
+                        if scratch._map_block.compressed else "plain device memory (map_scratch_alloc: "
+                        "compression not granted)")
     stream = torch.cuda.current_stream()
     n_chunks = prog.n_chunks(args.chunk)
     my_chunks = prog.rank_chunks(rank, world, args.chunk)
@@ -453,7 +466,12 @@ def main():
     # the bucket-table path and the full sort (the north_star's generate -> sort -> detect)
     alt, roof_sort = None, None
     if not args.no_alt_path:
-        alt = {"identical_result": True}
+        alt = {"identical_result": True, "scratch": "plain device memory (torch.empty): the keys paths scatter "
+                                                    "incompressible keys, slower in compressible memory"}
+        if not args.plain_scratch:
+            del scratch
+            torch.cuda.synchronize()
+            scratch = torch.empty(prog.scratch_bytes(args.chunk), dtype=torch.uint8, device="cuda")
         for alt_mode in [m for m in ("table", "sort") if m != args.detect]:
             step(detect=alt_mode)
             if world > 1:
@@ -485,7 +503,8 @@ def main():
         for name in ("3a", "3b", "4a", "4b", "4c", "4d", "2b", "1a"):
             oi = config(name)
             op = mc.MapProgram(oi.src, oi.grid, oi.block, oi.params)
-            osc = torch.empty(op.scratch_bytes(), dtype=torch.uint8, device="cuda")
+            osc = (torch.empty(op.scratch_bytes(), dtype=torch.uint8, device="cuda") if args.plain_scratch
+                   else mc.alloc_scratch(op.scratch_bytes()))
             for _ in range(2):
                 orr = op.check_races(scratch=osc, stream=stream)
             ms_o = min(op.check_races(scratch=osc, stream=stream).device_ms for _ in range(3))
@@ -535,6 +554,7 @@ def main():
                                        f"key exchange over {world} ranks (all_to_all_single)"),
                        "l2": "inputs larger than L2: a 1 GiB direct-address table of 16-bit cells (or 8 GiB of "
                              "keys) per chunk vs 126 MB L2; no flush needed",
+                       "scratch": scratch_kind,
                        "verdict": "racy" if r0.verdict else "drf",
                        "witness": list(r0.witness.as_tuple()) if r0.witness else None},
             "roofline": roofline,

@@ -243,6 +243,26 @@ const char *map_array_name(const map_program *p, uint32_t idx);
 void map_program_free(map_program *p);
 const char *map_status_str(map_status s);
 
+/* ---- optional scratch allocator ----
+ * The library never allocates its device scratch; a caller may take it from
+ * here to get *compressible* device memory (flags MAP_ALLOC_COMPRESSIBLE:
+ * cuMemCreate with generic compression when the device supports it, else plain
+ * cudaMalloc).  The direct path (MAP_DETECT_DIRECT) clears its tables to zero
+ * before each chunk and its atomic ORs then fill those lines from DRAM; all-zero
+ * lines compress, so the clear and the fills move fewer DRAM bytes (DESIGN.md
+ * §6.1, 5a: 1262 -> 1391 G acc/s).  Results are identical in either memory.
+ * map_scratch_alloc: `bytes` (> 0) of device memory on `device` (made current);
+ * *ptr receives the address (caller-owned until map_scratch_free), *size (may be
+ * NULL) the rounded-up size, *compressed (may be NULL) 1 if the driver granted
+ * compression.  Errors: MAP_E_ARG (null ptr, bytes 0, unknown flag), MAP_E_CUDA
+ * (no device / driver), MAP_E_NOMEM (out of device memory).
+ * map_scratch_free: release a map_scratch_alloc block (synchronises the device
+ * first); NULL is a no-op; MAP_E_ARG for a pointer this helper did not return. */
+#define MAP_ALLOC_COMPRESSIBLE 1u
+map_status map_scratch_alloc(int device, uint64_t bytes, uint32_t flags, void **ptr, uint64_t *size,
+                             uint32_t *compressed);
+map_status map_scratch_free(void *ptr);
+
 /* ---- stage API (multi-GPU key exchange; NCCL via torch) ----
  * The hot path split at the exchange point, for a (phase, block) unit too
  * large for one GPU: every rank generates a slice of a chunk's tuples, the keys

@@ -458,6 +458,47 @@ def status_str(status: int) -> str:
     return _lib.map_status_str(status).decode()
 
 
+_lib.map_scratch_alloc.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p),
+                                   ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)]
+_lib.map_scratch_alloc.restype = ctypes.c_int
+_lib.map_scratch_free.argtypes = [ctypes.c_void_p]
+_lib.map_scratch_free.restype = ctypes.c_int
+EXPORTS = EXPORTS + ("map_scratch_alloc", "map_scratch_free")
+
+
+class _ScratchBlock:
+    """A map_scratch_alloc block, exposed through __cuda_array_interface__ so that
+    torch.as_tensor wraps it without a copy; freed when the last tensor on it dies."""
+
+    def __init__(self, nbytes: int, device: int, compressible: bool):
+        ptr, size, comp = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_uint32()
+        st = _lib.map_scratch_alloc(device, int(nbytes), 1 if compressible else 0, ctypes.byref(ptr),
+                                    ctypes.byref(size), ctypes.byref(comp))
+        if st != 0:
+            raise MapError(st, f"map_scratch_alloc({nbytes} B): {status_str(st)}")
+        self.ptr, self.size, self.compressed = int(ptr.value), int(size.value), bool(comp.value)
+        self.__cuda_array_interface__ = {"shape": (self.size,), "typestr": "|u1", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+    def __del__(self):
+        if getattr(self, "ptr", 0):
+            _lib.map_scratch_free(ctypes.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+def alloc_scratch(nbytes: int, device: Optional[int] = None, compressible: bool = True):
+    """Device scratch (a torch uint8 CUDA tensor) from map_scratch_alloc: compressible
+    memory when the device grants it (the direct path's cleared tables then cost fewer
+    DRAM bytes, include/mapcheck.h), else plain device memory.  `.compressed` on the
+    returned tensor's `_map_block` says which."""
+    import torch
+    dev = torch.cuda.current_device() if device is None else int(device)
+    blk = _ScratchBlock(nbytes, dev, compressible)
+    t = torch.as_tensor(blk, device=f"cuda:{dev}")
+    t._map_block = blk
+    return t
+
+
 def fastdiv_selftest(n: int, d: int) -> int:
     """Host copy of the kernels' invariant-divisor quotient (for CPU tests)."""
     return _lib.mapc_test_fastdiv(n, d)

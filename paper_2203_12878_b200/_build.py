@@ -15,6 +15,7 @@ SOURCES = [
     "capi/jit.cpp",
     "capi/bcapi.cpp",
     "capi/execute.cpp",
+    "capi/alloc.cpp",
     "babycuda/bcgen.cpp",
     "babycuda/bcfront.cpp",
     "kernels/generate.cu",

@@ -1,6 +1,6 @@
 """Device throughput of every config family at full size (every detect path).
 
-Usage: python scripts/probe_configs.py [names...] [--paths auto,unit,direct,table,sort]"""
+Usage: python scripts/probe_configs.py [names...] [--paths=auto,unit,direct,table,sort] [--compressible]"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,7 +17,8 @@ for name in (args or CONFIG_NAMES):
         continue
     inst = config(name)
     p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
-    scratch = torch.empty(p.scratch_bytes(), dtype=torch.uint8, device="cuda")
+    scratch = (mc.alloc_scratch(p.scratch_bytes()) if "--compressible" in sys.argv
+               else torch.empty(p.scratch_bytes(), dtype=torch.uint8, device="cuda"))
     out = {"cfg": name}
     for det in paths:
         gen = "jit" if det == "unit" else "auto"

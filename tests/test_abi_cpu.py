@@ -216,3 +216,23 @@ def test_literal_max_accepted():
     # 2^64 - 1 is a natural literal on both sides (R3)
     assert oracle.check("rd[18446744073709551615 - tid]", block=(2, 1, 1)).status == 0
     mc.MapProgram("rd[18446744073709551615 - tid]", block=(2, 1, 1))
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="needs a machine without a GPU")
+def test_scratch_alloc_without_device_fails_loudly():
+    """map_scratch_alloc (include/mapcheck.h): argument errors before device errors,
+    MAP_E_CUDA without a device (the library still loads: the driver API is looked
+    up at run time, libcuda is not linked); freeing NULL is a no-op, a foreign
+    pointer is MAP_E_ARG."""
+    import ctypes
+    lib = mc._lib
+    p, sz, comp = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_uint32()
+    assert lib.map_scratch_alloc(0, 1 << 20, 1, None, ctypes.byref(sz), ctypes.byref(comp)) == 8
+    assert lib.map_scratch_alloc(0, 0, 1, ctypes.byref(p), None, None) == 8
+    assert lib.map_scratch_alloc(0, 1 << 20, 6, ctypes.byref(p), None, None) == 8
+    assert lib.map_scratch_alloc(0, 1 << 20, 1, ctypes.byref(p), ctypes.byref(sz), ctypes.byref(comp)) == 6
+    assert p.value is None and sz.value == 0 and comp.value == 0
+    assert lib.map_scratch_free(None) == 0
+    assert lib.map_scratch_free(ctypes.c_void_p(0x1000)) == 8
+    with pytest.raises(mc.MapError):
+        mc.alloc_scratch(1 << 20, device=0)

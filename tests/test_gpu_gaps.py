@@ -228,3 +228,39 @@ def test_many_phase_plan_auto_takes_jit(name):
     t_vm = min(p.check_races(gen="vm").device_ms for _ in range(3))
     t_auto = min(p.check_races().device_ms for _ in range(3))
     assert t_auto * 2 < t_vm, (t_auto, t_vm)
+
+
+# ---- scratch in compressible device memory (map_scratch_alloc) ---------------
+
+def test_scratch_alloc_compressible_and_freed():
+    import torch
+    t = mc.alloc_scratch(3 << 30)
+    assert t.is_cuda and t.dtype == torch.uint8 and t.numel() >= 3 << 30
+    assert t._map_block.compressed            # B200 grants generic compression
+    t.fill_(7)
+    assert int(t[(3 << 30) - 1].item()) == 7
+    free0 = torch.cuda.mem_get_info()[0]
+    del t
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] >= free0 + (3 << 30) - (64 << 20)   # released, not cached
+    for _ in range(3):                                                     # no leak over cycles
+        u = mc.alloc_scratch(2 << 30, compressible=False)
+        assert not u._map_block.compressed
+        del u
+
+
+@pytest.mark.parametrize("inst", [config("5a", T=4, R=4, C=128), config("5b", T=4, R=4, C=128),
+                                  config("3b", ts=32, rw=8, grid=2048), config("4b", n=1 << 16, bs=1024),
+                                  config("4c", n=1 << 16, bs=1024)], ids=lambda i: i.name)
+def test_compressible_scratch_same_results(inst):
+    """Every detect path over compressible scratch = over plain scratch = the oracle
+    (the memory kind changes DRAM traffic only)."""
+    import torch
+    o = _want(oracle.check_instance(inst))
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    comp = mc.alloc_scratch(p.scratch_bytes())
+    comp.fill_(0xFF)                         # dirty, as a reused buffer would be
+    plain = torch.full((p.scratch_bytes(),), 0xFF, dtype=torch.uint8, device="cuda")
+    for det in ("auto", "direct", "table", "sort"):
+        for s in (comp, plain, comp):
+            assert _got(p.check_races(scratch=s, detect=det)) == o, det
