@@ -172,6 +172,11 @@ typedef struct {
  * another on the caller's stream only (no side stream: each chunk's clear,
  * generate and scan in turn) -- for measuring the kernels alone; same results. */
 #define MAP_EXEC_SEQUENTIAL 0x100u
+/* MAP_EXEC_PROFILE_GENERATE (map_exec.flags, with map_exec.stats): time only the
+ * generate launches (MAP_K_GENERATE, MAP_K_DIRECT, MAP_K_UNIT) with CUDA events;
+ * the other classes are counted (launches, bytes) but not timed (ms = 0), so
+ * the timing events perturb the run less (one event pair per chunk). */
+#define MAP_EXEC_PROFILE_GENERATE 0x200u
 
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */

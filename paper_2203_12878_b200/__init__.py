@@ -66,6 +66,7 @@ class _Exec(ctypes.Structure):
 GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
 DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40, "unit": 0x80}   # MAP_DETECT_* (mapcheck.h)
 EXEC_SEQUENTIAL = 0x100                                                       # MAP_EXEC_SEQUENTIAL
+EXEC_PROFILE_GENERATE = 0x200                                                 # MAP_EXEC_PROFILE_GENERATE
 
 
 class _Result(ctypes.Structure):
@@ -381,7 +382,9 @@ class MapProgram:
         stream: a torch.cuda.Stream (default: the current stream);
         rank/world: process only rank `rank`'s chunks (rank_chunks; multi-GPU sharding; with
                     chunk_max_accesses 0 the plan uses default_chunk(world));
-        profile: record CUDA events around every launch and return per-kernel-class timings;
+        profile: record CUDA events around every launch and return per-kernel-class timings
+                 (True), or around the generate launches only ("generate": the other classes are
+                 counted, not timed; MAP_EXEC_PROFILE_GENERATE);
         gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised);
         detect: "auto" | "direct" | "table" | "sort" (include/mapcheck.h MAP_DETECT_*);
         overlap: False = MAP_EXEC_SEQUENTIAL (the direct path's chunks one after another)."""
@@ -400,7 +403,8 @@ class MapProgram:
         ex = _Exec(dev, ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(scratch.data_ptr()),
                    scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
                    ctypes.pointer(stats) if stats is not None else None,
-                   GEN_PATHS[gen] | DETECT_PATHS[detect] | (0 if overlap else EXEC_SEQUENTIAL))
+                   GEN_PATHS[gen] | DETECT_PATHS[detect] | (0 if overlap else EXEC_SEQUENTIAL) |
+                   (EXEC_PROFILE_GENERATE if profile == "generate" else 0))
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:
@@ -477,12 +481,13 @@ class _ScratchBlock:
         if st != 0:
             raise MapError(st, f"map_scratch_alloc({nbytes} B): {status_str(st)}")
         self.ptr, self.size, self.compressed = int(ptr.value), int(size.value), bool(comp.value)
+        self._free = _lib.map_scratch_free          # held: module globals may be gone at exit
         self.__cuda_array_interface__ = {"shape": (self.size,), "typestr": "|u1", "data": (self.ptr, False),
                                          "version": 3, "strides": None}
 
     def __del__(self):
         if getattr(self, "ptr", 0):
-            _lib.map_scratch_free(ctypes.c_void_p(self.ptr))
+            self._free(self.ptr)
             self.ptr = 0
 
 

@@ -170,6 +170,7 @@ struct map_program {
   uint64_t default_cap_cache = 0;    // default_cap(), computed once
   uint64_t g_h2d = 0;
   map_kernel_stats g_stats{};
+  std::vector<uint64_t> g_marks;     // profiled graph: (kind, event, event) per timed launch
   ~map_program() {
     for (cudaEvent_t e : events) cudaEventDestroy(e);
     for (cudaEvent_t e : sync_events) cudaEventDestroy(e);
@@ -846,29 +847,41 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   size_t ev = 2;
   uint32_t launches = 0;
   map_kernel_stats st_acc{};
+  // per-launch timing events go to the stream the run is enqueued on (the caller's,
+  // or the capture stream); inside a capture they become event-record nodes of the
+  // graph (cudaEventRecordExternal), so a profiled run replays as a graph too
+  cudaStream_t rec_s = s;
+  bool capturing = false;
+  auto rec = [&](size_t e, cudaStream_t st) {
+    cudaEventRecordWithFlags(p->events[e], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+  };
+  const bool gen_only = (ex->flags & MAP_EXEC_PROFILE_GENERATE) != 0;
+  auto timed = [&](int kind) {
+    return prof && (!gen_only || kind == MAP_K_GENERATE || kind == MAP_K_DIRECT || kind == MAP_K_UNIT);
+  };
   auto begin = [&](int kind) -> size_t {
     ++launches;
     st_acc.launches[kind]++;
-    if (!prof) return 0;
-    cudaEventRecord(p->events[ev], s);
+    if (!timed(kind)) return 0;
+    rec(ev, rec_s);
     marks.push_back({kind, ev, ev + 1});
     ev += 2;
     return ev - 1;
   };
   auto end = [&](size_t e1) {
-    if (prof) cudaEventRecord(p->events[e1], s);
+    if (prof && e1) rec(e1, rec_s);
   };
   auto begin_on = [&](int kind, cudaStream_t st) -> size_t {   // same, on another stream
     ++launches;
     st_acc.launches[kind]++;
-    if (!prof) return 0;
-    cudaEventRecord(p->events[ev], st);
+    if (!timed(kind)) return 0;
+    rec(ev, st);
     marks.push_back({kind, ev, ev + 1});
     ev += 2;
     return ev - 1;
   };
   auto end_on = [&](size_t e1, cudaStream_t st) {
-    if (prof) cudaEventRecord(p->events[e1], st);
+    if (prof && e1) rec(e1, st);
   };
   uint64_t h2d = 0;
   // Everything the run enqueues between the two timing events.  Without
@@ -1131,15 +1144,20 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     put(&plan_for, 8); put(&ex->flags, 4); put(&ex->scratch, sizeof(void*)); put(&ex->scratch_bytes, 8);
     put(&ex->stream, sizeof(void*)); put(&ex->device, 4); put(&rank, 4); put(&world, 4); put(&gen_mode, 4);
     put(&p->pinned, sizeof(void*));
+    const uint8_t pf = prof;
+    put(&pf, 1);
   }
   // (not with the look-back onesweep variant: its epochs must advance every run)
-  const bool use_graph = graphs_env && !prof && !mine.empty() && sort_mode == 1;
+  const bool use_graph = graphs_env && !mine.empty() && sort_mode == 1;
   if (use_graph && p->gexec && p->gkey == gkey) {            // replay
     CK(cudaEventRecord(p->events[0], s));
     CK(cudaGraphLaunch(p->gexec, s));
     launches = p->g_launches;
     h2d = p->g_h2d;
     st_acc = p->g_stats;
+    marks.clear();
+    for (size_t i = 0; i + 3 <= p->g_marks.size(); i += 3)
+      marks.push_back({(int)p->g_marks[i], (size_t)p->g_marks[i + 1], (size_t)p->g_marks[i + 2]});
   } else if (use_graph && p->glast_key == gkey) {            // second identical call: capture
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; p->gkey.clear(); }
     if (!p->cap || p->cap_dev != ex->device) {
@@ -1149,7 +1167,11 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       p->cap_dev = ex->device;
     }
     CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+    rec_s = p->cap;
+    capturing = true;
     const map_status est = enqueue(p->cap);
+    capturing = false;
+    rec_s = s;
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(p->cap, &graph);
     if (est != MAP_OK) { if (graph) cudaGraphDestroy(graph); return est; }
@@ -1168,6 +1190,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     p->g_launches = launches;
     p->g_h2d = h2d;
     p->g_stats = st_acc;
+    p->g_marks.clear();
+    for (const Mark& mk : marks) p->g_marks.insert(p->g_marks.end(), {(uint64_t)mk.kind, mk.e0, mk.e1});
     CK(cudaEventRecord(p->events[0], s));
     CK(cudaGraphLaunch(p->gexec, s));
   } else {

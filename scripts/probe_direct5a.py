@@ -8,7 +8,8 @@ from workloads import config
 
 inst = config("5a")
 p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
-scratch = torch.empty(p.scratch_bytes(), dtype=torch.uint8, device="cuda")
+scratch = (torch.empty(p.scratch_bytes(), dtype=torch.uint8, device="cuda") if os.environ.get("PLAIN_SCRATCH")
+           else mc.alloc_scratch(p.scratch_bytes()))
 out = {"env": {k: v for k, v in os.environ.items() if k.startswith("MAPC_")}}
 for ovl in (False, True):
     p.check_races(scratch=scratch, overlap=ovl)

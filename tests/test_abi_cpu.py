@@ -236,3 +236,15 @@ def test_scratch_alloc_without_device_fails_loudly():
     assert lib.map_scratch_free(ctypes.c_void_p(0x1000)) == 8
     with pytest.raises(mc.MapError):
         mc.alloc_scratch(1 << 20, device=0)
+
+
+def test_python_flag_constants_match_header():
+    """The binding's flag values are the header's #defines (marshalling only)."""
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "mapcheck.h")).read()
+    val = lambda name: int(re.search(r"#define " + name + r" (0x[0-9A-Fa-f]+|\d+)u", hdr).group(1), 0)
+    assert mc.GEN_PATHS == {"auto": val("MAP_GEN_AUTO"), "vm": val("MAP_GEN_VM"), "jit": val("MAP_GEN_JIT")}
+    for k in ("sort", "table", "direct", "unit", "auto"):
+        assert mc.DETECT_PATHS[k] == val("MAP_DETECT_" + k.upper())
+    assert mc.EXEC_SEQUENTIAL == val("MAP_EXEC_SEQUENTIAL")
+    assert mc.EXEC_PROFILE_GENERATE == val("MAP_EXEC_PROFILE_GENERATE")

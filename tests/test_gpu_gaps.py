@@ -264,3 +264,23 @@ def test_compressible_scratch_same_results(inst):
     for det in ("auto", "direct", "table", "sort"):
         for s in (comp, plain, comp):
             assert _got(p.check_races(scratch=s, detect=det)) == o, det
+
+
+def test_profiled_runs_replay_as_graphs():
+    """profile=True calls are captured (third call on) with their timing events as
+    graph nodes: same results and the same per-kernel launch counts in the eager,
+    capturing and replaying calls, every timed class with a positive time."""
+    inst = config("5b", T=4, R=4, C=128)
+    o = _want(oracle.check_instance(inst))
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    runs = [p.check_races(profile=True, gen="jit") for _ in range(5)]
+    for r in runs:
+        assert _got(r) == o
+    launches = [{k: v["launches"] for k, v in r.kernels.items()} for r in runs]
+    assert all(x == launches[0] for x in launches)
+    for r in runs[2:]:
+        for k, v in r.kernels.items():
+            if v["launches"]:
+                assert v["ms"] > 0, (k, v)
+    plain = [p.check_races(gen="jit").device_ms for _ in range(3)]
+    assert min(r.device_ms for r in runs[2:]) < 3 * min(plain) + 0.05
