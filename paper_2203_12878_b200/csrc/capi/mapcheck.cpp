@@ -139,6 +139,75 @@ struct NvtxRange {
   NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// Host-side CUDA resources recycled across programs: a caller that compiles a
+// fresh program per call (the e2e path: MAP text in, verdict out) would otherwise
+// pay cudaMallocHost, stream and event creation (and their destruction) on every
+// call.  Never freed: the process's exit releases them (no CUDA calls from static
+// destructors).
+struct ResourcePool {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> pinned;
+  std::vector<std::pair<int, cudaStream_t>> streams;       // (device, non-blocking stream)
+  std::vector<std::pair<int, cudaEvent_t>> timing, sync;   // (device, event)
+};
+ResourcePool& pool() {
+  static ResourcePool* p = new ResourcePool();
+  return *p;
+}
+void* pool_pinned(size_t bytes, size_t* got) {
+  {
+    ResourcePool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    size_t best = P.pinned.size();
+    for (size_t i = 0; i < P.pinned.size(); ++i)
+      if (P.pinned[i].second >= bytes && (best == P.pinned.size() || P.pinned[i].second < P.pinned[best].second))
+        best = i;
+    if (best < P.pinned.size()) {
+      void* r = P.pinned[best].first;
+      *got = P.pinned[best].second;
+      P.pinned.erase(P.pinned.begin() + best);
+      return r;
+    }
+  }
+  void* r = nullptr;
+  if (cudaMallocHost(&r, bytes) != cudaSuccess) return nullptr;
+  *got = bytes;
+  return r;
+}
+void pool_release_pinned(void* ptr, size_t bytes) {
+  if (!ptr) return;
+  ResourcePool& P = pool();
+  std::lock_guard<std::mutex> g(P.mu);
+  P.pinned.emplace_back(ptr, bytes);
+}
+cudaError_t pool_stream(int dev, cudaStream_t* out) {
+  {
+    ResourcePool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    for (size_t i = 0; i < P.streams.size(); ++i)
+      if (P.streams[i].first == dev) {
+        *out = P.streams[i].second;
+        P.streams.erase(P.streams.begin() + i);
+        return cudaSuccess;
+      }
+  }
+  return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+}
+cudaError_t pool_event(int dev, bool timing, cudaEvent_t* out) {
+  {
+    ResourcePool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    auto& v = timing ? P.timing : P.sync;
+    for (size_t i = v.size(); i-- > 0;)
+      if (v[i].first == dev) {
+        *out = v[i].second;
+        v.erase(v.begin() + i);
+        return cudaSuccess;
+      }
+  }
+  return timing ? cudaEventCreate(out) : cudaEventCreateWithFlags(out, cudaEventDisableTiming);
+}
+
 }  // namespace
 
 struct map_program {
@@ -154,6 +223,7 @@ struct map_program {
   int device = -1;
   std::string last_error;
   std::vector<cudaEvent_t> events;   // pool for per-kernel timing
+  int events_dev = -1;               // device of events and sync_events
   // overlapped direct pipeline: a library-owned side stream (scan, clear and
   // witness of chunk k run there while chunk k+1's generate runs on the caller's
   // stream) and its ordering events
@@ -171,12 +241,22 @@ struct map_program {
   uint64_t g_h2d = 0;
   map_kernel_stats g_stats{};
   std::vector<uint64_t> g_marks;     // profiled graph: (kind, event, event) per timed launch
+  // timing and sync events, streams and the staging buffer go back to the pool
+  void release_events() {
+    ResourcePool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    for (cudaEvent_t e : events) P.timing.emplace_back(events_dev, e);
+    for (cudaEvent_t e : sync_events) P.sync.emplace_back(events_dev, e);
+    events.clear();
+    sync_events.clear();
+  }
   ~map_program() {
-    for (cudaEvent_t e : events) cudaEventDestroy(e);
-    for (cudaEvent_t e : sync_events) cudaEventDestroy(e);
-    if (side) cudaStreamDestroy(side);
     if (gexec) cudaGraphExecDestroy(gexec);
-    if (cap) cudaStreamDestroy(cap);
+    release_events();
+    ResourcePool& P = pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    if (side) P.streams.emplace_back(side_dev, side);
+    if (cap) P.streams.emplace_back(cap_dev, cap);
   }
 };
 
@@ -738,11 +818,16 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
     p->gkey.clear();
     p->glast_key.clear();
-    if (p->pinned) cudaFreeHost(p->pinned);
+    pool_release_pinned(p->pinned, p->pinned_bytes);
     p->pinned = nullptr;
     p->pinned_bytes = 0;
-    CK(cudaMallocHost(&p->pinned, P.stage_bytes));
-    p->pinned_bytes = P.stage_bytes;
+    size_t got = 0;
+    p->pinned = pool_pinned(P.stage_bytes, &got);
+    if (!p->pinned) {
+      p->last_error = "cudaMallocHost failed";
+      return MAP_E_CUDA;
+    }
+    p->pinned_bytes = got;
   }
   unsigned char* stage = (unsigned char*)p->pinned;
   for (auto& ch : P.chunks) {
@@ -837,9 +922,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // events: 2 per timed launch group + 2 for the whole run
   const bool prof = ex->stats != nullptr;
   size_t need_ev = 2 + (prof ? mine.size() * (2 * (8 + MAPC_MAX_PASSES)) : 0);
+  if (p->events_dev != ex->device) {   // events belong to the device current at creation
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; p->gkey.clear(); }
+    p->release_events();
+    p->events_dev = ex->device;
+  }
   while (p->events.size() < need_ev) {
     cudaEvent_t e;
-    CK(cudaEventCreate(&e));
+    CK(pool_event(ex->device, true, &e));
     p->events.push_back(e);
   }
   struct Mark { int kind; size_t e0, e1; };
@@ -906,14 +996,17 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags) && !use_unit(P.chunks[c], ex->flags, gen_mode);
   if (ovl) {
     if (!p->side || p->side_dev != ex->device) {
-      if (p->side) cudaStreamDestroy(p->side);
+      if (p->side) {
+        std::lock_guard<std::mutex> g(pool().mu);
+        pool().streams.emplace_back(p->side_dev, p->side);
+      }
       p->side = nullptr;
-      CK(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+      CK(pool_stream(ex->device, &p->side));
       p->side_dev = ex->device;
     }
     while (p->sync_events.size() < 5) {
       cudaEvent_t e;
-      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(pool_event(ex->device, false, &e));
       p->sync_events.push_back(e);
     }
     cudaStream_t s2 = p->side;
@@ -1161,9 +1254,12 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   } else if (use_graph && p->glast_key == gkey) {            // second identical call: capture
     if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; p->gkey.clear(); }
     if (!p->cap || p->cap_dev != ex->device) {
-      if (p->cap) cudaStreamDestroy(p->cap);
+      if (p->cap) {
+        std::lock_guard<std::mutex> g(pool().mu);
+        pool().streams.emplace_back(p->cap_dev, p->cap);
+      }
       p->cap = nullptr;
-      CK(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+      CK(pool_stream(ex->device, &p->cap));
       p->cap_dev = ex->device;
     }
     CK(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
@@ -1288,7 +1384,7 @@ map_status map_witness_get(const map_program* p, map_witness* out) {
 
 void map_program_free(map_program* p) {
   if (!p) return;
-  if (p->pinned) cudaFreeHost(p->pinned);
+  pool_release_pinned(p->pinned, p->pinned_bytes);
   delete p;
 }
 

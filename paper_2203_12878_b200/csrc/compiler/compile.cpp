@@ -767,6 +767,9 @@ struct Builder {
   uint32_t phase = 0;
   uint64_t instances = 0;
   std::vector<std::pair<int, std::vector<uint64_t>>> pending;   // (tmpl, syncenv) per instance
+  // choose_tuple_order per distinct group program in this compile (the phases of a
+  // time loop repeat the same few programs: 5a's 16 phases have 2)
+  std::map<std::string, bool> order_memo;
 
   explicit Builder(Compiled& c) : C(c) {}
 
@@ -913,7 +916,20 @@ struct Builder {
         for (size_t q = 0; q < parts.size(); ++q) {
           GroupProg& gq = parts[q];
           if (part_max[q] >= (1ull << 32)) C.u32_mode = false;
-          choose_tuple_order(&gq, C.n_threads);
+          {
+            std::string key(reinterpret_cast<const char*>(gq.ops.data()), gq.ops.size() * sizeof(MapcOp));
+            key.append(reinterpret_cast<const char*>(gq.trips), sizeof(gq.trips));
+            key.append(reinterpret_cast<const char*>(&gq.n_levels), sizeof(gq.n_levels));
+            key.append(reinterpret_cast<const char*>(&gq.n_emits), sizeof(gq.n_emits));
+            key.append(reinterpret_cast<const char*>(&gq.tuples_per_block), sizeof(gq.tuples_per_block));
+            auto it = order_memo.find(key);
+            if (it != order_memo.end()) {
+              gq.tid_inner = it->second;
+            } else {
+              choose_tuple_order(&gq, C.n_threads);
+              order_memo.emplace(std::move(key), gq.tid_inner);
+            }
+          }
           info.bound_per_block = checked((u128)info.bound_per_block +
                                              (u128)gq.tuples_per_block * std::max<uint32_t>(gq.n_emits, 0),
                                          "access bound");
@@ -987,7 +1003,8 @@ uint64_t warp_sectors(const GroupProg& g, uint64_t n_threads, bool tid_inner) {
   std::vector<int64_t> idx;
   for (int pos = 1; pos <= 3; ++pos) {
     const uint64_t t0 = (n * pos / 4) / 32 * 32;
-    std::vector<std::set<int64_t>> sec(g.n_emits);
+    std::vector<std::vector<int64_t>> sec(g.n_emits);
+    for (auto& v : sec) v.reserve(32);
     for (uint64_t t = t0; t < std::min(n, t0 + 32); ++t) {
       uint64_t rem = t, tid, k[MAPC_MAX_LEVELS] = {};
       if (tid_inner) { tid = rem % n_threads; rem /= n_threads; }
@@ -995,9 +1012,12 @@ uint64_t warp_sectors(const GroupProg& g, uint64_t n_threads, bool tid_inner) {
       if (!tid_inner) tid = rem % n_threads;
       eval_sites(g, tid, 0, k, &idx);
       for (size_t e = 0; e < idx.size() && e < sec.size(); ++e)
-        if (idx[e] >= 0) sec[e].insert(idx[e] >> 3);
+        if (idx[e] >= 0) sec[e].push_back(idx[e] >> 3);
     }
-    for (auto& s : sec) total += s.size();
+    for (auto& v : sec) {
+      std::sort(v.begin(), v.end());
+      total += std::unique(v.begin(), v.end()) - v.begin();
+    }
   }
   return total;
 }
