@@ -241,7 +241,7 @@ def ncu_direct():
 RED64_CEILING_TBS = 4.03
 
 
-def issue_roofline(kern, hbm, acc_per_launch=None):
+def issue_roofline(kern, hbm, acc_per_launch=None, reds_per_access=0.25):
     """The direct generate: primary view HBM (2 x table bytes per launch over its live
     CUDA-event time; DRAM traffic = algorithmic in the committed ncu capture).  Since the
     r1t/r1u instruction cuts it is no longer issue-bound (issue ~61% alone, r1w): what
@@ -259,12 +259,14 @@ def issue_roofline(kern, hbm, acc_per_launch=None):
     out = dict(hbm)
     if acc_per_launch:
         # 16-bit cells in aligned quads: one red.or.b64 per 4 accesses (5a: every site
-        # unit-stride, every quad aligned)
-        red_tbs = acc_per_launch / 4 * 8 / per_launch_s / 1e12
+        # unit-stride, every quad aligned); row-jammed by JU rows per thread, a row's
+        # three reads fold into one reduction: (JU + 2 + JU) per 16 JU accesses
+        red_tbs = acc_per_launch * reds_per_access * 8 / per_launch_s / 1e12
         out["red"] = {"achieved": red_tbs, "peak": RED64_CEILING_TBS, "unit": "TB/s of red.or.b64 payload",
                       "peak_kind": "measured microbenchmark (profiles/r1h_red_width_microbench.txt)",
                       "frac": red_tbs / RED64_CEILING_TBS,
-                      "work_model": "accesses / 4 red.or.b64 of 8 B per launch"}
+                      "reds_per_access": reds_per_access,
+                      "work_model": f"accesses x {reds_per_access:.4f} red.or.b64 of 8 B per launch"}
     out["alu"] = {"achieved": achieved, "peak": ISSUE_PEAK_G,
                   "peak_kind": "derived: 148 SMs x 4 schedulers x 1.965 GHz (one warp-instruction per scheduler-cycle)",
                   "unit": "G warp-inst/s", "frac": achieved / ISSUE_PEAK_G,
@@ -434,9 +436,15 @@ def main():
     ms_of = lambda c: kern.get(c, {}).get("ms", 0) + (kern.get("onesweep_next", {}).get("ms", 0) if c == "onesweep" else 0)
     dominant = max(ROOFLINE_MODELS, key=ms_of)
     roofline = kernel_roofline(kern, dominant, peak, peak_kind)
+    # reductions per access of the direct generate: 5a's stencil (three reads of a row,
+    # one write) in quads, row-jammed by JU rows per thread when the JIT took the jam
+    import re as _re
+    _m = _re.search(r"u_ < (\d+)u", prog.jit_source(0, 1)) if inst.name[0] == "5" else None
+    ju = int(_m.group(1)) if _m else 0
+    reds_per_access = (2 * ju + 2) / (16 * ju) if ju else 0.25
     if dominant == "direct":
         acc_launch = sum(r.n_accesses for r in results) / max(1, kern.get("direct", {}).get("launches", 0))
-        roofline = issue_roofline(kern, roofline, acc_launch)
+        roofline = issue_roofline(kern, roofline, acc_launch, reds_per_access)
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
     pipe_bytes = sum(v["bytes"] for v in kern.values())
     # the dominant kernel alone: the direct path's chunks run one after another
@@ -447,7 +455,8 @@ def main():
                                  world=world, profile=True, detect=args.detect, overlap=False) for _ in range(2)]
         k_solo = kernel_table(solo[1:])
         r_solo = issue_roofline(k_solo, kernel_roofline(k_solo, "direct", peak, peak_kind),
-                                solo[1].n_accesses / max(1, k_solo.get("direct", {}).get("launches", 0)))
+                                solo[1].n_accesses / max(1, k_solo.get("direct", {}).get("launches", 0)),
+                                reds_per_access)
         roofline["solo"] = {"achieved": r_solo["achieved"], "frac": r_solo["frac"], "unit": r_solo["unit"],
                             "red_frac": r_solo.get("red", {}).get("frac"),
                             "note": "same kernel, chunks run sequentially (no concurrent scans)"}

@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include "../compiler/compiler.h"
 #include "../devabi.h"
 #include "jit.h"
 
@@ -511,6 +512,76 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   return s.str();
 }
 
+// Row-jam rows per thread for a direct-mode chunk of 16-bit cells (paired_case):
+// every baked segment's program has a second-innermost loop (rows) and a
+// multiple-of-4 innermost range L dividing or divisible by the 512-tuple tile, the
+// segment is whole super-tiles of JU tiles and its row count is a multiple of JU
+// (a thread's rows never cross that loop's carry).  The largest JU in {16, 8, 4,
+// 2} that holds for every segment, else 0.  MAPC_JAM=0 disables, MAPC_JAM=n caps.
+// Site pairs (k, k2) of a program such that site k of row r + 1 is site k2 of
+// row r (same array, same index) at every sampled tuple where both are active and
+// at least one: the only pairs the row-jam compares at run time (the comparison
+// itself keeps it exact -- a pair that does not hold at some tuple just does not
+// merge there).  Sampled with the host evaluator of the bytecode.
+std::vector<std::pair<int, int>> jam_pairs(const JitProgram& pg, const MapcSeg& g) {
+  std::vector<std::pair<int, int>> out;
+  std::vector<uint32_t> arr;
+  for (const MapcOp& op : pg.ops)
+    if ((op.code & MAPC_CODE_MASK) == VM_EMIT) arr.push_back(op.aux >> 1);
+  const int ne = (int)arr.size();
+  if (pg.n_levels < 2 || ne == 0) return out;
+  const uint64_t nt = g.tid_div.d, rows = g.trip_div[pg.n_levels - 2].d, L = g.trip_div[pg.n_levels - 1].d;
+  if (rows < 2) return out;
+  std::vector<std::vector<int>> hold(ne, std::vector<int>(ne, 0));   // 0 unseen, 1 held, -1 broken
+  const uint64_t tids[] = {0, 1, nt / 2, nt - 1};
+  const uint64_t rs[] = {0, 1 % (rows - 1), (rows / 2) % (rows - 1), rows - 2};   // r + 1 < rows
+  const uint64_t cs[] = {0, 4 % L, (L / 2) / 4 * 4, (L - 4) % L};
+  std::vector<int64_t> a, b;
+  for (uint64_t tid : tids)
+    for (uint64_t r : rs)
+      for (uint64_t c : cs) {
+        uint64_t k0[MAPC_MAX_LEVELS] = {}, k1[MAPC_MAX_LEVELS] = {};
+        k0[pg.n_levels - 2] = r;
+        k1[pg.n_levels - 2] = r + 1;
+        k0[pg.n_levels - 1] = k1[pg.n_levels - 1] = c;
+        mapc::eval_ops_sites(pg.ops, pg.n_levels, tid % nt, g.b0, k0, &a);
+        mapc::eval_ops_sites(pg.ops, pg.n_levels, tid % nt, g.b0, k1, &b);
+        for (int k = 0; k < ne && k < (int)b.size(); ++k)
+          for (int k2 = 0; k2 < ne && k2 < (int)a.size(); ++k2) {
+            if (b[k] < 0 || a[k2] < 0 || hold[k][k2] < 0) continue;
+            hold[k][k2] = (b[k] == a[k2] && arr[k] == arr[k2]) ? 1 : -1;
+          }
+      }
+  for (int k = 0; k < ne; ++k)
+    for (int k2 = 0; k2 < ne; ++k2)
+      if (hold[k][k2] == 1) out.emplace_back(k, k2);
+  return out;
+}
+
+uint32_t jam_rows(const JitChunk& ch) {
+  static const int env = [] { const char* e = getenv("MAPC_JAM"); return e ? atoi(e) : 16; }();
+  if (env < 2 || ch.segs.empty() || ch.lay.sort_bits > 31) return 0;
+  for (uint32_t U = 16; U >= 2; U /= 2) {
+    if ((int)U > env) continue;
+    bool ok = true;
+    for (const MapcSeg& g : ch.segs) {
+      const JitProgram* pg = nullptr;
+      for (const JitProgram& p : ch.programs)
+        if (p.prog_begin == g.prog_begin) pg = &p;
+      if (!pg || pg->n_levels < 2 || pg->tid_inner || g.tid_inner || g.n_levels != pg->n_levels) { ok = false; break; }
+      const uint64_t L = pg->inner_range;
+      const uint64_t rows = g.trip_div[pg->n_levels - 2].d;
+      ok = L % 4 == 0 && g.trip_div[pg->n_levels - 1].d == L && (L <= MAPC_GEN_TILE ? MAPC_GEN_TILE % L == 0
+                                                                                   : L % MAPC_GEN_TILE == 0) &&
+           rows % U == 0 && g.n_tuples % ((uint64_t)MAPC_GEN_TILE * U) == 0 && g.tile_begin % U == 0 &&
+           g.n_tuples < (1ull << 32) && !jam_pairs(*pg, g).empty();   // something to merge
+      if (!ok) break;
+    }
+    if (ok) return U;
+  }
+  return 0;
+}
+
 }  // namespace
 
 std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes) {
@@ -541,6 +612,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   // measured 25% SLOWER: the direct generate is bound by the table's DRAM
   // read-modify-write traffic, not by the reduction count -- DESIGN.md §6.1.)
   const int minb = mode == MAPC_MODE_DIRECT ? minb_env : 0;
+  const uint32_t JU = paired && blocked && cell_bytes == 2 ? jam_rows(ch) : 0u;   // row-jam (paired_case), 0 = off
   s << "extern \"C\" __global__ void __launch_bounds__(" << T;
   if (minb > 0) s << ", " << minb;
   s << ") gen_" << index
@@ -564,12 +636,28 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (paired)   // one set for every case: per-case arrays inflate the register allocation per switch case
     s << "  " << (sf32 ? "u32" : "u64") << " sfP[" << MAPC_MAX_EMITS << "]; u32 cdP[" << MAPC_MAX_EMITS
       << "]; bool okP[" << MAPC_MAX_EMITS << "]; u64 accP[" << MAPC_MAX_EMITS << "]; (void)cdP; (void)accP;\n";
+  // row-jam: the previous row's quads.  Every slot is defined before the first row:
+  // a site that does not emit leaves its slot unwritten, and the row-to-row copy
+  // of an indeterminate value let NVRTC fold the loop-carried state wrongly
+  // (random row MAPs lost or misplaced codes until these were initialised)
+  if (JU)
+    s << "  u32 sfQ[" << MAPC_MAX_EMITS << "]; bool okQ[" << MAPC_MAX_EMITS << "]; u64 accQ[" << MAPC_MAX_EMITS << "];\n"
+      << "#pragma unroll\n"
+      << "  for (int k = 0; k < " << MAPC_MAX_EMITS << "; ++k) { sfQ[k] = 0u; okQ[k] = false; accQ[k] = 0ull; "
+         "sfP[k] = 0u; okP[k] = false; accP[k] = 0ull; }\n";
   if (mode == MAPC_MODE_FILTER)
     s << "  const u64 target = *target_ptr;\n"
       << "  if (target == ~0ull) return;\n";
   // (L2 eviction-priority hints -- evict-last on these reductions, evict-first on the
   // concurrent scan and clear -- were measured without effect: profiles/r2r_l2_hints_ab.jsonl)
-  s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
+  if (JU)   // row-jam: every CTA walks a contiguous block of super-tiles (JU tiles each)
+    s << "  const u64 n_super_ = total_tiles / " << JU << "u;\n"
+      << "  const u64 per_cta_ = (n_super_ + gridDim.x - 1) / gridDim.x;\n"
+      << "  const u64 st_end_ = min(n_super_, (u64)(blockIdx.x + 1) * per_cta_);\n"
+      << "  for (u64 st_ = (u64)blockIdx.x * per_cta_; st_ < st_end_; ++st_) {\n"
+      << "    const u64 tile = st_ * " << JU << "u;\n";
+  else
+    s << (blocked ? "  const u64 per_cta_ = (total_tiles + gridDim.x - 1) / gridDim.x;\n"
                     "  const u64 tile_end_ = min(total_tiles, (u64)(blockIdx.x + 1) * per_cta_);\n"
                     "  for (u64 tile = (u64)blockIdx.x * per_cta_; tile < tile_end_; ++tile) {\n"
                   : "  for (u64 tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {\n");
@@ -617,11 +705,48 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     // G consecutive tuples per thread: pairs of u32 cells (one red.or.b64), or
     // quads of 16-bit cells (one red.or.b64 over four cells)
     const int G = cell_bytes == 2 ? 4 : 2;
-    s << "    case " << pg.prog_begin << "u: {\n"
-      << "#pragma unroll 1\n"
-      << "      for (int v = 0; v < " << V / G << "; ++v) {\n"
-      << "        const u32 tp = tl0 + v * " << G * T << "u + " << G << "u * me;\n"
-      << "#pragma unroll\n"
+    // Row-jam (JU > 0, chunk-wide, jam_rows): a thread takes JU consecutive rows
+    // (second-innermost coordinate) of one column quad instead of one quad per
+    // tile; a cell the next row touches again (5a: a read-half row is read as
+    // row r + 1, r and r - 1 of three successive rows) is ORed into that row's
+    // quad in registers, and a quad is reduced into the table only when the next
+    // row no longer touches it -- 5a: 0.25 -> (JU + 2 + JU) / (16 JU) global
+    // red.or.b64 per access.  Same cells, same codes: the table is identical.
+    const bool jam = JU != 0 && G == 4;
+    const uint64_t L = pg.inner_range;
+    const bool nocarry = pg.inner_range % (uint64_t)G == 0;
+    const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
+    s << "    case " << pg.prog_begin << "u: {\n";
+    if (jam) {
+      s << "      const u32 sl_ = (u32)((tile - sg.tile_begin) / " << JU << "u);\n";
+      if (L <= 512)   // P = 512 / L rows per tile, L / 4 threads per row
+        s << "      const u32 tq_ = (sl_ * " << JU * (512 / L) << "u + (u32)(me / " << L / 4 << ") * " << JU << "u) * " << L
+          << "u + 4u * (u32)(me % " << L / 4 << ");\n";
+      else            // S = L / 512 super-tiles per row block
+        s << "      const u32 tq_ = (sl_ / " << L / 512 << "u) * " << JU * L << "u + (sl_ % " << L / 512
+          << "u) * 512u + 4u * (u32)me;\n";
+      s << "#pragma unroll\n"
+        << "      for (int k = 0; k < " << NE << "; ++k) okQ[k] = false;\n"
+        << "      bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n"
+        << "      {\n"
+        << "        const u32 t = tq_;\n"
+        << "        const bool valid = true;\n"
+        << "        u32 rem = t;\n"
+        << "        W r[" << MAPC_NREG << "];\n"
+        << decode_tuple(pg, "        ")
+        << "        valid0_ = valid; tidv0_ = tidv; lbv0_ = lbv; bid0_ = r[" << MAPC_REG_BID << "];\n";
+      for (uint32_t l = 0; l < pg.n_levels; ++l) s << "        c0_[" << l << "] = r[" << MAPC_REG_K0 + l << "];\n";
+      s << "        (void)t;\n"
+        << "      }\n"
+        << "#pragma unroll 1\n"
+        << "      for (u32 u_ = 0; u_ < " << JU << "u; ++u_) {\n"
+        << "        const u32 tp = tq_ + u_ * " << L << "u; (void)tp;\n";
+    } else {
+      s << "#pragma unroll 1\n"
+        << "      for (int v = 0; v < " << V / G << "; ++v) {\n"
+        << "        const u32 tp = tl0 + v * " << G * T << "u + " << G << "u * me;\n";
+    }
+    s << "#pragma unroll\n"
       << "        for (int k = 0; k < " << NE << "; ++k) okP[k] = false;\n";
     // tuple t: remember each site's cell; tuple t + 1: one red.or.b64 when the
     // two cells are adjacent and aligned, else one red.or.b32 each
@@ -629,9 +754,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     // coordinate + 1 (tp is even): its coordinates are copied, not decoded, so
     // NVRTC shares every value of the program that does not depend on that
     // coordinate between the two tuples.
-    const bool nocarry = pg.inner_range % (uint64_t)G == 0;
-    const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
-    if (nocarry)
+    if (nocarry && !jam)
       s << "        bool valid0_; u32 tidv0_, lbv0_; W bid0_; W c0_[" << std::max(1u, pg.n_levels) << "];\n";
     // sites whose cell advances by exactly h from tuple 0 to tuple h (32-bit sort fields)
     std::vector<bool> us;
@@ -665,7 +788,7 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     for (int h = 0; h < G; ++h) {
       s << "        {\n"
         << "          const u32 t = tp + " << h << "u;\n";
-      if (h >= 1 && nocarry) {
+      if (jam || (h >= 1 && nocarry)) {
         s << "          const bool valid = valid0_;\n"
           << "          W r[" << MAPC_NREG << "];\n"
           << "          const u32 tidv = tidv0_" << (tid_is_inner ? " + " + std::to_string(h) + "u" : "") << ";\n"
@@ -673,7 +796,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
           << "          r[" << MAPC_REG_TID << "] = (W)tidv; r[" << MAPC_REG_BID << "] = bid0_;\n";
         for (uint32_t l = 0; l < pg.n_levels; ++l)
           s << "          r[" << MAPC_REG_K0 + l << "] = c0_[" << l << "]"
-            << (!tid_is_inner && l + 1 == pg.n_levels ? " + (W)" + std::to_string(h) : "") << ";\n";
+            << (!tid_is_inner && l + 1 == pg.n_levels && h ? " + (W)" + std::to_string(h) : "")
+            << (jam && l + 2 == pg.n_levels ? " + (W)u_" : "") << ";\n";
         s << "          (void)t;\n";
       } else {
         s << "          const bool valid = t < sg.n_tuples;\n"
@@ -713,18 +837,42 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
       s << "        if (okP[" << pr.first << "] && okP[" << pr.second << "] && sfP[" << pr.first << "] == sfP["
         << pr.second << "]) { accP[" << pr.first << "] |= accP[" << pr.second << "]; okP[" << pr.second
         << "] = false; }\n";
-    if (G == 4)          // one red.or.b64 over an aligned quad, else the run's cells one by one
-      s << "#pragma unroll\n"
-        << "        for (int k = 0; k < " << ne << "; ++k) {\n"
-        << "          if (!okP[k]) continue;\n"
-        << "          if ((sfP[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (sfP[k] >> 2), accP[k]); "
-           "continue; }\n"
+    // one red.or.b64 over an aligned quad, else the run's cells one by one
+    auto flush4 = [&](const std::string& ok, const std::string& sf, const std::string& acc) {
+      return "#pragma unroll\n"
+             "        for (int k = 0; k < " + std::to_string(ne) + "; ++k) {\n"
+             "          if (" + ok + "[k]) {\n"
+             "            if ((" + sf + "[k] & 3u) == 0) { atomicOr(reinterpret_cast<u64*>(keys) + (" + sf + "[k] >> 2), " +
+             acc + "[k]); } else {\n"
+             "#pragma unroll\n"
+             "              for (int j = 0; j < 4; ++j) {\n"
+             "                const u32 c_ = (u32)(" + acc + "[k] >> (16 * j)) & 0xFFFFu;\n"
+             "                if (c_) { const u32 sj_ = " + sf + "[k] + (u32)j; " + red1("sj_", "c_") + " }\n"
+             "              }\n"
+             "            }\n"
+             "          }\n"
+             "        }\n";
+    };
+    if (jam) {
+      // this row's quads absorb the previous row's quads on the same cells; the
+      // previous row's others are final (the next row is compared with this one)
+      const MapcSeg* g0 = nullptr;
+      for (const MapcSeg& g : ch.segs)
+        if (g.prog_begin == pg.prog_begin && !g0) g0 = &g;
+      for (const auto& pr : g0 ? jam_pairs(pg, *g0) : std::vector<std::pair<int, int>>{})
+        s << "        if (okP[" << pr.first << "] && okQ[" << pr.second << "] && sfP[" << pr.first << "] == sfQ["
+          << pr.second << "]) { accP[" << pr.first << "] |= accQ[" << pr.second << "]; okQ[" << pr.second
+          << "] = false; }\n";
+      s << flush4("okQ", "sfQ", "accQ")
         << "#pragma unroll\n"
-        << "          for (int j = 0; j < 4; ++j) {\n"
-        << "            const u32 c_ = (u32)(accP[k] >> (16 * j)) & 0xFFFFu;\n"
-        << "            if (c_) { const auto sj_ = sfP[k] + j; " << red1("sj_", "c_") << " }\n"
-        << "          }\n"
-        << "        }\n";
+        << "        for (int k = 0; k < " << NE << "; ++k) { okQ[k] = okP[k]; sfQ[k] = sfP[k]; accQ[k] = accP[k]; }\n"
+        << "      }\n"
+        << flush4("okQ", "sfQ", "accQ")
+        << "      break; }\n";
+      return;
+    }
+    if (G == 4)
+      s << flush4("okP", "sfP", "accP");
     else
       s << "#pragma unroll\n"
         << "        for (int k = 0; k < " << ne << "; ++k)\n"

@@ -1030,6 +1030,14 @@ void choose_tuple_order(GroupProg* g, uint64_t n_threads) {
 
 }  // namespace
 
+void eval_ops_sites(const std::vector<MapcOp>& ops, uint32_t n_levels, uint64_t tid, uint64_t bid, const uint64_t* k,
+                    std::vector<int64_t>* out) {
+  GroupProg g;
+  g.ops = ops;
+  g.n_levels = n_levels;
+  eval_sites(g, tid, bid, k, out);
+}
+
 Compiled compile_map(const std::string& text, const uint32_t grid[3], const uint32_t block[3],
                      const std::vector<std::string>& names, const std::vector<uint64_t>& values) {
   Compiled C;

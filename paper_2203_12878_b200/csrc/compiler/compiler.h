@@ -78,4 +78,10 @@ inline uint32_t bits_for(uint64_t max_value) {   // bits to hold 0..max_value
   return b;
 }
 
+// Host evaluation of a group program's access sites for one tuple (the VM's
+// semantics): the index of every EMIT whose guard holds, in site order, -1 where
+// it does not (the JIT's row-jam samples it to find sites one row apart).
+void eval_ops_sites(const std::vector<MapcOp>& ops, uint32_t n_levels, uint64_t tid, uint64_t bid, const uint64_t* k,
+                    std::vector<int64_t>* out);
+
 }  // namespace mapc

@@ -209,3 +209,50 @@ def to_text(prog: dict) -> str:
         parts.append("shared " + ", ".join(prog["arrays"]) + ";")
     parts.append(stmt_text(prog["body"], multi))
     return "\n".join(parts)
+
+
+def random_rows_instance(seed: int) -> Instance:
+    """A random two-loop MAP over rows r (second-innermost) and columns c
+    (innermost), sized so that the JIT's row-jam applies (blockDim * R * C a
+    multiple of 1024, C a multiple of 4 dividing or divisible by 512): sites read
+    or write row (tid * R + r + a) mod H (or a row shared by every thread, or a
+    row stride 2) at column c + b, some under a guard on r, c or tid.  Test input
+    only."""
+    r = random.Random(10_000 + seed)
+    nt = r.choice([8, 16, 32, 64])
+    R = r.choice([2, 4, 8])
+    C = r.choice([4, 8, 16, 64, 512, 1024])
+    while nt * R * C < 1024:
+        C *= 2
+    H = nt * R
+    sites = []
+    # a stencil-like family of rows (consecutive offsets: rows r + a, r + a + 1, ...
+    # are touched again by the next row) plus a few unrelated sites
+    fam = r.choice(["tid", "tid", "shared", "stride2"])
+    a0 = r.choice([0, H - 1, 1])
+    n_fam = r.randint(2, 4)
+    fam_arr, fam_half, fam_b = r.choice(["A", "A", "B"]), r.choice(["", f"{2 * H + 2} * C + "]), r.choice([0, 0, 1])
+    plan = [(a0 + i, fam, True) for i in range(n_fam)] + \
+        [(r.choice([0, 1, 2, H - 1]), r.choice(["tid", "shared", "stride2"]), False) for _ in range(r.randint(0, 2))]
+    r.shuffle(plan)
+    for a, f, in_fam in plan:
+        kind = r.choice(["rd", "rd", "wr"])
+        arr = fam_arr if in_fam else r.choice(["A", "A", "A", "B"])
+        b = fam_b if in_fam else r.choice([0, 0, 0, 1, 2, 4])
+        row = {"tid": f"((tid * R + r + {a}) % H)", "shared": f"(r + {a % 3})",
+               "stride2": f"(2 * (tid * R + r) + {a % 2})"}[f]
+        half = fam_half if in_fam else r.choice(["", "", f"{2 * H + 2} * C + "])
+        acc = f"{kind} {arr}[{half}{row} * C + c + {b}]"
+        g = r.random()
+        if g < 0.2:
+            acc = f"if (r % 2 = {r.randint(0, 1)}) {{ {acc} }} else {{ skip }}"
+        elif g < 0.3:
+            acc = f"if (tid < {r.randint(1, nt)}) {{ {acc} }} else {{ skip }}"
+        elif g < 0.35:
+            acc = f"if (c >= {r.randint(0, C)}) {{ {acc} }} else {{ skip }}"
+        sites.append(acc)
+    src = "params R, C, H; shared A, B;\nforU r in 0..R { forU c in 0..C { " + "; ".join(sites) + " } }"
+    if r.random() < 0.3:
+        src += ";\nsync;\nforU r in 0..R { forU c in 0..C { " + "; ".join(reversed(sites)) + " } }"
+    return Instance(f"rows{seed}", src, grid=(r.choice([1, 2]), 1, 1), block=(nt, 1, 1),
+                    params={"R": R, "C": C, "H": H})
