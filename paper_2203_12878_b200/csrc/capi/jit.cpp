@@ -584,6 +584,11 @@ uint32_t jam_rows(const JitChunk& ch) {
 
 }  // namespace
 
+bool jam_active(const JitChunk& ch, uint32_t cell_bytes) {
+  static const bool blocked_env = [] { const char* e = getenv("MAPC_BLOCKED_TILES"); return !(e && e[0] == '0'); }();
+  return cell_bytes == 2 && blocked_env && jam_rows(ch) != 0;
+}
+
 std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t mode, uint32_t cell_bytes) {
   static_assert(sizeof(MapcSeg) == 5 * 8 + 8 * 4 + 9 * 16, "Seg layout mirrored in the JIT prelude");
   if (mode == MAPC_MODE_UNIT || mode == MAPC_MODE_UNITF)

@@ -45,6 +45,8 @@ std::string module_source(const std::vector<JitChunk>& chunks, bool u32, uint32_
 int compile_cubin(const std::string& src, std::vector<char>* cubin, std::string* log);
 // Compile (or fetch from the process-wide cache) the kernels of the chunks with
 // want[i] != 0 for one mode; out->kernels has one entry per chunk (null = not built).
+// The direct-mode kernel of this chunk is row-jammed (jit.cpp jam_rows).
+bool jam_active(const JitChunk& ch, uint32_t cell_bytes);
 // Number of distinct specialised kernels the chunks need (chunks that differ only
 // in data the kernel does not bake share one; build_module compiles each once).
 size_t distinct_kernels(const std::vector<JitChunk>& chunks, bool u32);

@@ -987,8 +987,15 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // segment table resident).  The generate leaves room on every SM for the
   // side kernels' CTAs.  MAPC_OVERLAP=0 restores the sequential pipeline.
   static const int ovl_env = [] { const char* e = getenv("MAPC_OVERLAP"); return e ? atoi(e) : 1; }();
-  static const int ovl_gen_ctas = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 12; }();
-  static const int ovl_side_ctas = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 3; }();
+  // CTAs/SM of the generate and of the side stream's kernels: 8 / 4 when the
+  // generate is row-jammed (fewer, heavier threads; profiles/r2zd_overlap_sweep.jsonl),
+  // 12 / 3 otherwise (profiles/r2o_overlap_ctas_sweep.jsonl); the env overrides both
+  static const int ovl_gen_env = [] { const char* e = getenv("MAPC_OVL_GEN_CTAS"); return e ? atoi(e) : 0; }();
+  static const int ovl_side_env = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 0; }();
+  bool jammed = false;
+  for (size_t c : mine) jammed = jammed || mapj::jam_active(P.chunks[c].jit, P.chunks[c].cell_bytes);
+  const int ovl_gen_ctas = ovl_gen_env ? ovl_gen_env : jammed ? 8 : 12;
+  const int ovl_side_ctas = ovl_side_env ? ovl_side_env : jammed ? 4 : 3;
   const size_t tab_stride = align_up(P.dtab_bytes);
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&
