@@ -361,7 +361,7 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
     // padded to whole rows) -- column-wise sites (3a's transposed reads: lanes 16
     // words apart) spread over all 32 banks instead of 2; the scan zeroes each word
     // after reading it, so the table is cleared once per CTA, not per unit
-    s << "  __shared__ u32 tab[" << words_k1 << "];\n"
+    s << "  __shared__ __align__(16) u32 tab[" << words_k1 << "];\n"
       << "  const u32 crank_ = 0u; (void)crank_;\n"
       << "  unsigned long long racy = 0, best = ~0ull;\n"
       << "  for (u32 i = me; i < " << words_k1 << "u; i += " << T << "u) tab[i] = 0u;\n"
@@ -470,12 +470,25 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
   s << (K == 1 ? "    __syncthreads();\n" : "    cl_sync();\n")
     << "    const u64 base_ = ((((u64)lph << " << L.w_array << "u) << " << L.w_block << "u) | lb) << " << L.w_index
     << "u;\n"
-    << "    for (u32 il = me; il < " << (K == 1 ? words_k1 : wpc) << "u; il += " << T << "u) {\n"
-    << (K == 1 ? "      const u32 i = il ^ ((il >> 5) & 31u);   // the word's index in the unit table (unswizzled)\n"
-               : "      const u32 i = crank_ * " + std::to_string(wpc) + "u + il;      // the word's index in the unit table\n")
-    << "      const u32 w = tab[il];\n"
-    << (K == 1 ? "      tab[il] = 0u;\n" : "")
-    << (cell_bytes == 2 ? "      if (!racy16w(w)) continue;\n" : "      if (!w) continue;\n");
+    ;
+  const bool pairs = K == 1 && cell_bytes == 2;   // two words per 8-byte shared load (and clear)
+  if (pairs)
+    s << "    for (u32 il2 = me; il2 < " << words_k1 / 2 << "u; il2 += " << T << "u) {\n"
+      << "      const unsigned long long w2 = reinterpret_cast<unsigned long long*>(tab)[il2];\n"
+      << "      reinterpret_cast<unsigned long long*>(tab)[il2] = 0ull;\n"
+      << "      if (!(racy16w((u32)w2) | racy16w((u32)(w2 >> 32)))) continue;\n"
+      << "#pragma unroll\n"
+      << "      for (u32 p_ = 0; p_ < 2u; ++p_) {\n"
+      << "      const u32 il = 2u * il2 + p_;\n"
+      << "      const u32 i = il ^ ((il >> 5) & 31u);   // the word's index in the unit table (unswizzled)\n"
+      << "      const u32 w = (u32)(w2 >> (32u * p_));\n";
+  else
+    s << "    for (u32 il = me; il < " << (K == 1 ? words_k1 : wpc) << "u; il += " << T << "u) {\n"
+      << (K == 1 ? "      const u32 i = il ^ ((il >> 5) & 31u);   // the word's index in the unit table (unswizzled)\n"
+                 : "      const u32 i = crank_ * " + std::to_string(wpc) + "u + il;      // the word's index in the unit table\n")
+      << "      const u32 w = tab[il];\n"
+      << (K == 1 ? "      tab[il] = 0u;\n" : "")
+      << (cell_bytes == 2 ? "      if (!racy16w(w)) continue;\n" : "      if (!w) continue;\n");
   // cell c = (array, index) -> sort field base_ + (array << (wB + wI)) + index
   auto cell_sf = [&](const std::string& c) {
     return "(base_ + (((u64)(" + c + ") >> " + std::to_string(L.w_index) + "u) << " +
@@ -483,12 +496,14 @@ std::string unit_kernel_source(const JitChunk& ch, int index, bool u32, uint32_t
            std::to_string(L.w_index >= 32 ? 0xFFFFFFFFull : ((1ull << L.w_index) - 1)) + "ull))";
   };
   if (cell_bytes == 2) {
-    s << "#pragma unroll\n"
+    // racy16w's byte lanes 0-1 belong to the word's first cell, 2-3 to its second
+    s << "      const u32 rw_ = racy16w(w);\n"
+      << "#pragma unroll\n"
       << "      for (u32 h = 0; h < 2u; ++h) {\n"
-      << "        const u32 c = (w >> (16u * h)) & 0xFFFFu;\n"
-      << "        if (((c >> 14) & 1u) && (__popc(c & 0x7Fu) > 3 || __popc((c >> 7) & 0x7Fu) > 3)) {\n"
+      << "        if ((rw_ >> (16u * h)) & 0xFFFFu) {\n"
       << "          ++racy; const u64 sf = " << cell_sf("2u * i + h") << "; best = sf < best ? sf : best; }\n"
       << "      }\n";
+    if (pairs) s << "      }\n";   // p_
   } else {
     s << "      if (((w >> " << 2 * wt << "u) & 1u) && (w & (w >> " << wt << "u) & TMASK)) {\n"
       << "        ++racy; const u64 sf = " << cell_sf("i") << "; best = sf < best ? sf : best; }\n";

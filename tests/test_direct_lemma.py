@@ -114,3 +114,29 @@ def test_racy16_word_swar_exhaustive():
                         (c | (other << 16), racy16(c) or racy16(other)),
                         (other | (c << 16), racy16(c) or racy16(other))):
             assert (f(w) != 0) == want, hex(w)
+        # lane-exact: bytes 0-1 of the result belong to the low cell, 2-3 to the high
+        # one (the unit scan counts racy cells from the halves: jit.cpp racy16w)
+        for w in (c | (other << 16), other | (c << 16)):
+            r = f(w)
+            assert ((r & 0xFFFF) != 0) == racy16(w & 0xFFFF), hex(w)
+            assert ((r >> 16) != 0) == racy16(w >> 16), hex(w)
+
+
+def test_jit_prelude_racy16w_is_racy16_word():
+    """The NVRTC prelude's copy of the SWAR test (jit.cpp racy16w, used by the unit
+    scan) is the same function as direct.cu's racy16_word checked above: same
+    statements once the type names and the named kind-bit temporary are normalised."""
+    import os
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    a = open(os.path.join(root, "paper_2203_12878_b200", "csrc", "capi", "jit.cpp")).read()
+    b = open(os.path.join(root, "paper_2203_12878_b200", "csrc", "kernels", "direct.cu")).read()
+    fa = re.search(r"u32 racy16w\(u32 w\) \{(.*?)\n\}", a, re.S).group(1)
+    fb = re.search(r"uint32_t racy16_word\(uint32_t w\) \{(.*?)\n\}", b, re.S).group(1)
+
+    def norm(t):
+        t = re.sub(r"//[^\n]*", "", t).replace("uint32_t", "u32")
+        t = t.replace("const u32 k = (w >> 14) & 0x00010001u;", "").replace("(k * 0x7F7Fu)",
+                                                                           "(((w >> 14) & 0x00010001u) * 0x7F7Fu)")
+        return re.sub(r"\s+", "", t)
+    assert norm(fa) == norm(fb)
