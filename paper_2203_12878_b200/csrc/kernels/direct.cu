@@ -98,12 +98,23 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
         for (int j = 0; j < PER; ++j) hit |= cell_racy(c[j], wt);
       }
       if (hit) {
+        const unsigned long long base = (i0 + u * stride) * PER;
+        if constexpr (sizeof(C) == 2) {     // the SWAR lanes say which cell: bytes 0-1 low, 2-3 high
+          const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-        for (int j = 0; j < PER; ++j)
-          if (cell_racy(c[j], wt)) {
-            ++racy;
-            best = min(best, (i0 + u * stride) * PER + j);
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t r = racy16_word(wv[q]);
+            if (r & 0xFFFFu) { ++racy; best = min(best, base + 2 * q); }
+            if (r >> 16) { ++racy; best = min(best, base + 2 * q + 1); }
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < PER; ++j)
+            if (cell_racy(c[j], wt)) {
+              ++racy;
+              best = min(best, base + j);
+            }
+        }
       }
     }
   }
