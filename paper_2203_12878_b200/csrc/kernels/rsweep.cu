@@ -178,7 +178,6 @@ k_rsweep(unsigned long long* __restrict__ bufA, unsigned long long* __restrict__
   if (!ctrl->active[pass]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Sm& S = *reinterpret_cast<Sm*>(smem_raw);
-  const uint32_t G = gridDim.x;
   const uint32_t shift = pay_bits + 8 * pass;
   const uint32_t nxt = ctrl->next_active[pass];
   bool fuse_on = RED_NEXT && nxt < MAPC_MAX_PASSES && !ctrl->rt_bad[nxt];
