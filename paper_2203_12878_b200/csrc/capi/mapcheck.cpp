@@ -37,7 +37,7 @@ cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long 
                                  uint32_t cell_bytes, cudaStream_t s);
 cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm, cudaStream_t s);
 cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
-                                    MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s);
+                                    MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s, int unroll);
 cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
 cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t w_tid,
                                      unsigned long long cap, cudaStream_t s);
@@ -229,6 +229,8 @@ struct map_program {
   // stream) and its ordering events
   cudaStream_t side = nullptr;
   int side_dev = -1;
+  cudaStream_t side2 = nullptr;      // the table clears when three tables rotate (MAPC_TABLES=3)
+  int side2_dev = -1;
   std::vector<cudaEvent_t> sync_events;
   // CUDA graph of a whole run's launches, captured on the second identical call
   // (same plan, flags, scratch, stream, shard) and replayed after that
@@ -256,6 +258,7 @@ struct map_program {
     ResourcePool& P = pool();
     std::lock_guard<std::mutex> g(P.mu);
     if (side) P.streams.emplace_back(side_dev, side);
+    if (side2) P.streams.emplace_back(side2_dev, side2);
     if (cap) P.streams.emplace_back(cap_dev, cap);
   }
 };
@@ -997,29 +1000,50 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   const int ovl_gen_ctas = ovl_gen_env ? ovl_gen_env : jammed ? 8 : 12;
   const int ovl_side_ctas = ovl_side_env ? ovl_side_env : jammed ? 4 : 3;
   const size_t tab_stride = align_up(P.dtab_bytes);
+  // tables in rotation: 2 (chunk k's scan then its clear for chunk k+2, both on the
+  // side stream), or 3 (MAPC_TABLES=3: the clear of chunk k's table for chunk k+3 on
+  // a second side stream, concurrent with chunk k+1's scan)
+  // (default: 3 with the row-jammed generate, whose side stream is the critical path
+  // -- profiles/r2zl_tables2.jsonl: 5a 1632 -> 1689 G acc/s, clears at 2 CTAs/SM; 2 otherwise)
+  static const int tables_env = [] { const char* e = getenv("MAPC_TABLES"); return e ? atoi(e) : 0; }();
+  const int NT = (tables_env ? tables_env == 3 : jammed) && mine.size() >= 3 && 3 * tab_stride <= P.cap * 8 ? 3 : 2;
+  // with three tables: the scans 6 CTAs/SM at 4 vectors in flight per thread (95 -> fewer
+  // registers, so they co-reside with the generate's 8), the clears 3 CTAs/SM
+  // (profiles/r2zl_tables4.jsonl: 5a 1709 G acc/s; r2zl_tables3.jsonl)
+  static const int clear_ctas_env = [] { const char* e = getenv("MAPC_OVL_CLEAR_CTAS"); return e ? atoi(e) : 0; }();
+  static const int scan_unroll_env = [] { const char* e = getenv("MAPC_SCAN_UNROLL"); return e ? atoi(e) : 0; }();
+  const int ovl_clear_ctas = clear_ctas_env ? clear_ctas_env : NT == 3 ? 3 : ovl_side_ctas;
+  const int ovl_scan_ctas = ovl_side_env ? ovl_side_env : NT == 3 ? 6 : ovl_side_ctas;
+  const int ovl_scan_unroll = scan_unroll_env ? scan_unroll_env : NT == 3 ? 4 : 8;
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&
              2 * tab_stride <= P.cap * 8;
   for (size_t c : mine) ovl = ovl && use_direct(P.chunks[c], ex->flags) && !use_unit(P.chunks[c], ex->flags, gen_mode);
   if (ovl) {
-    if (!p->side || p->side_dev != ex->device) {
-      if (p->side) {
+    auto own_stream = [&](cudaStream_t* st, int* dev) -> cudaError_t {
+      if (*st && *dev == ex->device) return cudaSuccess;
+      if (*st) {
         std::lock_guard<std::mutex> g(pool().mu);
-        pool().streams.emplace_back(p->side_dev, p->side);
+        pool().streams.emplace_back(*dev, *st);
       }
-      p->side = nullptr;
-      CK(pool_stream(ex->device, &p->side));
-      p->side_dev = ex->device;
-    }
-    while (p->sync_events.size() < 5) {
+      *st = nullptr;
+      *dev = ex->device;
+      return pool_stream(ex->device, st);
+    };
+    CK(own_stream(&p->side, &p->side_dev));
+    if (NT == 3) CK(own_stream(&p->side2, &p->side2_dev));
+    while (p->sync_events.size() < 12) {
       cudaEvent_t e;
       CK(pool_event(ex->device, false, &e));
       p->sync_events.push_back(e);
     }
     cudaStream_t s2 = p->side;
-    cudaEvent_t ev_gen[2] = {p->sync_events[0], p->sync_events[1]};
+    cudaStream_t s3 = NT == 3 ? p->side2 : p->side;   // the clears
+    cudaEvent_t ev_gen[2] = {p->sync_events[0], p->sync_events[1]};       // per control block
     cudaEvent_t ev_done[2] = {p->sync_events[2], p->sync_events[3]};
-    cudaEvent_t ev_join = p->sync_events[4];
+    cudaEvent_t ev_scanned[3] = {p->sync_events[4], p->sync_events[5], p->sync_events[6]};   // per table
+    cudaEvent_t ev_cleared[3] = {p->sync_events[7], p->sync_events[8], p->sync_events[9]};
+    cudaEvent_t ev_join = p->sync_events[10], ev_join3 = p->sync_events[11];
     auto* ctrl2 = (MapcCtrl*)(base + P.off_ctrl2);
     for (size_t c : mine) {
       const Chunk& ch = P.chunks[c];
@@ -1027,27 +1051,29 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
                          cudaMemcpyHostToDevice, s));
       h2d += ch.segs.size() * sizeof(MapcSeg);
     }
-    CK(cudaEventRecord(ev_join, s));                  // the side stream starts after the gate reset and uploads
+    CK(cudaEventRecord(ev_join, s));                  // the side streams start after the gate reset and uploads
     CK(cudaStreamWaitEvent(s2, ev_join, 0));
-    // the second table's first clear runs on the side stream under chunk 0's generate
-    {
-      const Chunk& c1 = P.chunks[mine[1]];
-      size_t m = begin_on(MAP_K_CLEAR, s2);
-      CK(mapc_launch_table_clear(dtab + tab_stride, c1.cells * c1.cell_bytes, n_sms, ovl_side_ctas, s2));
-      end_on(m, s2);
-      CK(cudaEventRecord(ev_done[1], s2));
+    if (NT == 3) CK(cudaStreamWaitEvent(s3, ev_join, 0));
+    // the other tables' first clears run under chunk 0's generate
+    for (int t = 1; t < NT; ++t) {
+      const Chunk& ct = P.chunks[mine[t]];
+      size_t m = begin_on(MAP_K_CLEAR, s3);
+      CK(mapc_launch_table_clear(dtab + t * tab_stride, ct.cells * ct.cell_bytes, n_sms, ovl_clear_ctas, s3));
+      end_on(m, s3);
+      CK(cudaEventRecord(ev_cleared[t], s3));
     }
     for (size_t i = 0; i < mine.size(); ++i) {
       const size_t c = mine[i];
       NvtxRange nvtx_chunk("chunk " + std::to_string(c) + " direct (overlapped)");
       const Chunk& ch = P.chunks[c];
       const MapcLayout L = effective_layout(ch, ex->flags);
-      const int b = (int)(i & 1);
+      const int b = (int)(i & 1);                     // control block
+      const int t = (int)(i % NT);                    // table
       MapcCtrl* cb = b ? ctrl2 : ctrl;
-      unsigned char* tb = dtab + b * tab_stride;
+      unsigned char* tb = dtab + t * tab_stride;
       auto* sg = (MapcSeg*)(base + P.off_allsegs + ch.dev_segs);
       const uint64_t tbytes = ch.cells * ch.cell_bytes;
-      if (i >= 2) CK(cudaStreamWaitEvent(s, ev_done[b], 0));   // chunk i-2 released table b and ctrl b
+      if (i >= 2) CK(cudaStreamWaitEvent(s, ev_done[b], 0));   // chunk i-2 released control block b
       size_t m = begin(MAP_K_OTHER);
       CK(mapc_launch_chunk_init(cb, ch.dense_total, s));
       end(m);
@@ -1055,8 +1081,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         m = begin(MAP_K_CLEAR);
         CK(mapc_launch_table_clear(tb, tbytes, n_sms, 0, s));
         end(m);
+      } else {
+        CK(cudaStreamWaitEvent(s, ev_cleared[t], 0));   // table t cleared for this chunk
       }
-      if (i == 1) CK(cudaStreamWaitEvent(s, ev_done[1], 0));   // table 1 cleared on the side stream
       if (ch.total_tiles) {
         m = begin(MAP_K_DIRECT);
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, sg, (int)ch.segs.size(), ch.total_tiles,
@@ -1066,19 +1093,25 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       }
       CK(cudaEventRecord(ev_gen[b], s));
       CK(cudaStreamWaitEvent(s2, ev_gen[b], 0));
-      // scan, then clear table b when chunk i+2 uses it again (a scan that also
-      // zeroes the cells it read was measured 2.5x slower: profiles/r1k_*)
+      // scan, then clear table t when chunk i+NT uses it again (a scan that also
+      // zeroes the cells it read was measured 2.5x slower: profiles/r1k_*, r2ze_*)
       // the last chunk's scan has no generate to share the GPU with: full grid
       const bool last = i + 1 == mine.size();
       m = begin_on(MAP_K_DETECT, s2);
-      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_side_ctas, s2));
+      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_scan_ctas, s2,
+                                 last ? 8 : ovl_scan_unroll));
       end_on(m, s2);
-      if (i + 2 < mine.size()) {
-        // cleared for its next user, chunk i+2, whose table may be larger
-        const Chunk& nx = P.chunks[mine[i + 2]];
-        m = begin_on(MAP_K_CLEAR, s2);
-        CK(mapc_launch_table_clear(tb, nx.cells * nx.cell_bytes, n_sms, ovl_side_ctas, s2));
-        end_on(m, s2);
+      if (i + NT < mine.size()) {
+        // cleared for its next user, chunk i+NT, whose table may be larger
+        const Chunk& nx = P.chunks[mine[i + NT]];
+        if (NT == 3) {
+          CK(cudaEventRecord(ev_scanned[t], s2));
+          CK(cudaStreamWaitEvent(s3, ev_scanned[t], 0));
+        }
+        m = begin_on(MAP_K_CLEAR, s3);
+        CK(mapc_launch_table_clear(tb, nx.cells * nx.cell_bytes, n_sms, ovl_clear_ctas, s3));
+        end_on(m, s3);
+        CK(cudaEventRecord(ev_cleared[t], s3));
       }
       m = begin_on(MAP_K_OTHER, s2);
       launches += 2;
@@ -1095,8 +1128,12 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       end_on(m, s2);
       CK(cudaEventRecord(ev_done[b], s2));
     }
-    CK(cudaEventRecord(ev_join, s2));                 // join the side stream back into the caller's
+    CK(cudaEventRecord(ev_join, s2));                 // join the side streams back into the caller's
     CK(cudaStreamWaitEvent(s, ev_join, 0));
+    if (NT == 3) {
+      CK(cudaEventRecord(ev_join3, s3));
+      CK(cudaStreamWaitEvent(s, ev_join3, 0));
+    }
   }
   for (size_t c : mine) {
     if (ovl) break;
@@ -1151,7 +1188,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         end(m);
       }
       m = begin(MAP_K_DETECT);
-      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s));
+      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s, 8));
       end(m);
       m = begin(MAP_K_OTHER);
       launches += 2;

@@ -63,8 +63,7 @@ __host__ __device__ __forceinline__ uint32_t racy16_word(uint32_t w) {
 // Grid-stride over 16-byte vectors of cells, DS_UNROLL vectors in flight per
 // thread; each thread's first racy cell is its smallest (indices increase
 // along the stride).  The common all-clean vector costs a few ALU ops per cell.
-constexpr int DS_UNROLL = 8;
-template <typename C>
+template <typename C, int DS_UNROLL = 8>
 __global__ void __launch_bounds__(DS_THREADS)
 k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, MapcCtrl* __restrict__ ctrl) {
   constexpr int PER = 16 / sizeof(C);
@@ -212,15 +211,19 @@ extern "C" cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, 
   return cudaGetLastError();
 }
 
+// unroll: 16-B vectors in flight per thread, 8 (default) or 4 (fewer registers:
+// more scan CTAs fit next to the overlapped generate)
 extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes,
                                                uint32_t w_tid, MapcCtrl* ctrl, int n_sms, int ctas_per_sm,
-                                               cudaStream_t s) {
+                                               cudaStream_t s, int unroll) {
   if (cells == 0) return cudaSuccess;
   const unsigned long long vec = (cells * cell_bytes + 15) / 16;
-  const unsigned long long want = (vec + mapk::DS_THREADS * mapk::DS_UNROLL - 1) / (mapk::DS_THREADS * mapk::DS_UNROLL);
+  const unsigned long long want = (vec + mapk::DS_THREADS * 8 - 1) / (mapk::DS_THREADS * 8);
   const unsigned long long cap = (unsigned long long)n_sms * (ctas_per_sm > 0 ? ctas_per_sm : 16);
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  if (cell_bytes == 2)
+  if (cell_bytes == 2 && unroll == 4)
+    mapk::k_direct_scan<uint16_t, 4><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
+  else if (cell_bytes == 2)
     mapk::k_direct_scan<uint16_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint16_t*)tab, cells, w_tid, ctrl);
   else if (cell_bytes == 4)
     mapk::k_direct_scan<uint32_t><<<grid, mapk::DS_THREADS, 0, s>>>((const uint32_t*)tab, cells, w_tid, ctrl);
