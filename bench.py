@@ -595,7 +595,10 @@ def main():
             "pipeline_hbm": {"achieved": pipe_bytes / (ms_max / 1e3) / 1e9, "peak": peak,
                              "frac": pipe_bytes / (ms_max / 1e3) / 1e9 / peak if peak else None,
                              "note": "algorithmic bytes of every kernel of the timed steps / the steps' device time "
-                                     "(the direct pipeline overlaps the table scans with the next generate)"},
+                                     "(the direct pipeline overlaps the table scans with the next generate); over "
+                                     "compressible scratch (config.scratch) the cleared tables' zero lines compress, "
+                                     "so the physical DRAM traffic is lower than these bytes and frac can exceed 1 "
+                                     "(profiles/*_direct_ncu_full.txt: the generate's DRAM traffic per launch)"},
             "other_configs": others,
             "babycuda_executor": next2,
             "gpu_launches": launches,
