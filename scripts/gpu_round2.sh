@@ -1,4 +1,5 @@
 set -x
+bash scripts/box_info.sh > gpurun_out/${TAG:-r2}_box.txt 2>&1
 python -m pytest tests -m gpu -q > gpurun_out/${TAG:-r2}_gpu_tests.log 2>&1; echo tests_rc=$?; tail -3 gpurun_out/${TAG:-r2}_gpu_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG:-r2}_smoke.log 2>&1; echo smoke_rc=$?; tail -2 gpurun_out/${TAG:-r2}_smoke.log
 python bench.py > gpurun_out/${TAG:-r2}_bench.json 2> gpurun_out/${TAG:-r2}_bench.err; echo bench_rc=$?; cut -c1-400 gpurun_out/${TAG:-r2}_bench.json
