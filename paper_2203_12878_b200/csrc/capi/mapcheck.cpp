@@ -997,7 +997,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   static const int ovl_side_env = [] { const char* e = getenv("MAPC_OVL_SIDE_CTAS"); return e ? atoi(e) : 0; }();
   bool jammed = false;
   for (size_t c : mine) jammed = jammed || mapj::jam_active(P.chunks[c].jit, P.chunks[c].cell_bytes);
-  const int ovl_gen_ctas = ovl_gen_env ? ovl_gen_env : jammed ? 8 : 12;
+  int ovl_gen_ctas = ovl_gen_env ? ovl_gen_env : jammed ? 8 : 12;
   const int ovl_side_ctas = ovl_side_env ? ovl_side_env : jammed ? 4 : 3;
   const size_t tab_stride = align_up(P.dtab_bytes);
   // tables in rotation: 2 (chunk k's scan then its clear for chunk k+2, both on the
@@ -1007,13 +1007,15 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   // -- profiles/r2zl_tables2.jsonl: 5a 1632 -> 1689 G acc/s, clears at 2 CTAs/SM; 2 otherwise)
   static const int tables_env = [] { const char* e = getenv("MAPC_TABLES"); return e ? atoi(e) : 0; }();
   const int NT = (tables_env ? tables_env == 3 : jammed) && mine.size() >= 3 && 3 * tab_stride <= P.cap * 8 ? 3 : 2;
-  // with three tables: the scans 6 CTAs/SM at 4 vectors in flight per thread (95 -> fewer
-  // registers, so they co-reside with the generate's 8), the clears 3 CTAs/SM
-  // (profiles/r2zl_tables4.jsonl: 5a 1709 G acc/s; r2zl_tables3.jsonl)
+  // with three tables: the generate 10 CTAs/SM, the scans 6 at 4 vectors in flight per
+  // thread (fewer registers, so they co-reside with the generate), the clears 4
+  // (profiles/r2zl_tables4.jsonl, r2zo_tables6.jsonl: 5a 1718 G acc/s; r2zn_tables5.jsonl
+  // on a faster box: 1992)
   static const int clear_ctas_env = [] { const char* e = getenv("MAPC_OVL_CLEAR_CTAS"); return e ? atoi(e) : 0; }();
   static const int scan_unroll_env = [] { const char* e = getenv("MAPC_SCAN_UNROLL"); return e ? atoi(e) : 0; }();
-  const int ovl_clear_ctas = clear_ctas_env ? clear_ctas_env : NT == 3 ? 3 : ovl_side_ctas;
+  const int ovl_clear_ctas = clear_ctas_env ? clear_ctas_env : NT == 3 ? 4 : ovl_side_ctas;
   const int ovl_scan_ctas = ovl_side_env ? ovl_side_env : NT == 3 ? 6 : ovl_side_ctas;
+  if (NT == 3 && !ovl_gen_env) ovl_gen_ctas = 10;   // the jammed kernel's occupancy cap (profiles/r2zo_tables6.jsonl)
   const int ovl_scan_unroll = scan_unroll_env ? scan_unroll_env : NT == 3 ? 4 : 8;
   bool ovl = ovl_env != 0 && !(ex->flags & MAP_EXEC_SEQUENTIAL) && gen_mode == 1 && mine.size() >= 2 &&
              P.off_dtab == P.off_b &&
