@@ -299,13 +299,20 @@ def kernel_roofline(kern, cls, peak, peak_kind):
 
 
 def kernel_table(results):
+    """Per-class totals over the results.  With sampled timing (profile="sampled") only
+    some launches carry events: "ms" is then the timed launches' average duration times
+    every launch of the class (the estimate of the class's total), "timed" how many
+    launches were actually timed."""
     kern = {}
     for r in results:
         for k, v in (r.kernels or {}).items():
-            d = kern.setdefault(k, {"ms": 0.0, "launches": 0, "bytes": 0})
-            d["ms"] += v["ms"]
+            d = kern.setdefault(k, {"ms_timed": 0.0, "launches": 0, "bytes": 0, "timed": 0})
+            d["ms_timed"] += v["ms"]
             d["launches"] += v["launches"]
             d["bytes"] += v["bytes"]
+            d["timed"] += v.get("timed", v["launches"])
+    for d in kern.values():
+        d["ms"] = d["ms_timed"] / d["timed"] * d["launches"] if d["timed"] else 0.0
     return kern
 
 
@@ -389,7 +396,7 @@ def main():
     # identical call into a CUDA graph (per-launch timing events included, as
     # event-record nodes) and the timed steps replay it
     for _ in range(max(args.warmup, 0)):
-        step(profile="generate")
+        step(profile="sampled")
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
@@ -401,10 +408,12 @@ def main():
     e0.record(stream)
     results = []
     for _ in range(args.steps):
-        # CUDA events around the generate launches only (MAP_EXEC_PROFILE_GENERATE):
+        # CUDA events around the generate launches of every fourth chunk only
+        # (MAP_EXEC_PROFILE_GENERATE | MAP_EXEC_PROFILE_SAMPLED, 4 of 5a's 16 per step;
+        # profiles/r2zq_prof_overhead.json: events on all 16 cost 1.6% of the step):
         # the roofline's kernel is timed live inside the timed region; the other
-        # classes are counted here and timed in one extra step after it
-        results.append(step(profile="generate"))
+        # classes are counted here and timed in two extra steps after it
+        results.append(step(profile="sampled"))
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -464,7 +473,8 @@ def main():
                        "GB_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None,
                        "launches_per_step": v["launches"] / len(results),
                        "timed": "after the timed region (2 profiled steps)" if v.get("timed_after") else
-                                "live, inside the timed region"} for k, v in kern.items()}
+                                f"live, inside the timed region ({v['timed']} of {v['launches']} launches "
+                                f"carried events)"} for k, v in kern.items()}
 
     # e2e: the public API from host text to host verdict, every step (compile + H2D bytecode + D2H result)
     e2e = None

@@ -101,9 +101,11 @@ enum {
   MAP_K_COUNT = 10
 };
 typedef struct {
-  float ms[MAP_K_COUNT];
-  uint32_t launches[MAP_K_COUNT];
-  uint64_t bytes[MAP_K_COUNT];
+  float ms[MAP_K_COUNT];            /* summed over the timed launches                      */
+  uint32_t launches[MAP_K_COUNT];   /* every launch of the class                           */
+  uint64_t bytes[MAP_K_COUNT];      /* algorithmic bytes of every launch                   */
+  uint32_t timed[MAP_K_COUNT];      /* launches that carried timing events (ms / timed =   */
+                                    /* the average launch duration)                        */
 } map_kernel_stats;
 
 /* Execution resources borrowed from the caller. */
@@ -177,6 +179,10 @@ typedef struct {
  * the other classes are counted (launches, bytes) but not timed (ms = 0), so
  * the timing events perturb the run less (one event pair per chunk). */
 #define MAP_EXEC_PROFILE_GENERATE 0x200u
+/* MAP_EXEC_PROFILE_SAMPLED (with MAP_EXEC_PROFILE_GENERATE): time only the generate
+ * launches of every fourth chunk of the run (positions 2, 6, 10, ...: past the
+ * pipeline's fill), so the timing perturbs the run least; `timed` counts them. */
+#define MAP_EXEC_PROFILE_SAMPLED 0x400u
 
 typedef struct {
   int32_t verdict;            /* 0 = DRF, 1 = RACY (over the chunks this call ran)   */

@@ -54,7 +54,8 @@ _NK = len(KERNEL_CLASSES)
 
 
 class _Stats(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_float * _NK), ("launches", ctypes.c_uint32 * _NK), ("bytes", ctypes.c_uint64 * _NK)]
+    _fields_ = [("ms", ctypes.c_float * _NK), ("launches", ctypes.c_uint32 * _NK), ("bytes", ctypes.c_uint64 * _NK),
+                ("timed", ctypes.c_uint32 * _NK)]
 
 
 class _Exec(ctypes.Structure):
@@ -67,6 +68,7 @@ GEN_PATHS = {"auto": 0, "vm": 1, "jit": 2}
 DETECT_PATHS = {"auto": 0x00, "sort": 0x10, "table": 0x20, "direct": 0x40, "unit": 0x80}   # MAP_DETECT_* (mapcheck.h)
 EXEC_SEQUENTIAL = 0x100                                                       # MAP_EXEC_SEQUENTIAL
 EXEC_PROFILE_GENERATE = 0x200                                                 # MAP_EXEC_PROFILE_GENERATE
+EXEC_PROFILE_SAMPLED = 0x400                                                  # MAP_EXEC_PROFILE_SAMPLED
 
 
 class _Result(ctypes.Structure):
@@ -384,7 +386,8 @@ class MapProgram:
                     chunk_max_accesses 0 the plan uses default_chunk(world));
         profile: record CUDA events around every launch and return per-kernel-class timings
                  (True), or around the generate launches only ("generate": the other classes are
-                 counted, not timed; MAP_EXEC_PROFILE_GENERATE);
+                 counted, not timed; MAP_EXEC_PROFILE_GENERATE), or around every fourth chunk's
+                 generate ("sampled": MAP_EXEC_PROFILE_SAMPLED); kernels[k]["timed"] counts them;
         gen: generate path, "auto" | "vm" (bytecode interpreter) | "jit" (NVRTC-specialised);
         detect: "auto" | "direct" | "table" | "sort" (include/mapcheck.h MAP_DETECT_*);
         overlap: False = MAP_EXEC_SEQUENTIAL (the direct path's chunks one after another)."""
@@ -404,7 +407,8 @@ class MapProgram:
                    scratch.numel() * scratch.element_size(), int(chunk_max_accesses), int(rank), int(world),
                    ctypes.pointer(stats) if stats is not None else None,
                    GEN_PATHS[gen] | DETECT_PATHS[detect] | (0 if overlap else EXEC_SEQUENTIAL) |
-                   (EXEC_PROFILE_GENERATE if profile == "generate" else 0))
+                   (EXEC_PROFILE_GENERATE if profile in ("generate", "sampled") else 0) |
+                   (EXEC_PROFILE_SAMPLED if profile == "sampled" else 0))
         r = _Result()
         st = _lib.map_check_races(self._h, ctypes.byref(ex), ctypes.byref(r))
         if st != 0:
@@ -417,8 +421,8 @@ class MapProgram:
                 res.witness = Witness(w.phase, w.array, w.block, w.index, w.tid_lo, w.tid_hi, w.kind_lo, w.kind_hi,
                                       w.array_name.decode())
         if stats is not None:
-            res.kernels = {k: {"ms": stats.ms[i], "launches": stats.launches[i], "bytes": stats.bytes[i]}
-                           for i, k in enumerate(KERNEL_CLASSES)}
+            res.kernels = {k: {"ms": stats.ms[i], "launches": stats.launches[i], "bytes": stats.bytes[i],
+                               "timed": stats.timed[i]} for i, k in enumerate(KERNEL_CLASSES)}
         return res
 
 

@@ -949,14 +949,18 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     cudaEventRecordWithFlags(p->events[e], st, capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
   };
   const bool gen_only = (ex->flags & MAP_EXEC_PROFILE_GENERATE) != 0;
+  const bool sampled = gen_only && (ex->flags & MAP_EXEC_PROFILE_SAMPLED) != 0;
+  size_t chunk_pos = 0;                              // position of the chunk being enqueued (sampling)
   auto timed = [&](int kind) {
-    return prof && (!gen_only || kind == MAP_K_GENERATE || kind == MAP_K_DIRECT || kind == MAP_K_UNIT);
+    return prof && (!gen_only || kind == MAP_K_GENERATE || kind == MAP_K_DIRECT || kind == MAP_K_UNIT) &&
+           (!sampled || chunk_pos % 4 == 2);
   };
   auto begin = [&](int kind) -> size_t {
     ++launches;
     st_acc.launches[kind]++;
     if (!timed(kind)) return 0;
     rec(ev, rec_s);
+    st_acc.timed[kind]++;
     marks.push_back({kind, ev, ev + 1});
     ev += 2;
     return ev - 1;
@@ -969,6 +973,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     st_acc.launches[kind]++;
     if (!timed(kind)) return 0;
     rec(ev, st);
+    st_acc.timed[kind]++;
     marks.push_back({kind, ev, ev + 1});
     ev += 2;
     return ev - 1;
@@ -1066,6 +1071,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     }
     for (size_t i = 0; i < mine.size(); ++i) {
       const size_t c = mine[i];
+      chunk_pos = i;
       NvtxRange nvtx_chunk("chunk " + std::to_string(c) + " direct (overlapped)");
       const Chunk& ch = P.chunks[c];
       const MapcLayout L = effective_layout(ch, ex->flags);
@@ -1137,8 +1143,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       CK(cudaStreamWaitEvent(s, ev_join3, 0));
     }
   }
+  size_t seq_pos = 0;
   for (size_t c : mine) {
     if (ovl) break;
+    chunk_pos = seq_pos++;
     const Chunk& ch = P.chunks[c];
     NvtxRange nvtx_chunk("chunk " + std::to_string(c) +
                          (use_unit(ch, ex->flags, gen_mode) ? " unit" : use_direct(ch, ex->flags) ? " direct" : " keys"));

@@ -284,3 +284,23 @@ def test_profiled_runs_replay_as_graphs():
                 assert v["ms"] > 0, (k, v)
     plain = [p.check_races(gen="jit").device_ms for _ in range(3)]
     assert min(r.device_ms for r in runs[2:]) < 3 * min(plain) + 0.05
+
+
+def test_sampled_generate_timing():
+    """profile="sampled" (MAP_EXEC_PROFILE_GENERATE | MAP_EXEC_PROFILE_SAMPLED): every
+    launch counted, only the generates of chunk positions 2, 6, 10, ... timed, in the
+    eager, capturing and replaying calls alike; results unchanged."""
+    inst = config("5b", T=12, R=32, C=256)
+    o = _want(oracle.check_instance(inst))
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    n = p.n_chunks()
+    assert n >= 6
+    want_timed = len([i for i in range(n) if i % 4 == 2])
+    full = p.check_races(profile=True, gen="jit").kernels["direct"]
+    for _ in range(4):
+        r = p.check_races(profile="sampled", gen="jit")
+        assert _got(r) == o
+        k = r.kernels["direct"]
+        assert k["launches"] == full["launches"] == n
+        assert k["timed"] == want_timed and k["ms"] > 0
+        assert r.kernels["detect"]["timed"] == 0 and r.kernels["detect"]["ms"] == 0
