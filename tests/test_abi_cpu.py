@@ -248,3 +248,8 @@ def test_python_flag_constants_match_header():
         assert mc.DETECT_PATHS[k] == val("MAP_DETECT_" + k.upper())
     assert mc.EXEC_SEQUENTIAL == val("MAP_EXEC_SEQUENTIAL")
     assert mc.EXEC_PROFILE_GENERATE == val("MAP_EXEC_PROFILE_GENERATE")
+    assert mc.EXEC_PROFILE_SAMPLED == val("MAP_EXEC_PROFILE_SAMPLED")
+    # map_kernel_stats mirrored field by field (ms, launches, bytes, timed)
+    import ctypes
+    assert [f for f, _ in mc._Stats._fields_] == ["ms", "launches", "bytes", "timed"]
+    assert ctypes.sizeof(mc._Stats) == 10 * (4 + 4 + 8 + 4)
