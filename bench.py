@@ -215,8 +215,9 @@ def ncu_traffic(which):
 ROOFLINE_MODELS = {
     "direct": ("generate fused with the direct-address table reductions (gen_0, mode direct)", "direct",
                "2 x table bytes per launch: every cell of the 2^S-cell table read and written once "
-               "(the per-access red.or are served by L2); bound by the rate of global red.or.b64 into the "
-               "HBM-resident table (profiles/r1h_red_width_microbench.txt); the issue view is under alu. "
+               "(the reductions are served by L2; row-jammed, 0.133 red.or.b64 per 5a access, see red); "
+               "bound by the L2's rate of atomic updates into the HBM-resident table "
+               "(profiles/r1h_red_width_microbench.txt); the issue view is under alu. "
                "Over compressible scratch (config.scratch) the zero-filled lines the reductions fill "
                "compress, so the measured DRAM traffic (traffic) is below these algorithmic bytes"),
     "onesweep": ("k_rsweep (static-range LSD radix pass)", "rsweep", "16 B per key per active pass (8 read + 8 write)"),
