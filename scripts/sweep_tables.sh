@@ -1,5 +1,5 @@
-# 5a with three tables in rotation (the default with the row-jammed generate): generate / clear CTAs
+# 5a with three tables in rotation: scan depth x scan CTAs
 bash scripts/box_info.sh | tail -1
-for rep in 1 2; do for g in 8 10; do for cl in 3 4; do
-  MAPC_OVL_GEN_CTAS=$g MAPC_OVL_SIDE_CTAS=6 MAPC_OVL_CLEAR_CTAS=$cl timeout 300 python scripts/probe_direct5a.py 2>&1 | grep '^{'
-done; done; done
+for un in 2 4; do for sd in 6 8 10; do
+  MAPC_SCAN_UNROLL=$un MAPC_OVL_SIDE_CTAS=$sd timeout 300 python scripts/probe_direct5a.py 2>&1 | grep '^{'
+done; done
