@@ -1,5 +1,5 @@
-# 5a with three tables in rotation: scan depth x scan CTAs
+# 5a, three tables: register cap of the generate (MAPC_JIT_MINB) x its CTAs per SM
 bash scripts/box_info.sh | tail -1
-for un in 2 4; do for sd in 6 8 10; do
-  MAPC_SCAN_UNROLL=$un MAPC_OVL_SIDE_CTAS=$sd timeout 300 python scripts/probe_direct5a.py 2>&1 | grep '^{'
+for mb in 10 12 16; do for g in 10 12 14; do
+  MAPC_JIT_MINB=$mb MAPC_OVL_GEN_CTAS=$g timeout 300 python scripts/probe_direct5a.py 2>&1 | grep '^{'
 done; done
