@@ -252,6 +252,7 @@ std::string chunk_key(const JitChunk& ch, bool u32, uint32_t mode, uint32_t cell
   }
   put(k, ch.segs.size());
   k.append(reinterpret_cast<const char*>(ch.segs.data()), ch.segs.size() * sizeof(MapcSeg));
+  put(k, ch.comp);
   if (mode == MAPC_MODE_UNIT || mode == MAPC_MODE_UNITF) {
     put(k, ch.unit_cluster);
     put(k, ch.unit_threads);
@@ -637,7 +638,8 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
   if (minb > 0) s << ", " << minb;
   s << ") gen_" << index
     << "(const Seg* __restrict__ segs, int n_segs, u64 total_tiles, u64* __restrict__ keys, u64* n_ctr, u32* err_flag, "
-       "u64 cap, const u64* target_ptr) {\n"
+       "u64 cap, const u64* target_ptr, const u64* __restrict__ pcomp_) {\n"
+    << "  (void)pcomp_;\n"
     << "  typedef " << (u32 ? "u32" : "u64") << " W;\n"
     << "  typedef " << (cell_bytes == 4 ? "u32" : "u64") << " CELL;\n"
     << "  const u32 WI = " << ch.lay.w_index << "u, WB_ = " << ch.lay.w_block << "u, PAY = " << ch.lay.pay_bits << "u;\n"
@@ -703,11 +705,17 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     int ne = 0;
     for (const MapcOp& op : pg.ops) ne += (op.code & MAPC_CODE_MASK) == VM_EMIT;
     const int NE = std::max(ne, 1);
+    // stride-compressed table (ch.comp, 16-bit cells, 32-bit cell indices): the
+    // phase's block at cbase_, one cell per 2^csh_ indices of residue cres_
+    const bool comp = ch.comp && cell_bytes == 2 && sf32 && mode == MAPC_MODE_DIRECT;
     const std::string cell =
         "u64 idx_ = (u64)(IX) - IDX_LO; if (WI < 64 && (idx_ >> WI) != 0) { err |= " +
         std::to_string(MAPC_ERR_LAYOUT) + "u; idx_ = 0; } " +
-        (sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
-              : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
+        (comp ? std::string("const u32 sf_ = cbase_ + ((((u32)(ARR) << WB_) | lbv) << (WI - csh_)) + "
+                            "(((u32)idx_ - cres_) >> csh_); if (((u32)idx_ - cres_) & ((1u << csh_) - 1u)) err |= ") +
+                    std::to_string(MAPC_ERR_LAYOUT) + "u; "
+         : sf32 ? std::string("const u32 sf_ = (u32)sg.key_hi + ((u32)(ARR) << (WB_ + WI)) + (lbv << WI) + (u32)idx_; ")
+                : std::string("const u64 sf_ = sg.key_hi + ((ARR) << (WB_ + WI)) + ((u64)lbv << WI) + idx_; ")) +
         (cell_bytes == 2 ? std::string("const u32 cd_ = tcd_ | ((u32)(KIND) << 14); ")
                          : "const u32 cd_ = tidv | ((~tidv & (u32)TMASK) << " + std::to_string(ch.lay.w_tid) +
                                "u) | ((u32)(KIND) << " + std::to_string(2 * ch.lay.w_tid) + "u); ") +
@@ -737,6 +745,10 @@ std::string chunk_kernel_source(const JitChunk& ch, int index, bool u32, uint32_
     const bool nocarry = pg.inner_range % (uint64_t)G == 0;
     const bool tid_is_inner = pg.tid_inner || pg.n_levels == 0;
     s << "    case " << pg.prog_begin << "u: {\n";
+    if (comp)
+      s << "      const u32 lphc_ = (u32)(sg.key_hi >> (WA_ + WB_ + WI));\n"
+        << "      const u32 cbase_ = (u32)pcomp_[2 * lphc_];\n"
+        << "      const u32 csh_ = (u32)(pcomp_[2 * lphc_ + 1] & 255ull), cres_ = (u32)(pcomp_[2 * lphc_ + 1] >> 8);\n";
     if (jam) {
       s << "      const u32 sl_ = (u32)((tile - sg.tile_begin) / " << JU << "u);\n";
       if (L <= 512)   // P = 512 / L rows per tile, L / 4 threads per row
@@ -1159,7 +1171,7 @@ cudaError_t launch_unit_filter(const JitHandle& h, size_t chunk, const unsigned 
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         int n_sms, int max_ctas_per_sm, cudaStream_t s) {
+                         int n_sms, int max_ctas_per_sm, cudaStream_t s, const unsigned long long* pcomp) {
   if (total_tiles == 0) return cudaSuccess;
   const void* fn = (const void*)h.kernels[chunk];
   int occ = 1;
@@ -1169,7 +1181,7 @@ cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, 
   const unsigned long long capb = (unsigned long long)n_sms * occ;
   const int grid = (int)(total_tiles < capb ? total_tiles : capb);
   void* args[] = {(void*)&segs, (void*)&n_segs, (void*)&total_tiles, (void*)&keys, (void*)&n_ctr, (void*)&err_flag,
-                  (void*)&cap, (void*)&target};
+                  (void*)&cap, (void*)&target, (void*)&pcomp};
   return cudaLaunchKernel(fn, dim3(grid), dim3(MAPC_GEN_THREADS), args, 0, s);
 }
 

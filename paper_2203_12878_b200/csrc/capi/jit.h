@@ -31,6 +31,7 @@ struct JitChunk {
   uint32_t unit_cluster = 1;      // CTAs per unit: 1 = the unit's table in one CTA's shared memory,
                                   // K > 1 = spread over a K-CTA cluster (distributed shared memory)
   uint32_t unit_threads = 128;    // threads per CTA of the unit kernel
+  bool comp = false;              // direct mode: stride-compressed table (pcomp, mapcheck.cpp Chunk)
 };
 
 struct JitHandle {
@@ -55,7 +56,7 @@ int build_module(const std::vector<JitChunk>& chunks, bool u32, uint32_t mode, c
 cudaError_t launch_chunk(const JitHandle& h, size_t chunk, const MapcSeg* segs, int n_segs,
                          unsigned long long total_tiles, unsigned long long* keys, unsigned long long* n_ctr,
                          unsigned int* err_flag, unsigned long long cap, const unsigned long long* target,
-                         int n_sms, int max_ctas_per_sm, cudaStream_t s);
+                         int n_sms, int max_ctas_per_sm, cudaStream_t s, const unsigned long long* pcomp = nullptr);
 // Unit mode (MAPC_MODE_UNIT): n_units (phase, block) units of the chunk, one CTA
 // each at a time; counts into n_ctr (guarded accesses), racy, racy_sf (atomicMin).
 // cluster = CTAs per unit (thread-block cluster, DSMEM table when > 1), threads per

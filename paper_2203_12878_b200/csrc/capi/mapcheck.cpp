@@ -36,6 +36,8 @@ cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long 
                                  uint32_t max_emits, uint32_t force_compact, uint32_t mode, void* tab,
                                  uint32_t cell_bytes, cudaStream_t s);
 cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm, cudaStream_t s);
+cudaError_t mapc_launch_comp_to_sf(MapcCtrl* ctrl, const unsigned long long* pcomp, uint32_t nph, uint32_t wa,
+                                   uint32_t wb, uint32_t wi, cudaStream_t s);
 cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
                                     MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s, int unroll);
 cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
@@ -109,6 +111,13 @@ struct Chunk {
   bool unit_ok = false;                     // per-(phase, block) tables fit shared memory (MAPC_MODE_UNIT)
   size_t unit_smem = 0;                     // dynamic shared bytes per CTA of a cluster unit
   size_t dev_segs = 0;                      // offset of this chunk's segment table in the all-chunks region
+  // stride-compressed direct table (JIT direct mode, 16-bit cells): every site of local
+  // phase q has index - idx_lo == res[q] (mod 2^sh[q]), so the phase's block keeps one
+  // cell per 2^sh[q] indices; pcomp = per q {base, sh | res << 8} (device copy follows
+  // the segment table); comp_cells = the compressed table's cells
+  bool comp_ok = false;
+  uint64_t comp_cells = 0;
+  std::vector<unsigned long long> pcomp;
 };
 
 struct Plan {
@@ -130,6 +139,14 @@ struct Plan {
 };
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// a chunk's segment table, then its stride-compression table (Chunk::pcomp): staged
+// and uploaded together
+size_t pcomp_off(const Chunk& ch) { return align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg), 64); }
+size_t seg_blob(const Chunk& ch) { return pcomp_off(ch) + ch.pcomp.size() * sizeof(unsigned long long); }
+// the direct table of a chunk: stride-compressed with the specialised generate
+bool comp_on(const Chunk& ch, int gen_mode) { return ch.comp_ok && ch.cell_bytes == 2 && gen_mode == 1; }
+uint64_t dcells(const Chunk& ch, int gen_mode) { return comp_on(ch, gen_mode) ? ch.comp_cells : ch.cells; }
 
 // NVTX range for the host-side stages (visible in nsys / ncu timelines)
 struct NvtxRange {
@@ -380,6 +397,47 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
       }
     }
   }
+  // stride compression of the direct table: per local phase, the largest 2^k such
+  // that every site's (index - idx_lo) has the same residue modulo 2^k (the compiler's
+  // known low bits, GroupProg::site_kb/kv)
+  {
+    const uint32_t nph = ch.phase_hi - ch.phase_lo + 1;
+    const uint32_t WI = L.w_index, WAB = L.w_array + L.w_block;
+    std::vector<int> k(nph, -1);                 // -1: no site yet
+    std::vector<uint64_t> r(nph, 0);
+    for (size_t i = i0; i < i1; ++i)
+      for (size_t ii : ph[i].inst) {
+        const mapc::InstanceInfo& in = C.inst[ii];
+        const uint32_t q = in.phase - ch.phase_lo;
+        for (const mapc::GroupProg& g : in.groups)
+          for (size_t e = 0; e < g.site_kb.size(); ++e) {
+            uint32_t kb = std::min<uint32_t>(g.site_kb[e], WI);
+            const uint64_t rv = (g.site_kv[e] - L.idx_lo) & (kb >= 64 ? ~0ull : ((1ull << kb) - 1));
+            if (k[q] < 0) {
+              k[q] = (int)kb;
+              r[q] = rv;
+            } else {
+              kb = std::min<uint32_t>(kb, (uint32_t)k[q]);
+              const uint64_t diff = (rv ^ r[q]) & ((1ull << kb) - 1);
+              if (diff) kb = std::min<uint32_t>(kb, (uint32_t)__builtin_ctzll(diff));
+              k[q] = (int)kb;
+              r[q] &= (1ull << kb) - 1;
+            }
+          }
+      }
+    uint64_t cells = 0;
+    ch.pcomp.assign(2 * (size_t)nph, 0);
+    for (uint32_t q = 0; q < nph; ++q) {
+      const uint32_t sh = k[q] < 0 ? WI : (uint32_t)k[q];
+      ch.pcomp[2 * q] = cells;
+      ch.pcomp[2 * q + 1] = (unsigned long long)sh | (r[q] << 8);
+      cells += (1ull << WAB) << (WI - sh);
+    }
+    ch.comp_cells = cells;
+    // worth it when the table shrinks at least 2x; 32-bit cell indices, <= 64 phases
+    ch.comp_ok = L.sort_bits <= 31 && nph <= 64 && cells * 2 <= (1ull << L.sort_bits);
+    ch.jit.comp = ch.comp_ok;
+  }
   *out = std::move(ch);
 }
 
@@ -467,7 +525,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
     ch.stage_ops = stage;
     stage += align_up(std::max<size_t>(1, ch.ops.size()) * sizeof(MapcOp), 64);
     ch.stage_segs = stage;
-    stage += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg), 64);
+    stage += align_up(seg_blob(ch), 64);
   }
   size_t dtab = 0;
   for (auto& ch : out.chunks) {
@@ -534,7 +592,11 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_lb = off; off += align_up(out.lb_bytes);
   out.off_ff = off; off += align_up(det_tiles * sizeof(MapcSegState));
   out.off_lf = off; off += align_up(det_tiles * sizeof(MapcSegState));
-  out.off_segs = off; off += align_up(std::max<size_t>(1, out.max_segs) * sizeof(MapcSeg));
+  {
+    size_t blob = 0;
+    for (auto& ch : out.chunks) blob = std::max(blob, seg_blob(ch));
+    out.off_segs = off; off += align_up(blob);
+  }
   out.off_ctrl = off; off += align_up(sizeof(MapcCtrl));
   out.off_res = off; off += align_up(std::max<size_t>(1, out.chunks.size()) * sizeof(MapcChunkResult));
   out.rh_bytes = (size_t)MAPC_MAX_PASSES * MAPC_MAX_RANGES * MAPC_RADIX * 4;
@@ -548,7 +610,7 @@ map_status make_plan(const mapc::Compiled& C, uint64_t cap, Plan* P, std::string
   out.off_allsegs = off;
   for (auto& ch : out.chunks) {
     ch.dev_segs = off - out.off_allsegs;
-    off += align_up(std::max<size_t>(1, ch.segs.size()) * sizeof(MapcSeg));
+    off += align_up(seg_blob(ch));
   }
   out.dtab_bytes = dtab;
   if (dtab <= kcap * 8) {
@@ -836,6 +898,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
   for (auto& ch : P.chunks) {
     if (!ch.ops.empty()) std::memcpy(stage + ch.stage_ops, ch.ops.data(), ch.ops.size() * sizeof(MapcOp));
     if (!ch.segs.empty()) std::memcpy(stage + ch.stage_segs, ch.segs.data(), ch.segs.size() * sizeof(MapcSeg));
+    if (!ch.pcomp.empty())
+      std::memcpy(stage + ch.stage_segs + pcomp_off(ch), ch.pcomp.data(), ch.pcomp.size() * sizeof(unsigned long long));
   }
   MapcChunkResult* host_res = (MapcChunkResult*)(stage + P.stage_bytes -
                                                  align_up(std::max<size_t>(1, P.chunks.size()) * sizeof(MapcChunkResult), 64));
@@ -1054,9 +1118,9 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     auto* ctrl2 = (MapcCtrl*)(base + P.off_ctrl2);
     for (size_t c : mine) {
       const Chunk& ch = P.chunks[c];
-      CK(cudaMemcpyAsync(base + P.off_allsegs + ch.dev_segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg),
+      CK(cudaMemcpyAsync(base + P.off_allsegs + ch.dev_segs, stage + ch.stage_segs, seg_blob(ch),
                          cudaMemcpyHostToDevice, s));
-      h2d += ch.segs.size() * sizeof(MapcSeg);
+      h2d += seg_blob(ch);
     }
     CK(cudaEventRecord(ev_join, s));                  // the side streams start after the gate reset and uploads
     CK(cudaStreamWaitEvent(s2, ev_join, 0));
@@ -1065,7 +1129,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     for (int t = 1; t < NT; ++t) {
       const Chunk& ct = P.chunks[mine[t]];
       size_t m = begin_on(MAP_K_CLEAR, s3);
-      CK(mapc_launch_table_clear(dtab + t * tab_stride, ct.cells * ct.cell_bytes, n_sms, ovl_clear_ctas, s3));
+      CK(mapc_launch_table_clear(dtab + t * tab_stride, dcells(ct, gen_mode) * ct.cell_bytes, n_sms, ovl_clear_ctas, s3));
       end_on(m, s3);
       CK(cudaEventRecord(ev_cleared[t], s3));
     }
@@ -1080,7 +1144,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       MapcCtrl* cb = b ? ctrl2 : ctrl;
       unsigned char* tb = dtab + t * tab_stride;
       auto* sg = (MapcSeg*)(base + P.off_allsegs + ch.dev_segs);
-      const uint64_t tbytes = ch.cells * ch.cell_bytes;
+      const uint64_t tbytes = dcells(ch, gen_mode) * ch.cell_bytes;
+      const auto* pc = comp_on(ch, gen_mode)
+                           ? reinterpret_cast<const unsigned long long*>(reinterpret_cast<unsigned char*>(sg) + pcomp_off(ch))
+                           : nullptr;
       if (i >= 2) CK(cudaStreamWaitEvent(s, ev_done[b], 0));   // chunk i-2 released control block b
       size_t m = begin(MAP_K_OTHER);
       CK(mapc_launch_chunk_init(cb, ch.dense_total, s));
@@ -1096,7 +1163,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         m = begin(MAP_K_DIRECT);
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, sg, (int)ch.segs.size(), ch.total_tiles,
                               (unsigned long long*)tb, &cb->n, &cb->err, L.cap, &cb->wit_sf, n_sms,
-                              ovl_gen_ctas, s));
+                              ovl_gen_ctas, s, pc));
         end(m);
       }
       CK(cudaEventRecord(ev_gen[b], s));
@@ -1106,9 +1173,14 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       // the last chunk's scan has no generate to share the GPU with: full grid
       const bool last = i + 1 == mine.size();
       m = begin_on(MAP_K_DETECT, s2);
-      CK(mapc_launch_direct_scan(tb, ch.cells, ch.cell_bytes, L.w_tid, cb, n_sms, last ? 0 : ovl_scan_ctas, s2,
-                                 last ? 8 : ovl_scan_unroll));
+      CK(mapc_launch_direct_scan(tb, dcells(ch, gen_mode), ch.cell_bytes, L.w_tid, cb, n_sms,
+                                 last ? 0 : ovl_scan_ctas, s2, last ? 8 : ovl_scan_unroll));
       end_on(m, s2);
+      if (pc) {
+        ++launches;
+        st_acc.launches[MAP_K_OTHER]++;
+        CK(mapc_launch_comp_to_sf(cb, pc, ch.phase_hi - ch.phase_lo + 1, L.w_array, L.w_block, L.w_index, s2));
+      }
       if (i + NT < mine.size()) {
         // cleared for its next user, chunk i+NT, whose table may be larger
         const Chunk& nx = P.chunks[mine[i + NT]];
@@ -1117,7 +1189,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
           CK(cudaStreamWaitEvent(s3, ev_scanned[t], 0));
         }
         m = begin_on(MAP_K_CLEAR, s3);
-        CK(mapc_launch_table_clear(tb, nx.cells * nx.cell_bytes, n_sms, ovl_clear_ctas, s3));
+        CK(mapc_launch_table_clear(tb, dcells(nx, gen_mode) * nx.cell_bytes, n_sms, ovl_clear_ctas, s3));
         end_on(m, s3);
         CK(cudaEventRecord(ev_cleared[t], s3));
       }
@@ -1152,8 +1224,8 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
                          (use_unit(ch, ex->flags, gen_mode) ? " unit" : use_direct(ch, ex->flags) ? " direct" : " keys"));
     const MapcLayout L = effective_layout(ch, ex->flags);
     CK(mapc_upload_ops((const MapcOp*)(stage + ch.stage_ops), ch.ops.size(), s));
-    CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, ch.segs.size() * sizeof(MapcSeg), cudaMemcpyHostToDevice, s));
-    h2d += ch.ops.size() * sizeof(MapcOp) + ch.segs.size() * sizeof(MapcSeg);
+    CK(cudaMemcpyAsync(segs, stage + ch.stage_segs, seg_blob(ch), cudaMemcpyHostToDevice, s));
+    h2d += ch.ops.size() * sizeof(MapcOp) + seg_blob(ch);
     size_t m = begin(MAP_K_OTHER);
     CK(mapc_launch_chunk_init(ctrl, ch.dense_total, s));
     end(m);
@@ -1183,7 +1255,10 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
     if (use_direct(ch, ex->flags)) {
       // sort-free direct-address detect (direct.cu): clear the table, fold every
       // access into its cell, scan the table, re-emit the witness cell's keys
-      const uint64_t tbytes = ch.cells * ch.cell_bytes;
+      const uint64_t tbytes = dcells(ch, gen_mode) * ch.cell_bytes;
+      const auto* pc = comp_on(ch, gen_mode)
+                           ? reinterpret_cast<const unsigned long long*>(reinterpret_cast<unsigned char*>(segs) + pcomp_off(ch))
+                           : nullptr;
       m = begin(MAP_K_CLEAR);
       CK(mapc_launch_table_clear(dtab, tbytes, n_sms, 0, s));
       end(m);
@@ -1191,15 +1266,20 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         m = begin(MAP_K_DIRECT);
         if (gen_mode == 1)
           CK(mapj::launch_chunk(P.jit[MAPC_MODE_DIRECT], c, segs, (int)ch.segs.size(), ch.total_tiles,
-                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s));
+                                (unsigned long long*)dtab, &ctrl->n, &ctrl->err, L.cap, &ctrl->wit_sf, n_sms, 0, s, pc));
         else
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, 0, 0, MAPC_MODE_DIRECT, dtab, ch.cell_bytes, s));
         end(m);
       }
       m = begin(MAP_K_DETECT);
-      CK(mapc_launch_direct_scan(dtab, ch.cells, ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s, 8));
+      CK(mapc_launch_direct_scan(dtab, dcells(ch, gen_mode), ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s, 8));
       end(m);
+      if (pc) {
+        ++launches;
+        st_acc.launches[MAP_K_OTHER]++;
+        CK(mapc_launch_comp_to_sf(ctrl, pc, ch.phase_hi - ch.phase_lo + 1, L.w_array, L.w_block, L.w_index, s));
+      }
       m = begin(MAP_K_OTHER);
       launches += 2;
       st_acc.launches[MAP_K_OTHER] += 2;
@@ -1377,7 +1457,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       // direct path: the fused generate reads and writes every cell of the
       // table once (the per-access reductions happen in L2), the clear writes
       // it and the scan reads it
-      const uint64_t tbytes = P.chunks[c].cells * P.chunks[c].cell_bytes;
+      const uint64_t tbytes = dcells(P.chunks[c], gen_mode) * P.chunks[c].cell_bytes;
       st_acc.bytes[MAP_K_DIRECT] += 2 * tbytes;
       st_acc.bytes[MAP_K_CLEAR] += tbytes;
       st_acc.bytes[MAP_K_DETECT] += tbytes;

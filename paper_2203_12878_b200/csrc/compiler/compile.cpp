@@ -111,7 +111,12 @@ struct Val {
   Interval iv;
   bool is_const = false;
   uint64_t c = 0;
+  uint32_t kb = 0;       // known low bits: value mod 2^kb == kv (64 for constants)
+  uint64_t kv = 0;
 };
+
+inline uint64_t low_mask(uint32_t k) { return k >= 64 ? ~0ull : ((1ull << k) - 1); }
+inline uint32_t ctz64(uint64_t x) { return x ? (uint32_t)__builtin_ctzll(x) : 64u; }
 
 struct SIns {
   uint8_t code;
@@ -182,6 +187,8 @@ class Lowerer {
   uint64_t max_value_ = 0;
   Interval index_hull_{kU64, 0};
   uint32_t n_emits_ = 0;
+  std::vector<uint32_t> emit_kb_;
+  std::vector<uint64_t> emit_kv_;
 
   int fresh(Interval iv) {
     vals_.push_back(Val{iv, false, 0});
@@ -190,9 +197,26 @@ class Lowerer {
   int konst(uint64_t c) {
     auto it = consts_.find(c);
     if (it != consts_.end()) return it->second;
-    vals_.push_back(Val{{c, c}, true, c});
+    vals_.push_back(Val{{c, c}, true, c, 64u, c});
     consts_[c] = (int)vals_.size() - 1;
     return (int)vals_.size() - 1;
+  }
+  // known low bits of a result (a CSE hit returns a value with the same bits)
+  int kbits(int d, uint32_t kb, uint64_t kv) {
+    if (d >= 0 && !isc(d)) {
+      vals_[d].kb = std::min<uint32_t>(kb, 64u);
+      vals_[d].kv = kv & low_mask(vals_[d].kb);
+    }
+    return d;
+  }
+  // a * b mod 2^k: x_i = v_i + 2^k_i m_i, so x1 x2 = v1 v2 + 2^k1 m1 v2 + 2^k2 m2 v1 + 2^(k1+k2) m1 m2
+  int kbits_mul(int d, int a, int b) {
+    const uint32_t k1 = vals_[a].kb, k2 = vals_[b].kb;
+    const uint64_t v1 = vals_[a].kv, v2 = vals_[b].kv;
+    const uint64_t t1 = (k1 >= 64 || v2 == 0) ? 64 : (uint64_t)k1 + ctz64(v2);
+    const uint64_t t2 = (k2 >= 64 || v1 == 0) ? 64 : (uint64_t)k2 + ctz64(v1);
+    const uint64_t t3 = (uint64_t)k1 + k2;
+    return kbits(d, (uint32_t)std::min<uint64_t>({t1, t2, t3, 64}), v1 * v2);
   }
   bool isc(int v) const { return vals_[v].is_const; }
   uint64_t cv(int v) const { return vals_[v].c; }
@@ -236,20 +260,24 @@ class Lowerer {
         if (ca && cb) return konst(checked((u128)cv(a) + cv(b), "+"));
         if (ca && cv(a) == 0) return b;
         if (cb && cv(b) == 0) return a;
-        return emit_op(VM_ADD, a, b, {A.lo + B.lo, checked((u128)A.hi + B.hi, "+")}, false);
-      case BinOp::Sub:
+        return kbits(emit_op(VM_ADD, a, b, {A.lo + B.lo, checked((u128)A.hi + B.hi, "+")}, false),
+                     std::min(vals_[a].kb, vals_[b].kb), vals_[a].kv + vals_[b].kv);
+      case BinOp::Sub: {
         if (ca && cb) return konst(cv(a) > cv(b) ? cv(a) - cv(b) : 0);
         if (cb && cv(b) == 0) return a;
-        return emit_op(VM_SUB, a, b, {A.lo > B.hi ? A.lo - B.hi : 0, A.hi > B.lo ? A.hi - B.lo : 0}, false);
+        const int d = emit_op(VM_SUB, a, b, {A.lo > B.hi ? A.lo - B.hi : 0, A.hi > B.lo ? A.hi - B.lo : 0}, false);
+        // monus: exact subtraction (and its congruence) only when it never saturates
+        return A.lo >= B.hi ? kbits(d, std::min(vals_[a].kb, vals_[b].kb), vals_[a].kv - vals_[b].kv) : d;
+      }
       case BinOp::Mul: {
         if (ca && cb) return konst(checked((u128)cv(a) * cv(b), "*"));
         if ((ca && cv(a) == 0) || (cb && cv(b) == 0)) return konst(0);
         if (ca && cv(a) == 1) return b;
         if (cb && cv(b) == 1) return a;
         Interval r{A.lo * B.lo, checked((u128)A.hi * B.hi, "*")};
-        if (cb && is_pow2(cv(b))) return emit_op(VM_SHL, a, konst(log2u(cv(b))), r, false);
-        if (ca && is_pow2(cv(a))) return emit_op(VM_SHL, b, konst(log2u(cv(a))), r, false);
-        return emit_op(VM_MUL, a, b, r, false);
+        if (cb && is_pow2(cv(b))) return kbits_mul(emit_op(VM_SHL, a, konst(log2u(cv(b))), r, false), a, b);
+        if (ca && is_pow2(cv(a))) return kbits_mul(emit_op(VM_SHL, b, konst(log2u(cv(a))), r, false), a, b);
+        return kbits_mul(emit_op(VM_MUL, a, b, r, false), a, b);
       }
       case BinOp::Div: {
         if (cb && cv(b) != 0) {
@@ -271,7 +299,8 @@ class Lowerer {
           if (d == 1) return konst(0);
           if (A.hi < d) return a;                        // identity on [0, d)
           Interval r{0, std::min(A.hi, d - 1)};
-          if (is_pow2(d)) return emit_op(VM_BAND, a, -1, r, false, d - 1);
+          if (is_pow2(d))
+            return kbits(emit_op(VM_BAND, a, -1, r, false, d - 1), std::min(vals_[a].kb, log2u(d)), vals_[a].kv);
           return emit_op(VM_MOD, a, b, r, false);
         }
         bool may0 = B.lo == 0;
@@ -284,7 +313,9 @@ class Lowerer {
         if (ca && cv(a) == 0) return konst(0);
         uint64_t lo = (A.lo == 0) ? 0 : (B.lo >= 64 ? kU64 : shl_checked(A.lo, B.lo, "<<"));
         Interval r{lo, shl_checked(A.hi, B.hi, "<<")};
-        return emit_op(VM_SHL, a, b, r, false);
+        const int d = emit_op(VM_SHL, a, b, r, false);
+        if (cb && cv(b) < 64) return kbits(d, vals_[a].kb + (uint32_t)cv(b), vals_[a].kv << cv(b));
+        return d;
       }
       case BinOp::Shr: {
         if (ca && cb) return konst(cv(b) >= 64 ? 0 : cv(a) >> cv(b));
@@ -518,6 +549,8 @@ class Lowerer {
           e.emit_aux = ((uint32_t)st.array << 1) | (st.write ? 1u : 0u);
           ins_.push_back(e);
           ++n_emits_;
+          emit_kb_.push_back(vals_[ix].kb);
+          emit_kv_.push_back(vals_[ix].kv);
           index_hull_.lo = std::min(index_hull_.lo, iv(ix).lo);
           index_hull_.hi = std::max(index_hull_.hi, iv(ix).hi);
         } else if (here && fault_owner_ && expr_may_fault(st.index)) {
@@ -607,6 +640,8 @@ class Lowerer {
       x = bin(BinOp::Add, t, lo);
     } else {
       x = emit_op(VM_MADK, lo, sp, {L.lo, std::max(L.lo, xhi)}, false, 0, k_[d]);
+      // lo + k * step: the step's trailing zeros (k unknown) and lo's known bits
+      if (isc(sp)) kbits(x, std::min<uint32_t>(vals_[lo].kb, cv(sp) ? ctz64(cv(sp)) : 64u), vals_[lo].kv);
     }
     int var = st.var;
     xval_[var] = x;
@@ -751,6 +786,8 @@ class Lowerer {
     out->has_emit = n_emits_ > 0;
     out->dense = out->has_emit && !any_fault && !any_act;
     out->index = n_emits_ ? index_hull_ : Interval{0, 0};
+    out->site_kb = emit_kb_;
+    out->site_kv = emit_kv_;
     has_fault_ = any_fault;
   }
 

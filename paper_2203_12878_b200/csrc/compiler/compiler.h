@@ -41,6 +41,12 @@ struct GroupProg {
   // consecutive tuples (a warp) touch the fewest 32-byte sectors of cells
   // (choose_tuple_order); any order enumerates the same accesses.
   bool tid_inner = false;
+  // Per access site (EMIT order): the index's known low bits -- index mod 2^site_kb
+  // == site_kv for every tuple (a congruence proved during lowering; 0 = nothing
+  // known).  The direct table of a phase whose sites share a residue modulo 2^k is
+  // compressed by 2^k.
+  std::vector<uint32_t> site_kb;
+  std::vector<uint64_t> site_kv;
 };
 
 struct InstanceInfo {

@@ -135,6 +135,27 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
   }
 }
 
+// Stride-compressed table (mapcheck.cpp Chunk::pcomp): the scan's smallest racy cell
+// index back to its sort field -- local phase q = the last block base <= the index,
+// (array, block) from the index's high bits within the block, index - idx_lo = the low
+// bits * 2^sh + residue.  The map is monotone, so the smallest racy cell is the smallest
+// racy sort field.
+__global__ void k_comp_to_sf(MapcCtrl* __restrict__ ctrl, const unsigned long long* __restrict__ pcomp, uint32_t nph,
+                             uint32_t wa, uint32_t wb, uint32_t wi) {
+  const unsigned long long t = ctrl->racy_sf;
+  if (t == ~0ull) return;
+  uint32_t q = 0;
+  for (uint32_t i = 1; i < nph; ++i)
+    if (pcomp[2 * i] <= t) q = i;
+  const unsigned long long off = t - pcomp[2 * q];
+  const uint32_t sh = (uint32_t)(pcomp[2 * q + 1] & 255ull);
+  const unsigned long long res = pcomp[2 * q + 1] >> 8;
+  const uint32_t bits = wi - sh;
+  const unsigned long long sub = off >> bits;                    // (array << wb) | local block
+  const unsigned long long idx = ((off & ((1ull << bits) - 1ull)) << sh) + res;
+  ctrl->racy_sf = ((unsigned long long)q << (wa + wb + wi)) | (sub << wi) | idx;
+}
+
 // Canonical witness of the smallest racy cell from its keys (all with sf =
 // ctrl->racy_sf, in arrival order, ctrl->nf of them; filter-mode generate).
 constexpr int WF_THREADS = 512;
@@ -230,6 +251,12 @@ extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long lo
   else
     mapk::k_direct_scan<unsigned long long>
         <<<grid, mapk::DS_THREADS, 0, s>>>((const unsigned long long*)tab, cells, w_tid, ctrl);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t mapc_launch_comp_to_sf(MapcCtrl* ctrl, const unsigned long long* pcomp, uint32_t nph,
+                                              uint32_t wa, uint32_t wb, uint32_t wi, cudaStream_t s) {
+  mapk::k_comp_to_sf<<<1, 1, 0, s>>>(ctrl, pcomp, nph, wa, wb, wi);
   return cudaGetLastError();
 }
 

@@ -256,3 +256,30 @@ def random_rows_instance(seed: int) -> Instance:
         src += ";\nsync;\nforU r in 0..R { forU c in 0..C { " + "; ".join(reversed(sites)) + " } }"
     return Instance(f"rows{seed}", src, grid=(r.choice([1, 2]), 1, 1), block=(nt, 1, 1),
                     params={"R": R, "C": C, "H": H})
+
+
+def random_strided_instance(seed: int) -> Instance:
+    """A random MAP whose sites index with a power-of-two stride (index = s * (k * nt
+    + tid + a) + b, same or different residues b, per-phase strides, guards): the
+    shapes for which the direct table is stride-compressed.  Test input only."""
+    r = random.Random(20_000 + seed)
+    nt = r.choice([8, 16, 32, 64])
+    N = r.choice([4, 16, 64])
+    phases = []
+    for _ in range(r.randint(1, 3)):
+        s = r.choice([2, 4, 8, 16])
+        base = r.randrange(s)
+        sites = []
+        for _ in range(r.randint(1, 4)):
+            kind = r.choice(["rd", "rd", "wr"])
+            arr = r.choice(["A", "A", "B"])
+            a = r.choice([0, 0, 1, nt - 1])
+            b = base if r.random() < 0.8 else r.randrange(s)
+            t = r.choice(["tid", "tid", "(tid / 2)", "((tid + 1) % " + str(nt) + ")"])
+            acc = f"{kind} {arr}[{s} * (k * {nt} + {t} + {a}) + {b}]"
+            if r.random() < 0.2:
+                acc = f"if (k < {r.randint(1, N)}) {{ {acc} }} else {{ skip }}"
+            sites.append(acc)
+        phases.append("forU k in 0..N { " + "; ".join(sites) + " }")
+    src = "params N; shared A, B;\n" + ";\nsync;\n".join(phases)
+    return Instance(f"strided{seed}", src, grid=(r.choice([1, 2]), 1, 1), block=(nt, 1, 1), params={"N": N})
