@@ -1805,7 +1805,11 @@ size_t map_debug_dump(const map_program* p, char* buf, size_t cap) {
       out += "instance " + std::to_string(i) + " phase " + std::to_string(in.phase) + " group " + std::to_string(g) +
              " levels " + std::to_string(G.n_levels) + " trips";
       for (uint32_t l = 0; l < G.n_levels; ++l) out += " " + std::to_string(G.trips[l]);
-      out += std::string(G.dense ? " dense" : "") + (G.tid_inner ? " tid_inner" : "") + " emits " + std::to_string(G.n_emits) + "\n";
+      out += std::string(G.dense ? " dense" : "") + (G.tid_inner ? " tid_inner" : "") + " emits " + std::to_string(G.n_emits);
+      // per site: index mod 2^kb == kv (the known low bits behind the stride compression)
+      for (size_t e = 0; e < G.site_kb.size(); ++e)
+        out += " known" + std::to_string(e) + "=" + std::to_string(G.site_kb[e]) + ":" + std::to_string(G.site_kv[e]);
+      out += "\n";
       for (const MapcOp& op : G.ops) {
         const uint32_t c = op.code & MAPC_CODE_MASK;
         out += "  r" + std::to_string(op.dst) + " = " + (c <= VM_NOP ? names[c] : "?") + " ";

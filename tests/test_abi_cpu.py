@@ -253,3 +253,39 @@ def test_python_flag_constants_match_header():
     import ctypes
     assert [f for f, _ in mc._Stats._fields_] == ["ms", "launches", "bytes", "timed"]
     assert ctypes.sizeof(mc._Stats) == 10 * (4 + 4 + 8 + 4)
+
+
+def test_known_low_bits_are_sound():
+    """The compiler's known low bits of every access site (map_debug_dump "knownE=kb:kv",
+    the basis of the stride-compressed direct table): every index the site produces,
+    evaluated independently here, is congruent to kv modulo 2^kb -- on random strided
+    MAPs (workloads.fuzz.random_strided_instance) and the Blelloch configs' closed forms."""
+    from workloads import fuzz
+    checked = 0
+    for seed in range(40):
+        inst = fuzz.random_strided_instance(seed)
+        p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+        known = [[tuple(int(x) for x in m.split(":")) for m in re.findall(r"known\d+=(\d+:\d+)", line)]
+                 for line in p.dump().splitlines() if line.startswith("instance")]
+        phases = inst.src.split("params N; shared A, B;\n", 1)[1].split(";\nsync;\n")
+        assert len(known) == len(phases), (seed, len(known), len(phases))
+        nt, N = inst.block[0], inst.params["N"]
+        for ph, sites in zip(phases, known):
+            idx = re.findall(r"(?:rd|wr) [AB]\[([^\[\]]*)\]", ph)
+            assert len(idx) == len(sites), (seed, ph)
+            for text, (kb, kv) in zip(idx, sites):
+                expr = text.replace("/", "//")
+                mod = 1 << min(kb, 64)
+                for tid in range(nt):
+                    for k in range(N):
+                        v = eval(expr, {"tid": tid, "k": k})
+                        assert v % mod == kv % mod, (seed, text, kb, kv, tid, k, v)
+                        checked += 1
+    assert checked > 10000
+    # Blelloch up-sweep phase l (1-based): (2^(l-1)) * (2m + 1) - 1 and (2^(l-1)) * (2m + 2) - 1
+    inst = config("4c", n=1 << 10, bs=64)
+    p = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+    lines = [l for l in p.dump().splitlines() if l.startswith("instance")]
+    for l in range(1, 8):
+        kb = [tuple(int(x) for x in m.split(":")) for m in re.findall(r"known\d+=(\d+:\d+)", lines[l])]
+        assert kb[0] == (l, (1 << (l - 1)) - 1) and kb[1] == (l, (1 << l) - 1), (l, kb)
