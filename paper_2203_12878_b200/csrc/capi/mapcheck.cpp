@@ -36,13 +36,12 @@ cudaError_t mapc_launch_generate(const MapcSeg* segs, int n_segs, unsigned long 
                                  uint32_t max_emits, uint32_t force_compact, uint32_t mode, void* tab,
                                  uint32_t cell_bytes, cudaStream_t s);
 cudaError_t mapc_launch_table_clear(void* tab, unsigned long long bytes, int n_sms, int ctas_per_sm, cudaStream_t s);
-cudaError_t mapc_launch_comp_to_sf(MapcCtrl* ctrl, const unsigned long long* pcomp, uint32_t nph, uint32_t wa,
-                                   uint32_t wb, uint32_t wi, cudaStream_t s);
 cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long long cells, uint32_t cell_bytes, uint32_t w_tid,
                                     MapcCtrl* ctrl, int n_sms, int ctas_per_sm, cudaStream_t s, int unroll);
-cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s);
+cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi, cudaStream_t s,
+                                     const unsigned long long* pcomp, uint32_t nph, uint32_t wa, uint32_t wb, uint32_t wi);
 cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits, uint32_t w_tid,
-                                     unsigned long long cap, cudaStream_t s);
+                                     unsigned long long cap, cudaStream_t s, MapcChunkResult* out);
 int mapc_bucket_max_world();
 cudaError_t mapc_launch_bucket_count(const unsigned long long* keys, const MapcCtrl* ctrl, uint32_t pay_bits,
                                      uint32_t world, unsigned long long* counts, int n_sms, cudaStream_t s);
@@ -1176,11 +1175,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       CK(mapc_launch_direct_scan(tb, dcells(ch, gen_mode), ch.cell_bytes, L.w_tid, cb, n_sms,
                                  last ? 0 : ovl_scan_ctas, s2, last ? 8 : ovl_scan_unroll));
       end_on(m, s2);
-      if (pc) {
-        ++launches;
-        st_acc.launches[MAP_K_OTHER]++;
-        CK(mapc_launch_comp_to_sf(cb, pc, ch.phase_hi - ch.phase_lo + 1, L.w_array, L.w_block, L.w_index, s2));
-      }
+
       if (i + NT < mine.size()) {
         // cleared for its next user, chunk i+NT, whose table may be larger
         const Chunk& nx = P.chunks[mine[i + NT]];
@@ -1193,18 +1188,18 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
         end_on(m, s3);
         CK(cudaEventRecord(ev_cleared[t], s3));
       }
-      m = begin_on(MAP_K_OTHER, s2);
-      launches += 2;
-      st_acc.launches[MAP_K_OTHER] += 2;
-      CK(mapc_launch_witness_gate(cb, gate, ch.phase_lo, ch.phase_hi, s2));
+      m = begin_on(MAP_K_OTHER, s2);                  // gate (+ compressed-cell mapping) and witness + result
+      launches += 1;
+      st_acc.launches[MAP_K_OTHER] += 1;
+      CK(mapc_launch_witness_gate(cb, gate, ch.phase_lo, ch.phase_hi, s2, pc, ch.phase_hi - ch.phase_lo + 1,
+                                  L.w_array, L.w_block, L.w_index));
       if (ch.total_tiles) {
         ++launches;
         st_acc.launches[MAP_K_OTHER]++;
         CK(mapj::launch_chunk(P.jit[MAPC_MODE_FILTER], c, sg, (int)ch.segs.size(), ch.total_tiles, bufA, &cb->nf,
                               &cb->err, L.cap, &cb->wit_sf, n_sms, 0, s2));
       }
-      CK(mapc_launch_witness_flat(bufA, cb, L.pay_bits, L.w_tid, L.cap, s2));
-      CK(mapc_launch_chunk_finish(cb, 0, res + c, s2));
+      CK(mapc_launch_witness_flat(bufA, cb, L.pay_bits, L.w_tid, L.cap, s2, res + c));
       end_on(m, s2);
       CK(cudaEventRecord(ev_done[b], s2));
     }
@@ -1238,17 +1233,16 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
                             ch.jit.unit_cluster, ch.jit.unit_threads, ch.unit_smem, n_sms, s));
       end(m);
       m = begin(MAP_K_OTHER);
-      launches += 2;
-      st_acc.launches[MAP_K_OTHER] += 2;
-      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s));
+      launches += 1;
+      st_acc.launches[MAP_K_OTHER] += 1;
+      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s, nullptr, 0, 0, 0, 0));
       if (ch.total_tiles) {
         ++launches;
         st_acc.launches[MAP_K_OTHER]++;
         CK(mapj::launch_unit_filter(P.jit[MAPC_MODE_UNITF], c, &ctrl->wit_sf, bufA, &ctrl->nf, L.cap, &ctrl->err,
                                     (ch.bound + n_units - 1) / std::max<uint64_t>(n_units, 1), n_sms, s));
       }
-      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s));
-      CK(mapc_launch_chunk_finish(ctrl, 0, res + c, s));
+      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s, res + c));
       end(m);
       continue;
     }
@@ -1275,15 +1269,11 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
       m = begin(MAP_K_DETECT);
       CK(mapc_launch_direct_scan(dtab, dcells(ch, gen_mode), ch.cell_bytes, L.w_tid, ctrl, n_sms, 0, s, 8));
       end(m);
-      if (pc) {
-        ++launches;
-        st_acc.launches[MAP_K_OTHER]++;
-        CK(mapc_launch_comp_to_sf(ctrl, pc, ch.phase_hi - ch.phase_lo + 1, L.w_array, L.w_block, L.w_index, s));
-      }
       m = begin(MAP_K_OTHER);
-      launches += 2;
-      st_acc.launches[MAP_K_OTHER] += 2;
-      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s));
+      launches += 1;
+      st_acc.launches[MAP_K_OTHER] += 1;
+      CK(mapc_launch_witness_gate(ctrl, gate, ch.phase_lo, ch.phase_hi, s, pc, ch.phase_hi - ch.phase_lo + 1,
+                                  L.w_array, L.w_block, L.w_index));
       if (ch.total_tiles) {
         ++launches;
         st_acc.launches[MAP_K_OTHER]++;
@@ -1294,8 +1284,7 @@ map_status map_check_races(map_program* p, const map_exec* ex, map_result* out) 
           CK(mapc_launch_generate(segs, (int)ch.segs.size(), 0, ch.total_tiles, &L, p->C.u32_mode ? 1 : 0, bufA, ctrl,
                                   n_sms, ch.nreg, MAPC_MAX_EMITS, 0, MAPC_MODE_FILTER, nullptr, ch.cell_bytes, s));
       }
-      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s));
-      CK(mapc_launch_chunk_finish(ctrl, 0, res + c, s));
+      CK(mapc_launch_witness_flat(bufA, ctrl, L.pay_bits, L.w_tid, L.cap, s, res + c));
       end(m);
       continue;
     }

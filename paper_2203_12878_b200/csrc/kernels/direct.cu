@@ -140,8 +140,8 @@ k_direct_scan(const C* __restrict__ tab, unsigned long long cells, uint32_t wt, 
 // (array, block) from the index's high bits within the block, index - idx_lo = the low
 // bits * 2^sh + residue.  The map is monotone, so the smallest racy cell is the smallest
 // racy sort field.
-__global__ void k_comp_to_sf(MapcCtrl* __restrict__ ctrl, const unsigned long long* __restrict__ pcomp, uint32_t nph,
-                             uint32_t wa, uint32_t wb, uint32_t wi) {
+__device__ __forceinline__ void comp_to_sf(MapcCtrl* __restrict__ ctrl, const unsigned long long* __restrict__ pcomp,
+                                           uint32_t nph, uint32_t wa, uint32_t wb, uint32_t wi) {
   const unsigned long long t = ctrl->racy_sf;
   if (t == ~0ull) return;
   uint32_t q = 0;
@@ -160,34 +160,50 @@ __global__ void k_comp_to_sf(MapcCtrl* __restrict__ ctrl, const unsigned long lo
 // ctrl->racy_sf, in arrival order, ctrl->nf of them; filter-mode generate).
 constexpr int WF_THREADS = 512;
 __global__ void __launch_bounds__(WF_THREADS)
+// (out != nullptr: then also the chunk's result record -- what k_chunk_finish writes for
+// a chunk without radix passes -- one launch less per chunk)
 k_witness_flat(const unsigned long long* __restrict__ keys, MapcCtrl* __restrict__ ctrl, uint32_t pay_bits,
-               uint32_t w_tid, unsigned long long cap) {
+               uint32_t w_tid, unsigned long long cap, MapcChunkResult* __restrict__ out) {
   const unsigned long long target = ctrl->wit_sf;
-  if (target == ~0ull) return;
   const unsigned long long n = ctrl->nf;
-  if (n > cap) {
-    if (threadIdx.x == 0) atomicOr(&ctrl->err, MAPC_ERR_CAPACITY);
-    return;
-  }
-  const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
-  __shared__ St part[WF_THREADS];
-  St s;
-  st_init(s);
-  for (unsigned long long i = threadIdx.x; i < n; i += WF_THREADS) {
-    const unsigned long long key = keys[i];
-    if ((key >> pay_bits) != target) {          // library bug guard: the filter let a foreign key through
-      atomicOr(&ctrl->err, MAPC_ERR_LAYOUT);
-      continue;
+  const bool work = target != ~0ull && n <= cap;            // uniform over the block
+  if (target != ~0ull && n > cap && threadIdx.x == 0) atomicOr(&ctrl->err, MAPC_ERR_CAPACITY);
+  if (work) {
+    const uint32_t tmask = w_tid >= 32 ? 0xFFFFFFFFu : ((1u << w_tid) - 1u);
+    __shared__ St part[WF_THREADS];
+    St s;
+    st_init(s);
+    for (unsigned long long i = threadIdx.x; i < n; i += WF_THREADS) {
+      const unsigned long long key = keys[i];
+      if ((key >> pay_bits) != target) {          // library bug guard: the filter let a foreign key through
+        atomicOr(&ctrl->err, MAPC_ERR_LAYOUT);
+        continue;
+      }
+      st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
     }
-    st_add(s, (uint32_t)(key >> 1) & tmask, 1u << (key & 1u));
-  }
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int h = WF_THREADS / 2; h; h >>= 1) {
-    if (threadIdx.x < h) st_merge(part[threadIdx.x], part[threadIdx.x + h]);
+    part[threadIdx.x] = s;
     __syncthreads();
+    for (int h = WF_THREADS / 2; h; h >>= 1) {
+      if (threadIdx.x < h) st_merge(part[threadIdx.x], part[threadIdx.x + h]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) ctrl->witness = st_witness(part[0], target, w_tid);
   }
-  if (threadIdx.x == 0) ctrl->witness = st_witness(part[0], target, w_tid);
+  if (out) {
+    __syncthreads();                              // every thread's err bits are in
+    if (threadIdx.x == 0) {
+      __threadfence_block();
+      MapcChunkResult r;
+      r.n = ctrl->n;
+      r.witness = ctrl->witness;
+      r.racy = ctrl->racy;
+      r.err = atomicOr(&ctrl->err, 0u);
+      r.active_passes = 0;
+      r.table_reads = 0;
+      r.active_mask = 0;
+      *out = r;
+    }
+  }
 }
 
 // Which racy chunk folds a witness.  The canonical witness is the minimum over
@@ -196,8 +212,12 @@ k_witness_flat(const unsigned long long* __restrict__ keys, MapcCtrl* __restrict
 // chunk whose phases all exceed ph_hi cannot hold the minimum, so its filter
 // pass is skipped (its racy count still counts).  *gate = the smallest ph_hi
 // of a racy chunk so far (UINT32_MAX = none; reset once per run).
+// (pcomp != nullptr: the chunk's table was stride-compressed -- the scan's smallest racy
+// cell is mapped back to its sort field first, comp_to_sf)
 __global__ void k_witness_gate(MapcCtrl* __restrict__ ctrl, uint32_t* __restrict__ gate, uint32_t ph_lo,
-                               uint32_t ph_hi) {
+                               uint32_t ph_hi, const unsigned long long* __restrict__ pcomp, uint32_t nph, uint32_t wa,
+                               uint32_t wb, uint32_t wi) {
+  if (pcomp) comp_to_sf(ctrl, pcomp, nph, wa, wb, wi);
   const unsigned long long sf = ctrl->racy_sf;
   if (sf == ~0ull) return;
   if (*gate < ph_lo) return;
@@ -227,8 +247,9 @@ extern "C" cudaError_t mapc_launch_table_clear(void* tab, unsigned long long byt
 }
 
 extern "C" cudaError_t mapc_launch_witness_gate(MapcCtrl* ctrl, uint32_t* gate, uint32_t ph_lo, uint32_t ph_hi,
-                                                cudaStream_t s) {
-  mapk::k_witness_gate<<<1, 1, 0, s>>>(ctrl, gate, ph_lo, ph_hi);
+                                                cudaStream_t s, const unsigned long long* pcomp, uint32_t nph,
+                                                uint32_t wa, uint32_t wb, uint32_t wi) {
+  mapk::k_witness_gate<<<1, 1, 0, s>>>(ctrl, gate, ph_lo, ph_hi, pcomp, nph, wa, wb, wi);
   return cudaGetLastError();
 }
 
@@ -254,15 +275,10 @@ extern "C" cudaError_t mapc_launch_direct_scan(const void* tab, unsigned long lo
   return cudaGetLastError();
 }
 
-extern "C" cudaError_t mapc_launch_comp_to_sf(MapcCtrl* ctrl, const unsigned long long* pcomp, uint32_t nph,
-                                              uint32_t wa, uint32_t wb, uint32_t wi, cudaStream_t s) {
-  mapk::k_comp_to_sf<<<1, 1, 0, s>>>(ctrl, pcomp, nph, wa, wb, wi);
-  return cudaGetLastError();
-}
-
 extern "C" cudaError_t mapc_launch_witness_flat(const unsigned long long* keys, MapcCtrl* ctrl, uint32_t pay_bits,
-                                                uint32_t w_tid, unsigned long long cap, cudaStream_t s) {
-  mapk::k_witness_flat<<<1, mapk::WF_THREADS, 0, s>>>(keys, ctrl, pay_bits, w_tid, cap);
+                                                uint32_t w_tid, unsigned long long cap, cudaStream_t s,
+                                                MapcChunkResult* out) {
+  mapk::k_witness_flat<<<1, mapk::WF_THREADS, 0, s>>>(keys, ctrl, pay_bits, w_tid, cap, out);
   return cudaGetLastError();
 }
 
