@@ -480,6 +480,13 @@ def main():
     # e2e: the public API from host text to host verdict, every step (compile + H2D bytecode + D2H result)
     e2e = None
     if not args.no_e2e:
+        # warm-up of the end-to-end leg itself (first-use costs of a fresh program in
+        # this process: pinned staging buffer, side streams, events -- pooled after)
+        for _ in range(max(args.warmup, 1)):
+            p2 = mc.MapProgram(inst.src, inst.grid, inst.block, inst.params)
+            p2.check_races(scratch=scratch, stream=stream, chunk_max_accesses=args.chunk, rank=rank, world=world,
+                           detect=args.detect)
+            del p2
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
