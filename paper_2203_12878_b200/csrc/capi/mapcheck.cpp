@@ -399,7 +399,7 @@ void emit_chunk(const mapc::Compiled& C, const std::vector<PhaseInfo>& ph, size_
   // stride compression of the direct table: per local phase, the largest 2^k such
   // that every site's (index - idx_lo) has the same residue modulo 2^k (the compiler's
   // known low bits, GroupProg::site_kb/kv)
-  {
+  if (L.sort_bits <= 31) {                   // 32-bit cell indices only (the compressed path's arithmetic)
     const uint32_t nph = ch.phase_hi - ch.phase_lo + 1;
     const uint32_t WI = L.w_index, WAB = L.w_array + L.w_block;
     std::vector<int> k(nph, -1);                 // -1: no site yet
